@@ -1,0 +1,193 @@
+"""Pins of the oracle's segmental refinement (fig:fmgsr / fig:mgvsr).
+
+What fixes SR independently of the oracle's own arithmetic:
+  * the region definitions of PAPER.md:187-214, evaluated by brute force on cell sets;
+  * equivalences: C = Omega on every level (huge buffer) and a single segment must give
+    conventional FMG exactly (north_star; SPEC sr examples);
+  * symmetry: a symmetric f on a symmetric segment grid gives a symmetric u;
+  * the paper's trends: e_r decreases with the buffer and with larger
+    transition subdomains pN0V;
+  * frozen GSR cells: never changed by a smoother.
+The e_r VALUES of Tables 1-3 belong to a 27-point stencil on [0,2]x[0,1]^2: parity unpinned.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from oracle import Box, Config, Oracle
+
+
+def _cells(box):
+    return set(box.cells())
+
+
+def _linf_grow(cells, j):
+    out = set()
+    for c in cells:
+        for o in itertools.product(range(-j, j + 1), repeat=3):
+            out.add((c[0] + o[0], c[1] + o[1], c[2] + o[2]))
+    return out
+
+
+@pytest.mark.parametrize("J", [0, 1, 2, 3, 4])
+def test_regions_match_set_definitions(J):
+    cfg = Config(n=(16, 16, 16), M=4, seg=8, buffer=J, K=2)
+    o = Oracle(cfg)
+    for l in range(o.T + 1, o.M + 1):
+        S = o.S_l(l)
+        omega = _cells(o.dom[l])
+        for p in o.segs:
+            V = {c for c in omega if tuple(v // S for v in c) == p}
+            assert V == _cells(o.V(l, p))
+            C = _linf_grow(V, J) & omega
+            G = _linf_grow(C, 1) - C
+            GBC, GSR = G - omega, G & omega
+            assert C == _cells(o.C(l, p))
+            assert C | GSR == _cells(o.CG(l, p))              # range of prolongation L215
+            st = _cells(o.storage(l, p))
+            assert (C | G) <= st
+            # F: coarse cells whose 8 children all lie in C_l^p
+            omc = _cells(o.dom[l - 1])
+            F = {I for I in omc
+                 if all((2 * I[0] + a, 2 * I[1] + b, 2 * I[2] + c) in C
+                        for a, b, c in itertools.product((0, 1), repeat=3))}
+            assert F == _cells(o.F(l, p))
+            # zero-communication footprint (R15): the trilinear footprint of C cup GSR lies
+            # in the segment's own level-(l-1) storage (k >= 2) ...
+            foot = set()
+            for i in C | GSR:
+                par = tuple(v // 2 for v in i)
+                s = tuple(-1 if v % 2 == 0 else 1 for v in i)
+                for a, b, c in itertools.product((0, 1), repeat=3):
+                    foot.add((par[0] + a * s[0], par[1] + b * s[1], par[2] + c * s[2]))
+            if l - 1 > o.T:
+                assert foot <= _cells(o.storage(l - 1, p))
+            # ... and reaches outside Omega_{l-1} only through depth-1 (reflected) ghosts
+            for I in foot - omc:
+                assert all(-1 <= v <= n for v, n in zip(I, o.N[l - 1]))
+        # genuine regions tile Omega_l disjointly
+        assert sum(o.V(l, p).volume for p in o.segs) == len(omega)
+
+
+def test_huge_buffer_equals_conventional_fmg():
+    # J >= N - S makes C_l^p = Omega_l on every level: SR must reproduce FMG (north_star)
+    n = (32, 32, 32)
+    f = W.manufactured_f(n, 1 / 32) + W.noise(n, 1e-2)
+    u0 = O.solve(f, Config(n=n, M=4, K=0))
+    for S, K in [(16, 2), (8, 3)]:
+        u = O.solve(f, Config(n=n, M=4, seg=S, buffer=32, K=K))
+        assert np.abs(u - u0).max() <= 1e-14 * np.abs(u0).max()
+
+
+@pytest.mark.parametrize("J", [0, 1, 2])
+def test_single_segment_equals_conventional_fmg(J):
+    n = (32, 32, 32)
+    f = W.manufactured_f(n, 1 / 32)
+    u0 = O.solve(f, Config(n=n, M=4, K=0))
+    u = O.solve(f, Config(n=n, M=4, seg=32, buffer=J, K=3))
+    assert np.abs(u - u0).max() <= 1e-14 * np.abs(u0).max()
+
+
+def test_all_levels_sr():
+    # K = M: the transition level is the coarsest grid (T = 0)
+    n = (16, 16, 16)
+    f = W.manufactured_f(n, 1 / 16)
+    u = O.solve(f, Config(n=n, M=3, seg=8, buffer=2, K=3))
+    ue = W.manufactured_u(n, 1 / 16)
+    assert np.isfinite(u).all() and np.abs(u - ue).max() < 20 * np.abs(ue).max() * 1e-2
+
+
+def test_symmetric_rhs_gives_symmetric_solution():
+    n = (32, 32, 32)
+    f = W.random_field(n, seed=11)
+    f = f + f[:, :, ::-1]                     # mirror x1
+    f = f + f[:, ::-1, :]                     # mirror x2
+    f = f + np.transpose(f, (0, 2, 1))        # swap x1 <-> x2 (keeps both mirrors)
+    u = O.solve(f, Config(n=n, M=4, seg=8, buffer=2, K=2))
+    sc = np.abs(u).max()
+    assert np.abs(u - u[:, :, ::-1]).max() <= 1e-13 * sc
+    assert np.abs(u - np.transpose(u, (0, 2, 1))).max() <= 1e-13 * sc
+
+
+def test_deterministic():
+    n = (32, 32, 32)
+    f = W.make_rhs("manufactured+noise", n)
+    cfg = Config(n=n, M=4, seg=16, buffer=2, K=2)
+    assert np.array_equal(O.solve(f, cfg), O.solve(f, cfg))
+
+
+def _err(n, M, S, J, K):
+    f = W.manufactured_f(n, 1 / n[0])
+    u = W.manufactured_u(n, 1 / n[0])
+    return np.abs(O.solve(f, Config(n=n, M=M, seg=S, buffer=J, K=K)) - u).max()
+
+
+def test_error_ratio_decreases_with_buffer():
+    # A and B "both correlate with increased accuracy" (they increase J)
+    n = (64, 64, 64)
+    e_conv = _err(n, 5, 0, 0, 0)
+    er = [_err(n, 5, 16, J, 3) / e_conv for J in (0, 1, 2, 4, 8)]
+    assert all(a > b for a, b in zip(er, er[1:])), er
+    assert er[-1] < 1.5
+
+
+def test_error_ratio_grows_as_transition_subdomain_shrinks():
+    # halving pN0V (at fixed K, J) increases e_r
+    n = (64, 64, 64)
+    e_conv = _err(n, 5, 0, 0, 0)
+    er = [_err(n, 5, S, 2, 2) / e_conv for S in (32, 16, 8)]   # pN0V = 8, 4, 2
+    assert er[0] < er[1] < er[2], er
+
+
+def test_gsr_cells_are_never_smoothed():
+    # GSR cells are set by prolongation only ("frozen")
+    n = (32, 32, 32)
+    f = W.make_rhs("manufactured+noise", n)
+    o = Oracle(Config(n=n, M=4, seg=8, buffer=2, K=2))
+    checked = [0]
+    orig = o._cheb
+
+    def spy(deg, u, b, X, l):
+        if l > o.T:
+            before = u.a.copy()
+            orig(deg, u, b, X, l)
+            inside = u.box.intersect(o.dom[l])
+            m = np.zeros(u.box.shape, bool)
+            sl = tuple(slice(a - s, c - s) for a, c, s in zip(X.lo, X.hi, u.box.lo))
+            m[sl] = True
+            ins = np.zeros(u.box.shape, bool)
+            sl2 = tuple(slice(a - s, c - s) for a, c, s in zip(inside.lo, inside.hi, u.box.lo))
+            ins[sl2] = True
+            gsr = ins & ~m
+            assert np.array_equal(before[gsr], u.a[gsr])
+            checked[0] += 1
+        else:
+            orig(deg, u, b, X, l)
+
+    o._cheb = spy
+    o.solve(f)
+    assert checked[0] > 0
+
+
+def test_sr_error_second_order_at_fixed_segment_grid():
+    # SR keeps 2nd-order accuracy; at a fixed segment grid (S = N/2) and
+    # fixed K, J the SR error ratio per halving of h tends towards 4
+    errs = [_err((N, N, N), M, N // 2, 2, 2) for N, M in ((32, 4), (64, 5), (128, 6))]
+    q = [errs[0] / errs[1], errs[1] / errs[2]]
+    assert 2.5 < q[0] and 2.5 < q[1] < 4.6, (errs, q)
+
+
+def test_paper_tables_fixture_is_context_only():
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_tables.json")))
+    # the paper's own trend: down every column, e_r does not increase with B
+    for A in ("A2", "A4", "A6", "A8"):
+        rows = [g["table1"][A][f"B{b}"] for b in range(4)]
+        for c in range(3):
+            col = [r[c] for r in rows if r[c] is not None]
+            assert all(x >= y for x, y in zip(col, col[1:]))
+    assert g["table2"]["e_r"] == sorted(g["table2"]["e_r"])
