@@ -1,0 +1,287 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SR-FMG solve (BASELINE.json metric: fine-grid cells solved/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C3] [--dtype f64|f32]
+
+A step is one complete FMG+SR solve (sr_fmg_solve) of the workload: f-pyramid, coarsest
+solve, conventional FMG below the transition level, K SR levels, output gather.  Prints one
+JSON line on rank 0.  Default workload C3 (BASELINE.json configs[2]): 512^3 cells, fp64,
+manufactured f + N(0, 1e-3) noise, 8^3 segments of 64^3, buffer 2, 4 SR levels, M = 8 --
+the largest single-GPU configuration (configs[0]/[1] are the small parity cases).
+
+`--impl reference` times the CPU oracle (oracle/, the test reference implementation) on a
+bounded sample of the same workload on the host cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+WORKLOADS = {
+    # name: (n, M, seg, buffer, K, rhs)
+    "C1": ((32, 32, 32), 4, 16, 2, 2, "manufactured"),
+    "C2": ((128, 128, 128), 6, 32, 2, 3, "manufactured"),
+    "C3": ((512, 512, 512), 8, 64, 2, 4, "manufactured+noise"),
+    "C5": ((1024, 1024, 1024), 9, 128, 2, 4, "bumps"),
+}
+# bounded CPU sample of C3 for the oracle: the same 8^3 segment grid, K = 4, J = 2, at
+# 128^3 (1/64 of the cells); about 7 s of numpy per solve on one core
+ORACLE_SAMPLE = dict(n=(128, 128, 128), M=6, seg=16, buffer=2, K=4, rhs="manufactured+noise")
+KC_CHEB = 0  # kernel class index of k_cheb_step (sr_fmg_kernel_name)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > i + 2 and r[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def oracle_sample_solve():
+    import oracle as O
+    s = ORACLE_SAMPLE
+    f = W.make_rhs(s["rhs"], s["n"])
+    cfg = O.Config(n=s["n"], M=s["M"], seg=s["seg"], buffer=s["buffer"], K=s["K"])
+    t0 = time.perf_counter()
+    O.solve(f, cfg)
+    return time.perf_counter() - t0, float(np.prod(s["n"]))
+
+
+def sample_desc():
+    s = ORACLE_SAMPLE
+    return (f"oracle (numpy fp64) FMG+SR solve of {s['n'][0]}^3 cells, M={s['M']}, "
+            f"seg={s['seg']} (8^3 segments), buffer={s['buffer']}, K={s['K']}, "
+            f"{s['rhs']} rhs: the C3 segment grid/K/J at 1/64 of the cells")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        oracle_sample_solve()
+    ts, cells = [], 0.0
+    for _ in range(args.steps):
+        t, cells = oracle_sample_solve()
+        ts.append(t)
+    tot = sum(ts)
+    value = cells * len(ts) / tot
+    line = {
+        "impl": "reference", "metric": "fine-grid cells solved/s (FMG+SR)", "value": value,
+        "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (bounded CPU sample)", "sample": sample_desc()},
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle",
+                         "sample": sample_desc()},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1406_7808_b200 import Solver
+
+    n, M, seg, buf, K, rhs = WORKLOADS[args.config]
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    solver = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=args.dtype)
+    f_host = W.make_rhs(rhs, n).astype(np.float64 if args.dtype == "f64" else np.float32)
+    f = torch.from_numpy(f_host).cuda()
+    u = torch.empty_like(f)
+    cells = float(np.prod(n))
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 3)):
+        solver.solve(f, u)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K solves; CUDA events around every fine-level Chebyshev sweep
+    solver.profile_select(KC_CHEB, solver.M)
+    solver.solve(f, u)  # re-capture the graph with the profiling events (untimed)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    kms, kbytes, klaunch = 0.0, 0.0, 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        solver.solve(f, u)
+        stream.synchronize()  # read this step's kernel events (graph events are reused)
+        a, b, c = solver.profile_read()
+        kms, kbytes, klaunch = kms + a, kbytes + b, klaunch + c
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cells * world / (ms / 1e3)
+
+    # ---- end-to-end through the public API from pinned host buffers
+    solver.profile_select(-1, -1)
+    fh = torch.from_numpy(f_host).pin_memory()
+    uh = torch.empty_like(fh).pin_memory()
+    solver.solve_host(fh, uh)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        solver.solve_host(fh, uh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    nbytes = f_host.nbytes
+
+    peak, peak_src = measured_peak()
+    achieved = (kbytes / (kms / 1e3)) / 1e9 if kms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"{args.config}_{args.dtype}")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "fine-grid cells solved/s (FMG+SR, fp64)" if args.dtype == "f64"
+        else "fine-grid cells solved/s (FMG+SR, fp32)",
+        "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": f"synthetic ({rhs}, seed {W.SEED})",
+        "config": {"workload": f"{args.config}: {n[0]}x{n[1]}x{n[2]} cells per GPU, M={M}, "
+                               f"seg={seg}, buffer={buf}, K={K} SR levels, F(1,2,2)",
+                   "global_cells": cells * world,
+                   "parallelism": "independent replicas per GPU" if world > 1 else "1 GPU",
+                   "l2": "inputs larger than L2 (f %.2f GB, workspace %.2f GB)"
+                         % (nbytes / 1e9, solver.workspace_bytes / 1e9)},
+        "roofline": {"bound": "hbm", "kernel": "k_cheb_step @ finest level",
+                     "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic,
+                     "launches_per_step": klaunch / max(args.steps, 1),
+                     "alg_bytes_per_launch": kbytes / max(klaunch, 1),
+                     "avg_launch_ms": kms / max(klaunch, 1),
+                     "share_of_step": (kms / args.steps) / ms if ms > 0 else None},
+        "e2e": {"value": cells * world / (ems / 1e3), "unit": "cells/s",
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "ms_per_step": ems},
+        "gpu_launches": int(solver.launches_per_solve * args.steps),
+        "solve_alg_bytes": solver.alg_bytes_per_solve,
+        "solve_roofline_frac": (solver.alg_bytes_per_solve / (ms / 1e3)) / (peak * 1e9),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t1, c1 = oracle_sample_solve()
+        t2, c2 = oracle_sample_solve()
+        line["cpu_baseline"] = {"value": (c1 + c2) / (t1 + t2), "unit": "cells/s", "cores": 1,
+                                "kind": "oracle", "sample": sample_desc() + " (2 solves)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

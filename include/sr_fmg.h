@@ -1,0 +1,160 @@
+/*
+ * sr_fmg.h -- C ABI of the B200 segmental-refinement full-multigrid solver.
+ *
+ * Operation (the paper's problem statement, §2 Eq. 1-2):
+ *   solve  L_h u_h = f_h  on the cell-centred grid Omega_h, u = 0 on the boundary, with
+ *   L_h = -Lap_h the 7-point operator (readings R1/R2 of DESIGN.md §3), by one FAS full
+ *   multigrid F(alpha, nu1, nu2) solve (fig:fmg) whose finest
+ *   `sr_levels` levels are segmental-refinement levels (fig:fmgsr / fig:mgvsr,
+ *   PAPER.md:216-246): every segment of seg^3 genuine fine cells plus `buffer` buffer
+ *   cells is smoothed, residual-evaluated, restricted and prolongated on its own, with no
+ *   exchange between segments; the levels at and below the transition level
+ *   T = M - sr_levels run a conventional FAS V-cycle down to an exact coarsest solve.
+ *   The result is an APPROXIMATION (FMG algebraic error O(discretisation error), plus the
+ *   SR buffer perturbation) -- not the exact discrete solution.
+ *
+ * Layout.  f and u are dense arrays of n[0]*n[1]*n[2] elements, x1 fastest:
+ *   element (i1, i2, i3) at offset (i3*n[1] + i2)*n[0] + i1, cell centre
+ *   x_d = (i_d + 1/2) h.  Element type: double (SR_F64) or float (SR_F32).
+ *
+ * Ownership.  The caller owns f and u; the library never retains them after a call
+ *   returns.  The library owns its device workspace (allocated in create, freed in
+ *   destroy) and, when it captures one, the CUDA graph of a solve.
+ *
+ * Execution.  sr_fmg_solve is asynchronous and ordered on the handle's stream (the
+ *   legacy default stream unless one is given).  Device pointers must be 16-byte aligned
+ *   and must not overlap.  sr_fmg_solve_host is synchronous.
+ *
+ * Errors.  Every call returns SR_OK or an error code; sr_fmg_last_error() gives a
+ *   message.  create validates everything before allocating; on failure *out = NULL.
+ *   A CUDA error makes the handle sticky-failed: that call and every later call on the
+ *   handle return SR_ERR_CUDA until destroy.  A handle is not thread-safe.
+ *
+ * Determinism.  Results are bitwise reproducible for a fixed (descriptor, f).
+ */
+#ifndef SR_FMG_H
+#define SR_FMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SR_FMG_MAX_LEVELS 24
+
+typedef struct sr_fmg sr_fmg_t; /* opaque */
+
+typedef enum {
+  SR_OK = 0,
+  SR_ERR_INVALID_ARGUMENT = 1,  /* arithmetically impossible descriptor / null pointer */
+  SR_ERR_UNSUPPORTED_CONFIG = 2,/* valid, but outside what this build supports          */
+  SR_ERR_OUT_OF_MEMORY = 3,
+  SR_ERR_CUDA = 4,
+  SR_ERR_NCCL = 5
+} sr_status_t;
+
+typedef enum { SR_F64 = 0, SR_F32 = 1 } sr_dtype_t;
+
+/* Full descriptor.  Initialise with sr_fmg_desc_init() and override fields. */
+typedef struct {
+  int64_t n[3];       /* fine cells per dimension (x1, x2, x3); each divisible by 2^M   */
+  int32_t M;          /* number of coarsenings: levels 0..M, coarsest grid n/2^M (>= 1) */
+  int32_t seg;        /* S: genuine segment edge on the finest level; n_d % S == 0,      */
+                      /*    S % 2^sr_levels == 0 (ignored when sr_levels == 0)           */
+  int32_t buffer;     /* J: buffer cells on every SR level (Eq. 5 with A = J, B = 0)     */
+  int32_t sr_levels;  /* K: number of SR levels, 0 <= K <= M (0 = conventional FMG)      */
+  int32_t sched_A;    /* Eq. 5 buffer schedule J_k = 2 floor((A + B (K-k))/2)            */
+  int32_t sched_B;    /*   (PAPER.md:192); (-1, -1) = constant `buffer`                  */
+  int32_t dtype;      /* sr_dtype_t                                                       */
+  double h;           /* fine cell size; 0 = 1/n[0] (unit cube for cubic grids)          */
+  int32_t alpha;      /* F(alpha, nu1, nu2) Chebyshev degrees;       */
+  int32_t nu1;        /*   default (1, 2, 2)                                             */
+  int32_t nu2;
+  double cheb_lo;     /* Chebyshev interval [lo, hi] * lambda_max, lambda_max = 12/h_l^2 */
+  double cheb_hi;     /*   default [1/6, 1] (reading R8)                                 */
+  int32_t world;      /* number of ranks (GPUs); 1 = single GPU                          */
+  int32_t rank;
+  int32_t pgrid[3];   /* rank grid; world == pgrid[0]*pgrid[1]*pgrid[2]                  */
+  const void *nccl_id;/* 128-byte ncclUniqueId (world > 1)                               */
+  int32_t device;     /* CUDA device ordinal; -1 = current device                        */
+  void *stream;       /* cudaStream_t; NULL = legacy default stream                      */
+  int32_t use_graph;  /* 1 (default): capture a solve into a CUDA graph and replay it    */
+} sr_fmg_desc_t;
+
+typedef struct {
+  int32_t M, K, T;                         /* levels 0..M; transition level T = M-K    */
+  int32_t dtype;
+  int64_t n_level[SR_FMG_MAX_LEVELS][3];   /* cells of Omega_l per dimension           */
+  int32_t sr[SR_FMG_MAX_LEVELS];           /* 1 if level l is an SR level              */
+  int32_t seg_level[SR_FMG_MAX_LEVELS];    /* S_l (SR levels) or n_l[0] (conventional) */
+  int32_t buffer_level[SR_FMG_MAX_LEVELS]; /* J_l (0 on conventional levels)           */
+  int32_t nseg[SR_FMG_MAX_LEVELS][3];      /* segments per dimension (1 if conventional) */
+  int32_t storage_ext[SR_FMG_MAX_LEVELS][3];/* storage box extent per segment            */
+  int64_t storage_pitch[SR_FMG_MAX_LEVELS][3]; /* element strides: row, plane, segment  */
+  int64_t compute_cells[SR_FMG_MAX_LEVELS];/* sum_p |C_l^p|                             */
+  int64_t visits[SR_FMG_MAX_LEVELS];       /* level visits per solve (smoothing passes)  */
+  int64_t workspace_bytes;
+  int64_t launches_per_solve;              /* kernel launches in one solve               */
+  double alg_bytes_per_solve;              /* B_alg of DESIGN.md §6 (fused-design bytes) */
+} sr_fmg_info_t;
+
+/* Fill *d with defaults: cube 0, M 0, seg 0, buffer 2, K 0, sched (-1,-1), fp64,
+ * h 0, F(1,2,2), interval [1/6, 1], world 1, device -1, stream NULL, use_graph 1. */
+void sr_fmg_desc_init(sr_fmg_desc_t *d);
+
+/* North-star form: cube N^3, fp64, constant buffer, current device, default stream. */
+sr_status_t sr_fmg_create(int64_t N, int32_t M, int32_t seg, int32_t buffer,
+                          int32_t sr_levels, sr_fmg_t **out);
+sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t *d, sr_fmg_t **out);
+
+/* One FMG+SR solve.  f: device pointer to the fine right-hand side; u: device pointer to
+ * the output (every cell written).  Asynchronous on the handle's stream. */
+sr_status_t sr_fmg_solve(sr_fmg_t *h, const void *f, void *u);
+
+/* The same solve from HOST buffers: copies f to the device, solves, copies u back,
+ * synchronises.  Pinned host memory makes the copies asynchronous DMA. */
+sr_status_t sr_fmg_solve_host(sr_fmg_t *h, const void *f_host, void *u_host);
+
+/* Change the stream later solves are ordered on (a captured graph is reused). */
+sr_status_t sr_fmg_set_stream(sr_fmg_t *h, void *stream);
+
+void sr_fmg_destroy(sr_fmg_t *h); /* NULL-safe; synchronises the handle's stream */
+
+sr_status_t sr_fmg_get_info(const sr_fmg_t *h, sr_fmg_info_t *info);
+
+/* Message of the last error on h (or of the calling thread's last failed create when
+ * h == NULL).  Never NULL; valid until the next call on the same handle/thread. */
+const char *sr_fmg_last_error(const sr_fmg_t *h);
+
+/* Number of distinct kernels the library can launch, and their names (for launch lists). */
+int32_t sr_fmg_kernel_count(void);
+const char *sr_fmg_kernel_name(int32_t i);
+
+/* ---- test-only hooks (not part of the solver contract) ---------------------------------
+ * sr_fmg_debug_level_io: copy the internal storage of (level, field) of ALL segments
+ * between the device and a host buffer of nseg*storage_pitch[level][2] elements
+ * (field 0 = current u, 1 = rhs, 2 = t; write != 0 copies host -> device).
+ * sr_fmg_debug_op: run one kernel of the schedule on the internal buffers:
+ *   op 0 = CHEB(deg) on level with rhs = internal rhs buffer (or user f when level == M),
+ *   op 1 = residual + restriction level -> level-1,  op 2 = tau-rhs + t snapshot on level
+ *          (support from level+1),  op 3 = prolongation SET level-1 -> level,
+ *   op 4 = prolongation ADD of (u - t) level-1 -> level,  op 5 = exact coarsest solve. */
+sr_status_t sr_fmg_debug_level_io(sr_fmg_t *h, int32_t level, int32_t field, int32_t write,
+                                  void *host);
+sr_status_t sr_fmg_debug_op(sr_fmg_t *h, int32_t op, int32_t level, int32_t deg,
+                            const void *f_dev);
+
+/* Profiling hooks used by bench.py: select one kernel class (index into
+ * sr_fmg_kernel_name) at one level; later solves record a CUDA event pair around every
+ * such launch (inside the captured graph).  profile_read, after the solve completed,
+ * returns the summed device time (ms), the summed algorithmic bytes and
+ * the number of profiled launches of the last solve.  kernel_class -1 disables. */
+sr_status_t sr_fmg_profile_select(sr_fmg_t *h, int32_t kernel_class, int32_t level);
+sr_status_t sr_fmg_profile_read(sr_fmg_t *h, double *ms, double *bytes, int32_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SR_FMG_H */

@@ -1,0 +1,186 @@
+"""Thin Python front end of the SR-FMG C ABI (argument marshalling only).
+
+PyTorch supplies device memory and streams; every step of a solve runs in the library's
+CUDA kernels (paper_1406_7808_b200/csrc).  Arrays use shape (n3, n2, n1), x1 fastest,
+exactly the layout include/sr_fmg.h documents.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import Desc, Info, check, lib
+
+
+@dataclass
+class LevelInfo:
+    n: Tuple[int, int, int]
+    sr: bool
+    seg: int
+    buffer: int
+    nseg: Tuple[int, int, int]
+    storage_ext: Tuple[int, int, int]
+    pitch: Tuple[int, int, int]
+    compute_cells: int
+    visits: int
+
+
+class Solver:
+    """One FMG+SR solver instance (a handle of the C ABI).
+
+    Parameters mirror sr_fmg_desc_t: n (n1, n2, n3) or an int for a cube, M, seg (S),
+    buffer (J), K (SR levels), dtype "f64"/"f32", h (fine cell size), sched (Eq. 5 A, B),
+    F(alpha, nu1, nu2) degrees, Chebyshev interval fractions.
+    """
+
+    def __init__(self, n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None,
+                 alpha=1, nu1=2, nu2=2, cheb=(1.0 / 6.0, 1.0), device=None, use_graph=True):
+        if isinstance(n, int):
+            n = (n, n, n)
+        d = Desc()
+        lib.sr_fmg_desc_init(ctypes.byref(d))
+        for i in range(3):
+            d.n[i] = int(n[i])
+        d.M, d.seg, d.buffer, d.sr_levels = int(M), int(seg), int(buffer), int(K)
+        if sched is not None:
+            d.sched_A, d.sched_B = int(sched[0]), int(sched[1])
+        d.dtype = {"f64": _lib.SR_F64, "f32": _lib.SR_F32}[dtype]
+        d.h = 0.0 if h is None else float(h)
+        d.alpha, d.nu1, d.nu2 = int(alpha), int(nu1), int(nu2)
+        d.cheb_lo, d.cheb_hi = float(cheb[0]), float(cheb[1])
+        d.device = -1 if device is None else int(device)
+        d.use_graph = 1 if use_graph else 0
+        self._h = ctypes.c_void_p()
+        check(lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(self._h)))
+        self.n = tuple(int(v) for v in n)
+        self.shape = (self.n[2], self.n[1], self.n[0])
+        self.dtype = dtype
+        self.np_dtype = np.float64 if dtype == "f64" else np.float32
+        self._info = self._get_info()
+
+    # -- lifetime ------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib.sr_fmg_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- info ----------------------------------------------------------------------------
+    def _get_info(self):
+        inf = Info()
+        check(lib.sr_fmg_get_info(self._h, ctypes.byref(inf)), self._h)
+        return inf
+
+    @property
+    def M(self):
+        return self._info.M
+
+    @property
+    def K(self):
+        return self._info.K
+
+    @property
+    def T(self):
+        return self._info.T
+
+    def level(self, l) -> LevelInfo:
+        i = self._info
+        return LevelInfo(tuple(i.n_level[l]), bool(i.sr[l]), i.seg_level[l], i.buffer_level[l],
+                         tuple(i.nseg[l]), tuple(i.storage_ext[l]), tuple(i.storage_pitch[l]),
+                         i.compute_cells[l], i.visits[l])
+
+    @property
+    def launches_per_solve(self) -> int:
+        return self._info.launches_per_solve
+
+    @property
+    def alg_bytes_per_solve(self) -> float:
+        return self._info.alg_bytes_per_solve
+
+    @property
+    def workspace_bytes(self) -> int:
+        return self._info.workspace_bytes
+
+    # -- solves --------------------------------------------------------------------------
+    def _check_tensor(self, t, name):
+        import torch
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise TypeError(f"{name} must be a CUDA torch.Tensor")
+        want = torch.float64 if self.dtype == "f64" else torch.float32
+        if t.dtype != want or tuple(t.shape) != self.shape or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {want} tensor of shape {self.shape}")
+
+    def solve(self, f, out=None):
+        """u = FMG+SR solve of A u = f.  f, out: CUDA tensors of shape (n3, n2, n1).
+        Ordered on torch's current stream; returns `out`."""
+        import torch
+        self._check_tensor(f, "f")
+        if out is None:
+            out = torch.empty_like(f)
+        self._check_tensor(out, "out")
+        check(lib.sr_fmg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+              self._h)
+        check(lib.sr_fmg_solve(self._h, ctypes.c_void_p(f.data_ptr()),
+                               ctypes.c_void_p(out.data_ptr())), self._h)
+        return out
+
+    def solve_host(self, f, out=None):
+        """Same solve from host memory (numpy array or CPU tensor, pinned or not); copies
+        happen inside the library call.  Synchronous; returns `out`."""
+        import torch
+        if isinstance(f, np.ndarray):
+            f = torch.from_numpy(np.ascontiguousarray(f, dtype=self.np_dtype))
+        if out is None:
+            out = torch.empty(self.shape, dtype=f.dtype, pin_memory=f.is_pinned())
+        for t, nm in ((f, "f"), (out, "out")):
+            if t.is_cuda or tuple(t.shape) != self.shape or not t.is_contiguous():
+                raise ValueError(f"{nm} must be a contiguous host tensor of shape {self.shape}")
+        check(lib.sr_fmg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+              self._h)
+        check(lib.sr_fmg_solve_host(self._h, ctypes.c_void_p(f.data_ptr()),
+                                    ctypes.c_void_p(out.data_ptr())), self._h)
+        return out
+
+    # -- test / profiling hooks ----------------------------------------------------------
+    def level_storage(self, l, field=0) -> np.ndarray:
+        """Internal storage of level l (field 0 = u, 1 = rhs, 2 = t) as an array of shape
+        (nsegs, E_z, E_y, pitch_y) view-able per segment."""
+        li = self.level(l)
+        nsegs = li.nseg[0] * li.nseg[1] * li.nseg[2]
+        buf = np.empty(nsegs * li.pitch[2], dtype=self.np_dtype)
+        check(lib.sr_fmg_debug_level_io(self._h, l, field, 0, buf.ctypes.data_as(ctypes.c_void_p)),
+              self._h)
+        return buf
+
+    def set_level_storage(self, l, field, arr: np.ndarray):
+        arr = np.ascontiguousarray(arr, dtype=self.np_dtype)
+        check(lib.sr_fmg_debug_level_io(self._h, l, field, 1, arr.ctypes.data_as(ctypes.c_void_p)),
+              self._h)
+
+    def debug_op(self, op, level, deg=0, f=None):
+        ptr = ctypes.c_void_p(f.data_ptr()) if f is not None else None
+        check(lib.sr_fmg_debug_op(self._h, op, level, deg, ptr), self._h)
+
+    def profile_select(self, kernel_class: int, level: int):
+        check(lib.sr_fmg_profile_select(self._h, kernel_class, level), self._h)
+
+    def profile_read(self):
+        ms, by, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        check(lib.sr_fmg_profile_read(self._h, ctypes.byref(ms), ctypes.byref(by),
+                                      ctypes.byref(n)), self._h)
+        return ms.value, by.value, n.value

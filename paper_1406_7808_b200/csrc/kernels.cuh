@@ -1,0 +1,59 @@
+// Internal kernel interface of the SR-FMG library (not part of the C ABI).
+//
+// Every level l of the hierarchy is described by a `Lvl`: a grid of segments, each with a
+// private storage box grow(V, J+1) (SURVEY §8(a) layouts).  Conventional
+// levels (l <= T) are the special case of ONE segment with V = Omega_l and J = 0, whose
+// storage box is Omega_l plus a one-cell ghost ring ("Omega_h^{+1}").
+// Dimension order inside the library is (x, y, z) = (x1, x2, x3), x fastest.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace srfmg {
+
+struct Lvl {
+  int N[3];          // cells of Omega_l per dimension
+  int S[3];          // genuine segment edge per dimension (N on conventional levels)
+  int J;             // buffer width (0 on conventional levels)
+  int ns[3];         // segments per dimension
+  int E[3];          // storage extent per dimension: S + 2J + 2
+  int py;            // row pitch in elements
+  long long pz;      // plane pitch in elements
+  long long ss;      // segment stride in elements
+  int nsegs;
+  double inv_h2;     // 1 / h_l^2
+};
+
+// Read-only right-hand-side view: either a dense global array over Omega_l without ghosts
+// (user f or an f-pyramid level) or a level's segment storage (tau right-hand sides).
+template <class T>
+struct View {
+  const T* p;
+  int global;        // 1: dense global array, index g.z*sz + g.y*sy + g.x
+  long long sy, sz;  // strides (row, plane)
+  long long ss;      // segment stride (segment storage only)
+};
+
+// Launchers (kernels.cu).  All asynchronous on `st`.
+template <class T>
+void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* out, double c_mom,
+                      double c_res, int copy_gsr, cudaStream_t st);
+template <class T>
+void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc, int jr,
+                     cudaStream_t st);
+template <class T>
+void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st);
+template <class T>
+void launch_prolong(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
+                    cudaStream_t st);
+template <class T>
+void launch_coarsest(const Lvl& L0, T* u, View<T> b, const T* ainv, cudaStream_t st);
+template <class T>
+void launch_pyramid(const T* ff, int nfx, int nfy, int nfz, T* fc, cudaStream_t st);
+template <class T>
+void launch_gather(const Lvl& L, const T* useg, T* out, cudaStream_t st);
+
+extern const char* const kKernelNames[];
+extern const int kNumKernelNames;
+
+}  // namespace srfmg

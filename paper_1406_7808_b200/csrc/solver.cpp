@@ -1,0 +1,777 @@
+// Host side of the SR-FMG library: validation, level plan, workspace, the solve schedule
+// (fig:fmg / fig:fmgsr / fig:mgv / fig:mgvsr as one recursion over level descriptors),
+// CUDA-graph capture, and the C ABI of include/sr_fmg.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "sr_fmg.h"
+
+using srfmg::Lvl;
+using srfmg::View;
+
+namespace {
+
+thread_local std::string g_tls_err = "no error";
+
+enum KernelClass { KC_CHEB = 0, KC_RESTRICT, KC_TAU, KC_PROLONG, KC_COARSEST, KC_PYRAMID,
+                   KC_GATHER, KC_COUNT };
+
+struct LevelBufs {
+  void* u[2] = {nullptr, nullptr};  // two solution buffers (Chebyshev ping-pong)
+  int cur = 0;                      // which one holds the current iterate
+  void* rhs = nullptr;              // tau right-hand side (levels < M)
+  void* t = nullptr;                // t snapshot (levels < M)
+  void* fpyr = nullptr;             // dense f_l (levels < M)
+};
+
+struct ProfRec {
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+struct CellCounts {
+  long long compute = 0;   // sum_p |C^p|
+  long long cg = 0;        // sum_p |storage ∩ Omega| (C ∪ GSR)
+  long long storage = 0;   // sum_p |storage box|
+};
+
+long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct sr_fmg {
+  sr_fmg_desc_t d{};
+  int M = 0, K = 0, T = 0;
+  int esize = 8;
+  double h = 0;
+  std::vector<Lvl> L;
+  std::vector<LevelBufs> B;
+  std::vector<CellCounts> cells;
+  std::vector<double> theta, delta, sigma;
+  void* ainv = nullptr;
+  cudaStream_t stream = nullptr;   // user stream (solves are ordered on it)
+  cudaStream_t cap = nullptr;      // private stream used for graph capture
+  std::string err = "no error";
+  sr_status_t sticky = SR_OK;
+  cudaGraphExec_t gexec = nullptr;
+  const void* g_f = nullptr;
+  void* g_u = nullptr;
+  void* host_f = nullptr;  // device staging buffers for sr_fmg_solve_host
+  void* host_u = nullptr;
+  long long launches = 0;
+  bool sync_debug = false;
+  int prof_cls = -1, prof_level = -1;
+  std::vector<ProfRec> prof;
+  size_t prof_used = 0;
+  long long workspace = 0;
+  std::vector<long long> visits;
+};
+
+namespace {
+
+sr_status_t fail(sr_fmg* h, sr_status_t st, const std::string& msg) {
+  if (h) {
+    h->err = msg;
+    if (st == SR_ERR_CUDA || st == SR_ERR_NCCL) h->sticky = st;
+  } else {
+    g_tls_err = msg;
+  }
+  return st;
+}
+
+#define CU(h, call)                                                                  \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail((h), SR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------------------------------
+// validation (create-time, before any allocation)
+// ------------------------------------------------------------------------------------
+sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
+  auto bad = [&](const char* m) { msg = m; return SR_ERR_INVALID_ARGUMENT; };
+  if (d->M < 0 || d->M >= SR_FMG_MAX_LEVELS) return bad("M out of range");
+  for (int i = 0; i < 3; ++i) {
+    if (d->n[i] <= 0) return bad("n[d] must be positive");
+    if (d->n[i] % (1LL << d->M)) return bad("n[d] must be divisible by 2^M");
+    if (d->n[i] > (1LL << 30)) return bad("n[d] too large");
+  }
+  if (d->sr_levels < 0 || d->sr_levels > d->M) return bad("need 0 <= sr_levels <= M");
+  if (d->sr_levels > 0) {
+    if (d->seg <= 0) return bad("seg must be positive when sr_levels > 0");
+    for (int i = 0; i < 3; ++i)
+      if (d->n[i] % d->seg) return bad("n[d] must be divisible by seg");
+    if (d->seg % (1 << d->sr_levels)) return bad("seg must be divisible by 2^sr_levels");
+  }
+  if (d->buffer < 0) return bad("buffer must be >= 0");
+  if ((d->sched_A < 0) != (d->sched_B < 0)) return bad("sched_A/sched_B: both or neither");
+  if (d->dtype != SR_F64 && d->dtype != SR_F32) return bad("dtype must be SR_F64 or SR_F32");
+  if (d->h < 0 || !std::isfinite(d->h)) return bad("h must be >= 0 and finite");
+  if (d->alpha < 0 || d->nu1 < 0 || d->nu2 < 0) return bad("Chebyshev degrees must be >= 0");
+  if (!(d->cheb_lo > 0) || !(d->cheb_hi > d->cheb_lo)) return bad("need 0 < cheb_lo < cheb_hi");
+  if (d->world < 1) return bad("world must be >= 1");
+  if (d->world != d->pgrid[0] * d->pgrid[1] * d->pgrid[2]) return bad("world != prod(pgrid)");
+  if (d->rank < 0 || d->rank >= d->world) return bad("rank out of range");
+  // supported-config checks
+  if (d->world != 1) {
+    msg = "multi-GPU descriptors are not supported by this build (world must be 1)";
+    return SR_ERR_UNSUPPORTED_CONFIG;
+  }
+  long long n0 = 1;
+  for (int i = 0; i < 3; ++i) n0 *= d->n[i] >> d->M;
+  if (n0 > 1024) {
+    msg = "coarsest grid has more than 1024 cells (dense exact solve); increase M";
+    return SR_ERR_UNSUPPORTED_CONFIG;
+  }
+  return SR_OK;
+}
+
+int buffer_of(const sr_fmg_desc_t* d, int k) {  // Eq. 5
+  if (d->sched_A < 0) return d->buffer;
+  return 2 * ((d->sched_A + d->sched_B * (d->sr_levels - k)) / 2);
+}
+
+// ------------------------------------------------------------------------------------
+// level plan
+// ------------------------------------------------------------------------------------
+void make_plan(sr_fmg* h) {
+  const sr_fmg_desc_t* d = &h->d;
+  h->M = d->M;
+  h->K = d->sr_levels;
+  h->T = d->M - d->sr_levels;
+  h->esize = d->dtype == SR_F64 ? 8 : 4;
+  h->h = d->h > 0 ? d->h : 1.0 / (double)d->n[0];
+  const int pitch_mult = 32 / h->esize;  // rows start on 32-byte sectors
+  h->L.assign(h->M + 1, Lvl{});
+  h->cells.assign(h->M + 1, CellCounts{});
+  h->theta.assign(h->M + 1, 0);
+  h->delta.assign(h->M + 1, 0);
+  h->sigma.assign(h->M + 1, 0);
+  for (int l = 0; l <= h->M; ++l) {
+    Lvl& L = h->L[l];
+    const bool sr = l > h->T;
+    for (int i = 0; i < 3; ++i) L.N[i] = (int)(d->n[i] >> (h->M - l));
+    L.J = sr ? buffer_of(d, l - h->T) : 0;
+    for (int i = 0; i < 3; ++i) {
+      L.S[i] = sr ? (d->seg >> (h->M - l)) : L.N[i];
+      L.ns[i] = L.N[i] / L.S[i];
+      L.E[i] = L.S[i] + 2 * L.J + 2;
+    }
+    L.nsegs = L.ns[0] * L.ns[1] * L.ns[2];
+    L.py = (int)round_up(L.E[0], pitch_mult);
+    L.pz = (long long)L.py * L.E[1];
+    L.ss = round_up(L.pz * L.E[2], 32);
+    const double hl = h->h * (double)(1LL << (h->M - l));
+    L.inv_h2 = 1.0 / (hl * hl);
+    const double lam = 12.0 / (hl * hl);  // R8: lambda_max(A_l) = 12/h_l^2
+    const double a = d->cheb_lo * lam, b = d->cheb_hi * lam;
+    h->theta[l] = 0.5 * (b + a);
+    h->delta[l] = 0.5 * (b - a);
+    h->sigma[l] = h->theta[l] / h->delta[l];
+    // cell counts (region arithmetic of PAPER.md:187-210 on boxes)
+    CellCounts& c = h->cells[l];
+    for (int s = 0; s < L.nsegs; ++s) {
+      const int p[3] = {s % L.ns[0], (s / L.ns[0]) % L.ns[1], s / (L.ns[0] * L.ns[1])};
+      long long vc = 1, vcg = 1;
+      for (int i = 0; i < 3; ++i) {
+        const int lo = p[i] * L.S[i], hi = lo + L.S[i];
+        vc *= std::min(hi + L.J, L.N[i]) - std::max(lo - L.J, 0);
+        vcg *= std::min(hi + L.J + 1, L.N[i]) - std::max(lo - L.J - 1, 0);
+      }
+      c.compute += vc;
+      c.cg += vcg;
+      c.storage += (long long)L.E[0] * L.E[1] * L.E[2];
+    }
+  }
+  h->visits.assign(h->M + 1, 0);
+  for (int l = 0; l <= h->M; ++l) h->visits[l] = h->M - l + 1;
+}
+
+// dense inverse of A_0 (7-point, reflected ghosts) by Gauss-Jordan in fp64 (R7)
+std::vector<double> coarsest_inverse(const Lvl& L0) {
+  const int nx = L0.N[0], ny = L0.N[1], nz = L0.N[2];
+  const int n = nx * ny * nz;
+  std::vector<double> A((size_t)n * n, 0.0), I((size_t)n * n, 0.0);
+  auto id = [&](int x, int y, int z) { return (z * ny + y) * nx + x; };
+  for (int z = 0; z < nz; ++z)
+    for (int y = 0; y < ny; ++y)
+      for (int x = 0; x < nx; ++x) {
+        const int i = id(x, y, z);
+        double diag = 6.0;
+        const int c[3] = {x, y, z}, N[3] = {nx, ny, nz};
+        for (int dd = 0; dd < 3; ++dd)
+          for (int o = -1; o <= 1; o += 2) {
+            int q[3] = {c[0], c[1], c[2]};
+            q[dd] += o;
+            if (q[dd] < 0 || q[dd] >= N[dd]) {
+              diag += 1.0;  // ghost = -u_i
+            } else {
+              A[(size_t)i * n + id(q[0], q[1], q[2])] -= L0.inv_h2;
+            }
+          }
+        A[(size_t)i * n + i] += diag * L0.inv_h2;
+      }
+  for (int i = 0; i < n; ++i) I[(size_t)i * n + i] = 1.0;
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (std::fabs(A[(size_t)r * n + col]) > std::fabs(A[(size_t)piv * n + col])) piv = r;
+    if (piv != col)
+      for (int k = 0; k < n; ++k) {
+        std::swap(A[(size_t)piv * n + k], A[(size_t)col * n + k]);
+        std::swap(I[(size_t)piv * n + k], I[(size_t)col * n + k]);
+      }
+    const double inv = 1.0 / A[(size_t)col * n + col];
+    for (int k = 0; k < n; ++k) {
+      A[(size_t)col * n + k] *= inv;
+      I[(size_t)col * n + k] *= inv;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == col) continue;
+      const double fct = A[(size_t)r * n + col];
+      if (fct == 0.0) continue;
+      for (int k = 0; k < n; ++k) {
+        A[(size_t)r * n + k] -= fct * A[(size_t)col * n + k];
+        I[(size_t)r * n + k] -= fct * I[(size_t)col * n + k];
+      }
+    }
+  }
+  return I;
+}
+
+// ------------------------------------------------------------------------------------
+// launch bookkeeping: count launches, optional CUDA-event profiling of one (class, level)
+// ------------------------------------------------------------------------------------
+struct Launch {
+  sr_fmg* h;
+  cudaStream_t st;
+  ProfRec* rec = nullptr;
+  Launch(sr_fmg* h_, cudaStream_t st_, int cls, int level, double bytes) : h(h_), st(st_) {
+    h->launches++;
+    if (cls == h->prof_cls && level == h->prof_level) {
+      if (h->prof_used == h->prof.size()) {
+        ProfRec r{};
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        h->prof.push_back(r);
+      }
+      rec = &h->prof[h->prof_used++];
+      rec->bytes = bytes;
+      cudaEventRecord(rec->a, st);
+    }
+  }
+  ~Launch() {
+    if (rec) cudaEventRecord(rec->b, st);
+    if (h->sync_debug) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        fprintf(stderr, "sr_fmg: kernel failed: %s\n", cudaGetErrorString(e));
+        h->sticky = SR_ERR_CUDA;
+        h->err = std::string("kernel failed: ") + cudaGetErrorString(e);
+      }
+    }
+  }
+};
+
+// ------------------------------------------------------------------------------------
+// the schedule
+// ------------------------------------------------------------------------------------
+template <class T>
+struct Schedule {
+  sr_fmg* h;
+  cudaStream_t st;
+  const T* f;  // user fine rhs (device)
+  double w;    // element size
+
+  T* U(int l) { return (T*)h->B[l].u[h->B[l].cur]; }
+
+  View<T> fview(int l) {
+    const Lvl& L = h->L[l];
+    View<T> v;
+    v.p = (l == h->M) ? f : (const T*)h->B[l].fpyr;
+    v.global = 1;
+    v.sy = L.N[0];
+    v.sz = (long long)L.N[0] * L.N[1];
+    v.ss = 0;
+    return v;
+  }
+  View<T> sview(int l) {
+    const Lvl& L = h->L[l];
+    View<T> v;
+    v.p = (const T*)h->B[l].rhs;
+    v.global = 0;
+    v.sy = L.py;
+    v.sz = L.pz;
+    v.ss = L.ss;
+    return v;
+  }
+
+  // S^deg(L_l, u_l, b) on C_l of every segment (R8): ping-pong between the two buffers
+  void cheb(int l, int deg, View<T> b) {
+    if (deg <= 0) return;
+    const Lvl& L = h->L[l];
+    LevelBufs& bb = h->B[l];
+    const CellCounts& c = h->cells[l];
+    int lat = bb.cur, oth = 1 - bb.cur;
+    {
+      Launch g(h, st, KC_CHEB, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
+      srfmg::launch_cheb_step<T>(L, (const T*)bb.u[lat], nullptr, b, (T*)bb.u[oth], 0.0,
+                                 1.0 / h->theta[l], 1, st);
+    }
+    std::swap(lat, oth);
+    double rho_prev = 1.0 / h->sigma[l];
+    for (int k = 1; k < deg; ++k) {
+      const double rho = 1.0 / (2.0 * h->sigma[l] - rho_prev);
+      {
+        Launch g(h, st, KC_CHEB, l, w * 4.0 * c.compute);
+        srfmg::launch_cheb_step<T>(L, (const T*)bb.u[lat], (const T*)bb.u[oth], b,
+                                   (T*)bb.u[oth], rho * rho_prev, 2.0 * rho / h->delta[l], 0,
+                                   st);
+      }
+      std::swap(lat, oth);
+      rho_prev = rho;
+    }
+    bb.cur = lat;
+  }
+
+  int jr_for(int l) {  // restriction / F half-width for fine level l -> coarse l-1
+    return (l - 1 > h->T) ? h->L[l].J / 2 : 0;
+  }
+
+  void coarsest(View<T> b) {
+    Launch g(h, st, KC_COARSEST, 0, 0.0);
+    srfmg::launch_coarsest<T>(h->L[0], U(0), b, (const T*)h->ainv, st);
+  }
+
+  void prolong(int l, int add) {
+    const CellCounts& c = h->cells[l];
+    Launch g(h, st, KC_PROLONG, l,
+             w * (add ? 2.0 : 1.0) * c.cg + w * (add ? 2.0 : 1.0) * h->cells[l - 1].cg / 8.0);
+    srfmg::launch_prolong<T>(h->L[l], U(l), h->L[l - 1], U(l - 1), (const T*)h->B[l - 1].t, add,
+                             st);
+  }
+
+  // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors
+  void vcycle(int l, View<T> b) {
+    if (l == 0) {  // L120-121: exact solve
+      coarsest(b);
+      return;
+    }
+    cheb(l, h->d.nu1, b);  // L112 / L232
+    const int jr = jr_for(l);
+    {
+      const Lvl& Lf = h->L[l];
+      double tgt = h->L[l].nsegs;
+      for (int i = 0; i < 3; ++i) tgt *= (Lf.S[i] / 2 + 2 * jr);
+      Launch g(h, st, KC_RESTRICT, l, w * (16.0 + 2.0) * tgt);
+      srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
+                                st);  // L113-115 / L233, L235
+    }
+    {
+      const CellCounts& c = h->cells[l - 1];
+      Launch g(h, st, KC_TAU, l - 1, w * (2.0 * c.storage + 2.0 * c.compute));
+      srfmg::launch_tau<T>(h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, (T*)h->B[l - 1].t, jr,
+                           st);  // L116-117 / L234-236
+    }
+    vcycle(l - 1, sview(l - 1));  // L117 / L237-240
+    prolong(l, 1);                // L118 / L241
+    cheb(l, h->d.nu2, b);         // L119 / L242
+  }
+
+  void run(T* uout) {
+    const int M = h->M;
+    for (int l = M; l >= 1; --l) {  // R6: f pyramid
+      const Lvl& L = h->L[l];
+      Launch g(h, st, KC_PYRAMID, l, w * (double)L.N[0] * L.N[1] * L.N[2] * (1.0 + 1.0 / 8));
+      srfmg::launch_pyramid<T>(l == M ? f : (const T*)h->B[l].fpyr, L.N[0], L.N[1], L.N[2],
+                               (T*)h->B[l - 1].fpyr, st);
+    }
+    coarsest(fview(0));  // fig:fmg L137-138
+    for (int l = 1; l <= M; ++l) {  // fig:fmg L139-142 (l <= T), fig:fmgsr L220-223 (l > T)
+      prolong(l, 0);                // Pi onto C ∪ GSR
+      cheb(l, h->d.alpha, fview(l));
+      vcycle(l, fview(l));
+    }
+    {
+      const Lvl& L = h->L[M];
+      Launch g(h, st, KC_GATHER, M, w * 2.0 * L.N[0] * (double)L.N[1] * L.N[2]);
+      srfmg::launch_gather<T>(L, U(M), uout, st);  // R19
+    }
+  }
+};
+
+sr_status_t enqueue_solve(sr_fmg* h, const void* f, void* u, cudaStream_t st) {
+  h->launches = 0;
+  h->prof_used = 0;
+  for (int l = 0; l <= h->M; ++l) h->B[l].cur = 0;
+  if (h->esize == 8) {
+    Schedule<double> s{h, st, (const double*)f, 8.0};
+    s.run((double*)u);
+  } else {
+    Schedule<float> s{h, st, (const float*)f, 4.0};
+    s.run((float*)u);
+  }
+  if (h->sticky != SR_OK) return h->sticky;
+  CU(h, cudaGetLastError());
+  return SR_OK;
+}
+
+double alg_bytes(const sr_fmg* h) {
+  // B_alg: 5.5 words per compute cell per level visit, the f pyramid
+  // (8/7 N^3 words) and the output (N^3 words)
+  double words = 0;
+  for (int l = 1; l <= h->M; ++l) words += 5.5 * (double)h->visits[l] * h->cells[l].compute;
+  const Lvl& L = h->L[h->M];
+  const double n = (double)L.N[0] * L.N[1] * L.N[2];
+  words += n * (8.0 / 7.0) + n;
+  return words * h->esize;
+}
+
+void free_all(sr_fmg* h) {
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto& b : h->B) {
+    cudaFree(b.u[0]);
+    cudaFree(b.u[1]);
+    cudaFree(b.rhs);
+    cudaFree(b.t);
+    cudaFree(b.fpyr);
+  }
+  cudaFree(h->ainv);
+  cudaFree(h->host_f);
+  cudaFree(h->host_u);
+  for (auto& r : h->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  if (h->cap) cudaStreamDestroy(h->cap);
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+void sr_fmg_desc_init(sr_fmg_desc_t* d) {
+  if (!d) return;
+  std::memset(d, 0, sizeof(*d));
+  d->buffer = 2;
+  d->sched_A = -1;
+  d->sched_B = -1;
+  d->dtype = SR_F64;
+  d->alpha = 1;
+  d->nu1 = 2;
+  d->nu2 = 2;
+  d->cheb_lo = 1.0 / 6.0;
+  d->cheb_hi = 1.0;
+  d->world = 1;
+  d->pgrid[0] = d->pgrid[1] = d->pgrid[2] = 1;
+  d->device = -1;
+  d->use_graph = 1;
+}
+
+sr_status_t sr_fmg_create(int64_t N, int32_t M, int32_t seg, int32_t buffer, int32_t sr_levels,
+                          sr_fmg_t** out) {
+  sr_fmg_desc_t d;
+  sr_fmg_desc_init(&d);
+  d.n[0] = d.n[1] = d.n[2] = N;
+  d.M = M;
+  d.seg = seg;
+  d.buffer = buffer;
+  d.sr_levels = sr_levels;
+  return sr_fmg_create_ex(&d, out);
+}
+
+sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
+  if (!out) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!d) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "descriptor is NULL");
+  std::string msg;
+  sr_status_t st = validate(d, msg);
+  if (st != SR_OK) return fail(nullptr, st, msg);
+
+  sr_fmg* h = new sr_fmg();
+  h->d = *d;
+  make_plan(h);
+  for (int l = 1; l <= h->M; ++l) {
+    const Lvl &Lf = h->L[l], &Lc = h->L[l - 1];
+    if (l - 1 > h->T && Lc.J < (Lf.J + 1) / 2) {
+      delete h;
+      return fail(nullptr, SR_ERR_UNSUPPORTED_CONFIG,
+                  "buffer schedule violates J_{l-1} >= ceil(J_l/2) (prolongation footprint)");
+    }
+    if ((long long)Lf.E[0] * Lf.E[1] * Lf.E[2] >= (1LL << 31)) {
+      delete h;
+      return fail(nullptr, SR_ERR_UNSUPPORTED_CONFIG, "segment storage box too large");
+    }
+  }
+  {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      delete h;
+      return fail(nullptr, SR_ERR_CUDA,
+                  std::string("no CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+    }
+  }
+  const char* sd = std::getenv("SR_FMG_SYNC");
+  h->sync_debug = sd && sd[0] == '1';
+  if (d->device >= 0) {
+    cudaError_t e = cudaSetDevice(d->device);
+    if (e != cudaSuccess) {
+      delete h;
+      return fail(nullptr, SR_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+  }
+  h->stream = (cudaStream_t)d->stream;
+  h->B.assign(h->M + 1, LevelBufs{});
+  auto alloc = [&](void** p, size_t bytes) -> bool {
+    if (bytes == 0) bytes = 16;
+    if (cudaMalloc(p, bytes) != cudaSuccess) return false;
+    h->workspace += (long long)bytes;
+    return cudaMemset(*p, 0, bytes) == cudaSuccess;
+  };
+  bool ok = true;
+  for (int l = 0; l <= h->M && ok; ++l) {
+    const Lvl& L = h->L[l];
+    const size_t bytes = (size_t)L.ss * L.nsegs * h->esize;
+    ok = ok && alloc(&h->B[l].u[0], bytes) && alloc(&h->B[l].u[1], bytes);
+    if (l < h->M) {
+      ok = ok && alloc(&h->B[l].rhs, bytes) && alloc(&h->B[l].t, bytes);
+      ok = ok && alloc(&h->B[l].fpyr, (size_t)L.N[0] * L.N[1] * L.N[2] * h->esize);
+    }
+  }
+  std::vector<double> inv = coarsest_inverse(h->L[0]);
+  const size_t n0sq = inv.size();
+  ok = ok && alloc(&h->ainv, n0sq * h->esize);
+  if (ok) {
+    if (h->esize == 8) {
+      ok = cudaMemcpy(h->ainv, inv.data(), n0sq * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+    } else {
+      std::vector<float> f32(inv.begin(), inv.end());
+      ok = cudaMemcpy(h->ainv, f32.data(), n0sq * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+  }
+  if (ok) ok = cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    free_all(h);
+    delete h;
+    return fail(nullptr, SR_ERR_OUT_OF_MEMORY, "device allocation failed");
+  }
+  *out = h;
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_set_stream(sr_fmg_t* h, void* stream) {
+  if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
+  h->stream = (cudaStream_t)stream;
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_solve(sr_fmg_t* h, const void* f, void* u) {
+  if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->sticky != SR_OK) return h->sticky;
+  if (!f || !u) return fail(h, SR_ERR_INVALID_ARGUMENT, "f or u is NULL");
+  if (((uintptr_t)f & 15) || ((uintptr_t)u & 15))
+    return fail(h, SR_ERR_INVALID_ARGUMENT, "f and u must be 16-byte aligned");
+  const bool graph = h->d.use_graph && !h->sync_debug;
+  if (!graph) return enqueue_solve(h, f, u, h->stream);
+  if (!h->gexec || h->g_f != f || h->g_u != u) {
+    if (h->gexec) {
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+    CU(h, cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    sr_status_t st = enqueue_solve(h, f, u, h->cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    if (st != SR_OK) return st;
+    if (e != cudaSuccess) return fail(h, SR_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&h->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, SR_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    h->g_f = f;
+    h->g_u = u;
+  }
+  CU(h, cudaGraphLaunch(h->gexec, h->stream));
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_solve_host(sr_fmg_t* h, const void* f_host, void* u_host) {
+  if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->sticky != SR_OK) return h->sticky;
+  if (!f_host || !u_host) return fail(h, SR_ERR_INVALID_ARGUMENT, "f or u is NULL");
+  const Lvl& L = h->L[h->M];
+  const size_t bytes = (size_t)L.N[0] * L.N[1] * L.N[2] * h->esize;
+  if (!h->host_f) {
+    CU(h, cudaMalloc(&h->host_f, bytes));
+    CU(h, cudaMalloc(&h->host_u, bytes));
+  }
+  CU(h, cudaMemcpyAsync(h->host_f, f_host, bytes, cudaMemcpyHostToDevice, h->stream));
+  sr_status_t st = sr_fmg_solve(h, h->host_f, h->host_u);
+  if (st != SR_OK) return st;
+  CU(h, cudaMemcpyAsync(u_host, h->host_u, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  return SR_OK;
+}
+
+void sr_fmg_destroy(sr_fmg_t* h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->stream);
+  free_all(h);
+  delete h;
+}
+
+sr_status_t sr_fmg_get_info(const sr_fmg_t* h, sr_fmg_info_t* info) {
+  if (!h || !info) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "NULL argument");
+  std::memset(info, 0, sizeof(*info));
+  info->M = h->M;
+  info->K = h->K;
+  info->T = h->T;
+  info->dtype = h->d.dtype;
+  for (int l = 0; l <= h->M; ++l) {
+    const Lvl& L = h->L[l];
+    for (int i = 0; i < 3; ++i) {
+      info->n_level[l][i] = L.N[i];
+      info->nseg[l][i] = L.ns[i];
+      info->storage_ext[l][i] = L.E[i];
+    }
+    info->storage_pitch[l][0] = L.py;
+    info->storage_pitch[l][1] = L.pz;
+    info->storage_pitch[l][2] = L.ss;
+    info->sr[l] = l > h->T;
+    info->seg_level[l] = L.S[0];
+    info->buffer_level[l] = L.J;
+    info->compute_cells[l] = h->cells[l].compute;
+    info->visits[l] = h->visits[l];
+  }
+  info->workspace_bytes = h->workspace;
+  // count launches of one solve without enqueuing: dry count from the schedule shape
+  long long n = 0;
+  {
+    // pyramid M, coarsest 1, per FMG level l: prolong + alpha + vcycle(l)
+    auto cheb_n = [&](int deg) { return deg > 0 ? deg : 0; };
+    std::vector<long long> vc(h->M + 1, 0);
+    vc[0] = 1;
+    for (int l = 1; l <= h->M; ++l)
+      vc[l] = cheb_n(h->d.nu1) + 2 + vc[l - 1] + 1 + cheb_n(h->d.nu2);
+    n = h->M + 1 + 1;
+    for (int l = 1; l <= h->M; ++l) n += 1 + cheb_n(h->d.alpha) + vc[l];
+  }
+  info->launches_per_solve = n;
+  info->alg_bytes_per_solve = alg_bytes(h);
+  return SR_OK;
+}
+
+const char* sr_fmg_last_error(const sr_fmg_t* h) {
+  if (h) return h->err.c_str();
+  return g_tls_err.c_str();
+}
+
+int32_t sr_fmg_kernel_count(void) { return srfmg::kNumKernelNames; }
+const char* sr_fmg_kernel_name(int32_t i) {
+  if (i < 0 || i >= srfmg::kNumKernelNames) return "";
+  return srfmg::kKernelNames[i];
+}
+
+// ---- profiling (used by bench.py): CUDA events around every launch of one kernel class
+// at one level, recorded inside the captured graph of the next solves.
+sr_status_t sr_fmg_profile_select(sr_fmg_t* h, int32_t kernel_class, int32_t level) {
+  if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
+  h->prof_cls = kernel_class;
+  h->prof_level = level;
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  return SR_OK;
+}
+
+// After a solve has completed: total device time (ms), algorithmic bytes and the number
+// of profiled launches of that solve.
+sr_status_t sr_fmg_profile_read(sr_fmg_t* h, double* ms, double* bytes, int32_t* launches) {
+  if (!h || !ms || !bytes || !launches) return fail(h, SR_ERR_INVALID_ARGUMENT, "NULL argument");
+  double t = 0, b = 0;
+  for (size_t i = 0; i < h->prof_used; ++i) {
+    float x = 0;
+    CU(h, cudaEventElapsedTime(&x, h->prof[i].a, h->prof[i].b));
+    t += x;
+    b += h->prof[i].bytes;
+  }
+  *ms = t;
+  *bytes = b;
+  *launches = (int32_t)h->prof_used;
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_debug_level_io(sr_fmg_t* h, int32_t level, int32_t field, int32_t write,
+                                  void* host) {
+  if (!h || !host) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (level < 0 || level > h->M) return fail(h, SR_ERR_INVALID_ARGUMENT, "bad level");
+  LevelBufs& b = h->B[level];
+  void* p = field == 0 ? b.u[b.cur] : field == 1 ? b.rhs : field == 2 ? b.t : nullptr;
+  if (!p) return fail(h, SR_ERR_INVALID_ARGUMENT, "field not present on this level");
+  const Lvl& L = h->L[level];
+  const size_t bytes = (size_t)L.ss * L.nsegs * h->esize;
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (write) {
+    CU(h, cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice));
+    if (field == 0) CU(h, cudaMemcpy(b.u[1 - b.cur], host, bytes, cudaMemcpyHostToDevice));
+  } else {
+    CU(h, cudaMemcpy(host, p, bytes, cudaMemcpyDeviceToHost));
+  }
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_debug_op(sr_fmg_t* h, int32_t op, int32_t level, int32_t deg,
+                            const void* f_dev) {
+  if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (level < 0 || level > h->M) return fail(h, SR_ERR_INVALID_ARGUMENT, "bad level");
+  if ((op == 1 || op == 3 || op == 4) && level < 1)
+    return fail(h, SR_ERR_INVALID_ARGUMENT, "op needs level >= 1");
+  if (op == 2 && level >= h->M) return fail(h, SR_ERR_INVALID_ARGUMENT, "tau needs level < M");
+  cudaStream_t st = h->stream;
+  auto body = [&](auto tag) -> sr_status_t {
+    using T = decltype(tag);
+    Schedule<T> s{h, st, (const T*)f_dev, (double)sizeof(T)};
+    auto rhs = [&](int l) { return (l == h->M) ? s.fview(l) : s.sview(l); };
+    switch (op) {
+      case 0: s.cheb(level, deg, rhs(level)); break;
+      case 1:
+        srfmg::launch_restrict<T>(h->L[level], s.U(level), rhs(level), h->L[level - 1],
+                                  s.U(level - 1), (T*)h->B[level - 1].rhs, s.jr_for(level), st);
+        break;
+      case 2:
+        srfmg::launch_tau<T>(h->L[level], s.U(level), (T*)h->B[level].rhs, (T*)h->B[level].t,
+                             s.jr_for(level + 1), st);
+        break;
+      case 3: s.prolong(level, 0); break;
+      case 4: s.prolong(level, 1); break;
+      case 5: s.coarsest(s.sview(0)); break;
+      default: return fail(h, SR_ERR_INVALID_ARGUMENT, "unknown op");
+    }
+    return SR_OK;
+  };
+  if (op == 0 && level == h->M && !f_dev)
+    return fail(h, SR_ERR_INVALID_ARGUMENT, "level M smoothing needs f_dev");
+  sr_status_t r = h->esize == 8 ? body(double{}) : body(float{});
+  if (r != SR_OK) return r;
+  CU(h, cudaGetLastError());
+  CU(h, cudaStreamSynchronize(st));
+  return SR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+"""GPU path vs the CPU oracle, through the C ABI (needs a B200).
+
+Tolerances (north_star / DESIGN.md §4): fp64 relative L2 <= 1e-11, fp32 (against the fp64
+oracle) <= 1e-4.  Kernel-level tests load identical seeded data into the library's internal
+level storage (test hook) and compare one kernel with the oracle function it implements.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from oracle import Box, Field
+from tests.gpu_helpers import (from_fields, oracle_seg_index, rel_l2, seg_array, storage_box,
+                               to_fields)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from paper_1406_7808_b200 import Solver  # noqa: E402
+
+TOL64, TOL32 = 1e-11, 1e-4
+
+
+def _gpu_solve(f, **kw):
+    with Solver(**kw) as s:
+        ft = torch.from_numpy(f.astype(np.float64 if kw.get("dtype", "f64") == "f64"
+                                       else np.float32)).cuda()
+        return s.solve(ft).cpu().numpy().astype(np.float64)
+
+
+_ORACLE = {}
+
+
+def _oracle(f_key, f, n, M, seg, buffer, K, sched=None):
+    key = (f_key, n, M, seg, buffer, K, sched)
+    if key not in _ORACLE:
+        _ORACLE[key] = O.solve(f, O.Config(n=n, M=M, seg=seg, buffer=buffer, K=K, sched=sched))
+    return _ORACLE[key]
+
+
+SOLVE_CASES = [
+    # (name, n, M, seg, J, K, rhs)
+    ("C1", (32, 32, 32), 4, 16, 2, 2, "manufactured"),
+    ("C1-noise", (32, 32, 32), 4, 16, 2, 2, "manufactured+noise"),
+    ("conv-K0", (64, 64, 64), 5, 0, 0, 0, "manufactured+noise"),
+    ("C2-J1", (128, 128, 128), 6, 32, 1, 3, "manufactured"),
+    ("C2-J2", (128, 128, 128), 6, 32, 2, 3, "manufactured"),
+    ("C2-J4", (128, 128, 128), 6, 32, 4, 3, "manufactured"),
+    ("J0", (64, 64, 64), 5, 16, 0, 2, "manufactured+noise"),
+    ("J3", (64, 64, 64), 5, 16, 3, 3, "bumps"),
+    ("K=M", (16, 16, 16), 3, 8, 2, 3, "random"),
+    ("C3-like-64", (64, 64, 64), 5, 8, 2, 3, "manufactured+noise"),
+    ("noncubic", (64, 32, 32), 4, 16, 2, 2, "manufactured+noise"),
+    ("one-seg", (32, 32, 32), 4, 32, 2, 3, "random"),
+]
+
+
+@pytest.mark.parametrize("case", SOLVE_CASES, ids=[c[0] for c in SOLVE_CASES])
+def test_solve_fp64_matches_oracle(case):
+    name, n, M, seg, J, K, rhs = case
+    h = 1.0 / n[0]
+    f = W.make_rhs(rhs, n, h)
+    ref = _oracle(rhs, f, n, M, seg, J, K)
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
+    assert np.isfinite(u).all()
+    assert rel_l2(u, ref) <= TOL64, rel_l2(u, ref)
+
+
+@pytest.mark.parametrize("case", [SOLVE_CASES[1], SOLVE_CASES[4], SOLVE_CASES[9]],
+                         ids=["C1-noise", "C2-J2", "C3-like-64"])
+def test_solve_fp32_matches_fp64_oracle(case):
+    name, n, M, seg, J, K, rhs = case
+    f = W.make_rhs(rhs, n)
+    ref = _oracle(rhs, f, n, M, seg, J, K)
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype="f32")
+    assert rel_l2(u, ref) <= TOL32, rel_l2(u, ref)
+
+
+def test_eq5_schedule_matches_oracle():
+    n = (64, 64, 64)
+    f = W.make_rhs("manufactured+noise", n)
+    ref = _oracle("mn", f, n, 5, 16, 2, 3, sched=(2, 1))
+    with Solver(n, 5, seg=16, buffer=2, K=3, sched=(2, 1)) as s:
+        assert [s.level(l).buffer for l in (3, 4, 5)] == [4, 2, 2]   # J_k = 2 floor((2+(3-k))/2)
+        u = s.solve(torch.from_numpy(f).cuda()).cpu().numpy()
+    assert rel_l2(u, ref) <= TOL64
+
+
+def test_graph_and_eager_and_host_paths_bitwise_equal():
+    n = (64, 64, 64)
+    f = W.make_rhs("manufactured+noise", n)
+    ft = torch.from_numpy(f).cuda()
+    with Solver(n, 5, seg=16, buffer=2, K=3) as s:
+        a = s.solve(ft).cpu().numpy()
+        b = s.solve(ft).cpu().numpy()          # graph replay
+        c = s.solve_host(f).numpy()             # host API
+    with Solver(n, 5, seg=16, buffer=2, K=3, use_graph=False) as s:
+        d = s.solve(ft).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
+
+
+def test_final_level_state_matches_oracle():
+    # every SR level's final segment storage (u on C ∪ GSR) agrees with the oracle's
+    n, M, S, J, K = (32, 32, 32), 4, 16, 2, 2
+    f = W.make_rhs("manufactured+noise", n)
+    o = O.Oracle(O.Config(n=n, M=M, seg=S, buffer=J, K=K))
+    o.solve(f)
+    with Solver(n, M, seg=S, buffer=J, K=K, use_graph=False) as s:
+        s.solve(torch.from_numpy(f).cuda())
+        torch.cuda.synchronize()
+        for l in range(o.T + 1, M + 1):
+            li = s.level(l)
+            flds = to_fields(s.level_storage(l, 0), li)
+            for k, fld in enumerate(flds):
+                p = oracle_seg_index(li, k)
+                CG = o.CG(l, p)
+                assert fld.box == o.storage(l, p)
+                assert rel_l2(fld[CG], o.us[l][p][CG]) <= TOL64, (l, p)
+
+
+# ---------------------------------------------------------------------------- kernels
+N0, M0, S0, J0, K0 = (32, 32, 32), 4, 16, 2, 2   # T = 2; levels 3, 4 are SR
+
+
+def _random_fields(s, l, seed):
+    li = s.level(l)
+    rng = np.random.default_rng(seed)
+    nsegs = li.nseg[0] * li.nseg[1] * li.nseg[2]
+    buf = rng.standard_normal(nsegs * li.pitch[2])
+    return li, buf
+
+
+def _dom(l):
+    N = [v >> (M0 - l) for v in N0]
+    return Box((0, 0, 0), (N[2], N[1], N[0]))
+
+
+def _h(l):
+    return (1.0 / N0[0]) * 2 ** (M0 - l)
+
+
+@pytest.fixture(scope="module")
+def ksolver():
+    s = Solver(N0, M0, seg=S0, buffer=J0, K=K0, use_graph=False)
+    yield s
+    s.close()
+
+
+def _oracle_regions(l):
+    return O.Oracle(O.Config(n=N0, M=M0, seg=S0, buffer=J0, K=K0))
+
+
+@pytest.mark.parametrize("l,deg", [(3, 1), (3, 2), (2, 2), (1, 3)])
+def test_kernel_chebyshev(ksolver, l, deg):
+    s = ksolver
+    li, ubuf = _random_fields(s, l, 1)
+    _, bbuf = _random_fields(s, l, 2)
+    s.set_level_storage(l, 0, ubuf)
+    s.set_level_storage(l, 1, bbuf)
+    s.debug_op(0, l, deg)
+    got = to_fields(s.level_storage(l, 0), li)
+    us, bs = to_fields(ubuf, li), to_fields(bbuf, li)
+    o = _oracle_regions(l)
+    for k in range(len(us)):
+        X = o.C(l, oracle_seg_index(li, k)) if l > o.T else _dom(l)
+        CG = storage_box(li, k).intersect(_dom(l))
+        O.cheb(deg, us[k], bs[k], X, _h(l), _dom(l), 1 / 6, 1.0)
+        assert rel_l2(got[k][CG], us[k][CG]) <= 1e-13
+
+
+@pytest.mark.parametrize("l", [4, 3, 2])
+def test_kernel_residual_restriction(ksolver, l):
+    s = ksolver
+    o = _oracle_regions(l)
+    li, ubuf = _random_fields(s, l, 3)
+    lc = s.level(l - 1)
+    s.set_level_storage(l, 0, ubuf)
+    f = None
+    if l == M0:
+        fa = W.random_field(N0, seed=4)
+        f = torch.from_numpy(fa).cuda()
+        bfields = None
+    else:
+        _, bbuf = _random_fields(s, l, 4)
+        s.set_level_storage(l, 1, bbuf)
+        bfields = to_fields(bbuf, li)
+    # poison the coarse targets so untouched cells are visible
+    _, cb = _random_fields(s, l - 1, 5)
+    s.set_level_storage(l - 1, 0, cb)
+    s.set_level_storage(l - 1, 1, cb)
+    s.debug_op(1, l, 0, f)
+    got_u = to_fields(s.level_storage(l - 1, 0), lc)
+    got_r = to_fields(s.level_storage(l - 1, 1), lc)
+    us = to_fields(ubuf, li)
+    for k in range(len(us)):
+        p = oracle_seg_index(li, k)
+        X = o.C(l, p) if l > o.T else _dom(l)
+        if bfields is None:
+            b = Field(_dom(l), array=fa)
+        else:
+            b = bfields[k]
+        r = Field(X, array=O.residual(us[k], b, X, _h(l), _dom(l)))
+        if l - 1 > o.T:
+            tgt, kc = o.F(l, p), k
+        else:
+            tgt = (o.V(l - 1, p) if l > o.T else _dom(l - 1))
+            kc = 0
+        assert rel_l2(got_u[kc][tgt], O.restrict_avg8(us[k], tgt)) <= 1e-14
+        assert rel_l2(got_r[kc][tgt], O.restrict_avg8(r, tgt)) <= 1e-13
+
+
+@pytest.mark.parametrize("l", [3, 2])
+def test_kernel_tau(ksolver, l):
+    s = ksolver
+    o = _oracle_regions(l)
+    li, ubuf = _random_fields(s, l, 6)
+    _, rbuf = _random_fields(s, l, 7)
+    s.set_level_storage(l, 0, ubuf)
+    s.set_level_storage(l, 1, rbuf)
+    s.debug_op(2, l, 0)
+    got_b = to_fields(s.level_storage(l, 1), li)
+    got_t = to_fields(s.level_storage(l, 2), li)
+    us, rs = to_fields(ubuf, li), to_fields(rbuf, li)
+    for k in range(len(us)):
+        p = oracle_seg_index(li, k)
+        assert np.array_equal(got_t[k].a, us[k].a)
+        C = o.C(l, p) if l > o.T else _dom(l)
+        F = o.F(l + 1, p) if l > o.T else _dom(l)
+        O.fill_bc_ghosts(us[k], _dom(l))
+        b = Field(C, array=O.apply_A(us[k], C, _h(l)))
+        b[F] = rs[k][F] + O.apply_A(us[k], F, _h(l))
+        assert rel_l2(got_b[k][C], b[C]) <= 1e-13
+
+
+@pytest.mark.parametrize("l,add", [(4, 0), (4, 1), (3, 0), (3, 1), (2, 1)])
+def test_kernel_prolongation(ksolver, l, add):
+    s = ksolver
+    o = _oracle_regions(l)
+    li, ubuf = _random_fields(s, l, 8)
+    lc, wbuf = _random_fields(s, l - 1, 9)
+    _, tbuf = _random_fields(s, l - 1, 10)
+    s.set_level_storage(l, 0, ubuf)
+    s.set_level_storage(l - 1, 0, wbuf)
+    s.set_level_storage(l - 1, 2, tbuf)
+    s.debug_op(4 if add else 3, l, 0)
+    got = to_fields(s.level_storage(l, 0), li)
+    us, ws, ts = to_fields(ubuf, li), to_fields(wbuf, lc), to_fields(tbuf, lc)
+    for k in range(len(us)):
+        kc = k if l - 1 > o.T else 0
+        src = Field(ws[kc].box, array=ws[kc].a - ts[kc].a) if add else ws[kc]
+        O.fill_bc_ghosts(src, _dom(l - 1))
+        CG = storage_box(li, k).intersect(_dom(l))
+        exp = O.prolong(src, CG) + (us[k][CG] if add else 0.0)
+        assert rel_l2(got[k][CG], exp) <= 1e-14
+
+
+def test_kernel_coarsest(ksolver):
+    s = ksolver
+    li, ubuf = _random_fields(s, 0, 11)
+    _, bbuf = _random_fields(s, 0, 12)
+    s.set_level_storage(0, 1, bbuf)
+    s.debug_op(5, 0, 0)
+    got = to_fields(s.level_storage(0, 0), li)[0]
+    b = to_fields(bbuf, li)[0]
+    d0 = _dom(0)
+    assert rel_l2(got[d0], O.exact_solve(b[d0], d0, _h(0))) <= 1e-13
+
+
+# ---------------------------------------------------------------------------- full size
+def _c3(dtype="f64", N=512, M=8, rhs="manufactured+noise"):
+    n = (N, N, N)
+    f = W.make_rhs(rhs, n)
+    with Solver(n, M, seg=N // 8, buffer=2, K=4, dtype=dtype) as s:
+        ft = torch.from_numpy(f.astype(np.float64 if dtype == "f64" else np.float32)).cuda()
+        a = s.solve(ft)
+        b = s.solve(ft)
+        same = bool(torch.equal(a, b))
+        return f, a.double().cpu().numpy(), same
+
+
+def test_full_size_c3_properties():
+    # C3 at full size in bench.py's launch configuration (graph replay): deterministic,
+    # finite, fp32 within 1e-4 of fp64, and 2nd-order error against the manufactured
+    # solution at the same segment grid (256^3 vs 512^3)
+    f, u64, same = _c3("f64", rhs="manufactured")
+    assert same and np.isfinite(u64).all()
+    _, u32, _ = _c3("f32", rhs="manufactured")
+    assert rel_l2(u32, u64) <= TOL32
+    e512 = np.abs(u64 - W.manufactured_u((512,) * 3, 1 / 512)).max()
+    _, u256, _ = _c3("f64", N=256, M=7, rhs="manufactured")
+    e256 = np.abs(u256 - W.manufactured_u((256,) * 3, 1 / 256)).max()
+    assert 2.5 < e256 / e512 < 4.6, (e256, e512)
+
+
+def test_full_size_symmetry():
+    # a mirror/swap-symmetric f on the symmetric 8^3 segment grid gives a symmetric u
+    n = (512, 512, 512)
+    f = W.make_rhs("bumps", n)
+    f = f + f[:, :, ::-1]
+    f = f + f[:, ::-1, :]
+    f = f + np.transpose(f, (0, 2, 1))
+    with Solver(n, 8, seg=64, buffer=2, K=4) as s:
+        u = s.solve(torch.from_numpy(np.ascontiguousarray(f)).cuda()).cpu().numpy()
+    sc = np.abs(u).max()
+    assert np.abs(u - u[:, :, ::-1]).max() <= 1e-12 * sc
+    assert np.abs(u - np.transpose(u, (0, 2, 1))).max() <= 1e-12 * sc
