@@ -266,11 +266,11 @@ struct Launch {
       }
       rec = &h->prof[h->prof_used++];
       rec->bytes = bytes;
-      cudaEventRecord(rec->a, st);
+      cudaEventRecordWithFlags(rec->a, st, cudaEventRecordExternal);
     }
   }
   ~Launch() {
-    if (rec) cudaEventRecord(rec->b, st);
+    if (rec) cudaEventRecordWithFlags(rec->b, st, cudaEventRecordExternal);
     if (h->sync_debug) {
       cudaError_t e = cudaStreamSynchronize(st);
       if (e == cudaSuccess) e = cudaGetLastError();
