@@ -59,46 +59,80 @@ __device__ __forceinline__ T apply_A(const Lvl& L, const T* __restrict__ u, long
 }
 
 // ------------------------------------------------------------------------------------
+// Column-marching thread layout shared by the segment kernels: a CTA covers a (bx, by)
+// tile of one segment's storage plane, each thread owns one (x, y) column and marches z
+// over a chunk of planes, keeping the z-neighbours of its column in registers.  No
+// per-cell integer division; domain/region tests are hoisted per column.
+// ------------------------------------------------------------------------------------
+struct Col {
+  int ax, ay;   // local storage column
+  int z0, z1;   // local z chunk [z0, z1)
+};
+
+__device__ __forceinline__ bool col_index(int ex, int ey, int ez, int ntx, int zchunk, Col& c) {
+  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+  c.ax = tx * blockDim.x + threadIdx.x;
+  c.ay = ty * blockDim.y + threadIdx.y;
+  c.z0 = blockIdx.z * zchunk;
+  c.z1 = min(ez, c.z0 + zchunk);
+  return c.ax < ex && c.ay < ey && c.z0 < c.z1;
+}
+
+// ------------------------------------------------------------------------------------
 // One Chebyshev step (R8) on the compute region C = grow(V,J) ∩ Omega
 // (fig:fmgsr L222, fig:mgvsr L232/L242):
 //   out = cur + c_mom (cur - prev) + c_res (b - A cur)      on C
 //   out = cur                                               on GSR (if copy_gsr)
+// A = -Lap_h, 7 points (R1/R2); a neighbour outside Omega is the reflected ghost -u_i (R3,
+// PAPER.md:161); neighbour sum order z-, z+, y-, y+, x-, x+ (as the oracle).
 // prev may alias out (in-place second step: each thread reads prev at its own cell only).
 // ------------------------------------------------------------------------------------
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restrict__ cur,
                                                         const T* prev, View<T> b, T* out,
-                                                        T c_mom, T c_res, int copy_gsr) {
+                                                        T c_mom, T c_res, int copy_gsr, int ntx,
+                                                        int zchunk) {
+  Col c;
+  if (!col_index(L.E[0], L.E[1], L.E[2], ntx, zchunk, c)) return;
   const int s = blockIdx.y;
-  const int Ex = L.E[0], Ey = L.E[1], Ez = L.E[2];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= Ex * Ey * Ez) return;
-  int a[3];
-  a[0] = idx % Ex;
-  const int t = idx / Ex;
-  a[1] = t % Ey;
-  a[2] = t / Ey;
-  int p[3], o[3], g[3];
+  int p[3], o[3];
   seg_coords(L, s, p);
   seg_origin(L, p, o);
-  bool in = true, interior = true;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    g[d] = o[d] + a[d];
-    in = in && (g[d] >= 0) && (g[d] < L.N[d]);
-    interior = interior && (a[d] >= 1) && (a[d] <= L.E[d] - 2);
+  const int gx = o[0] + c.ax, gy = o[1] + c.ay;
+  if (gx < 0 || gx >= L.N[0] || gy < 0 || gy >= L.N[1]) return;
+  const bool cxy = c.ax >= 1 && c.ax <= L.E[0] - 2 && c.ay >= 1 && c.ay <= L.E[1] - 2;
+  const bool xm = gx > 0, xp = gx < L.N[0] - 1, ym = gy > 0, yp = gy < L.N[1] - 1;
+  const long long col = (long long)s * L.ss + (long long)c.ay * L.py + c.ax;
+  const T* cc = cur + col;
+  const T* bc = b.global ? b.p + (long long)gy * b.sy + gx : b.p + (long long)s * b.ss +
+                                                                 (long long)c.ay * b.sy + c.ax;
+  const long long pz = L.pz, py = L.py;
+  T zm = c.z0 > 0 ? cc[(long long)(c.z0 - 1) * pz] : T(0);
+  T v0 = cc[(long long)c.z0 * pz];
+  for (int az = c.z0; az < c.z1; ++az) {
+    const long long zo = (long long)az * pz;
+    const T zp = (az + 1 < L.E[2]) ? cc[zo + pz] : T(0);
+    const int gz = o[2] + az;
+    if (gz >= 0 && gz < L.N[2]) {
+      if (cxy && az >= 1 && az <= L.E[2] - 2) {
+        T sum = (gz > 0) ? zm : -v0;
+        sum += (gz < L.N[2] - 1) ? zp : -v0;
+        sum += ym ? cc[zo - py] : -v0;
+        sum += yp ? cc[zo + py] : -v0;
+        sum += xm ? cc[zo - 1] : -v0;
+        sum += xp ? cc[zo + 1] : -v0;
+        const long long bz = b.global ? (long long)gz * b.sz : (long long)az * b.sz;
+        const T r = bc[bz] - (T(6) * v0 - sum) * T(L.inv_h2);
+        T v = v0 + c_res * r;
+        if (prev != nullptr) v = v0 + c_mom * (v0 - prev[col + zo]) + c_res * r;
+        out[col + zo] = v;
+      } else if (copy_gsr) {
+        out[col + zo] = v0;
+      }
+    }
+    zm = v0;
+    v0 = zp;
   }
-  if (!in) return;
-  const long long off = loc_off(L, s, a[0], a[1], a[2]);
-  if (!interior) {
-    if (copy_gsr) out[off] = cur[off];
-    return;
-  }
-  const T c = cur[off];
-  const T r = view_at(b, s, a, g) - apply_A(L, cur, off, g);
-  T v = c + c_res * r;
-  if (prev != nullptr) v = c + c_mom * (c - prev[off]) + c_res * r;
-  out[off] = v;
 }
 
 // ------------------------------------------------------------------------------------
@@ -109,57 +143,105 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restri
 //                                           coarse rhs buffer until the tau kernel)
 // jr = floor(J_f/2) when the coarse level is an SR level (target F, R15); 0 otherwise
 // (target V_T^p at k = 1 (R16), or Omega_c on conventional levels).
+// One thread per coarse (X, Y) column, marching coarse Z; the 2x2 fine child columns'
+// planes 2Z-1..2Z+2 live in registers.
 // ------------------------------------------------------------------------------------
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restrict__ uf,
                                                        View<T> bf, Lvl Lc, T* __restrict__ uc,
-                                                       T* __restrict__ rc, int jr) {
+                                                       T* __restrict__ rc, int jr, int ntx,
+                                                       int zchunk) {
   const int s = blockIdx.y;
+  int B[3], lo[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
+  Col c;
+  if (!col_index(B[0], B[1], B[2], ntx, zchunk, c)) return;
   int pf[3], of[3];
   seg_coords(Lf, s, pf);
   seg_origin(Lf, pf, of);
-  int B[3], lo[3];
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    B[d] = Lf.S[d] / 2 + 2 * jr;
-    lo[d] = pf[d] * (Lf.S[d] / 2) - jr;
-  }
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= B[0] * B[1] * B[2]) return;
-  int I[3];
-  I[0] = lo[0] + idx % B[0];
-  const int t = idx / B[0];
-  I[1] = lo[1] + t % B[1];
-  I[2] = lo[2] + t / B[1];
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-    if (I[d] < 0 || I[d] >= Lc.N[d]) return;
+  for (int d = 0; d < 3; ++d) lo[d] = pf[d] * (Lf.S[d] / 2) - jr;
+  const int X = lo[0] + c.ax, Y = lo[1] + c.ay;
+  if (X < 0 || X >= Lc.N[0] || Y < 0 || Y >= Lc.N[1]) return;
+  const int Zb = max(lo[2] + c.z0, 0), Ze = min(lo[2] + c.z1, Lc.N[2]);
+  if (Zb >= Ze) return;
   const int cs = (Lc.nsegs == 1) ? 0 : s;
   int pc[3], oc[3];
   seg_coords(Lc, cs, pc);
   seg_origin(Lc, pc, oc);
-  T su = T(0), sr = T(0);
+  const long long fpz = Lf.pz, fpy = Lf.py;
+  // fine column (2X+dx, 2Y+dy) local offsets
+  const int fx = 2 * X - of[0], fy = 2 * Y - of[1];
+  const long long fcol = (long long)s * Lf.ss + (long long)fy * fpy + fx;
+  const T* u = uf + fcol;
+  const bool xm = X > 0, xp = X < Lc.N[0] - 1, ym = Y > 0, yp = Y < Lc.N[1] - 1;
+  const T* bcol;
+  long long bsz;
+  if (bf.global) {
+    bcol = bf.p + (long long)(2 * Y) * bf.sy + 2 * X;
+    bsz = bf.sz;
+  } else {
+    bcol = bf.p + (long long)s * bf.ss + (long long)fy * bf.sy + fx;
+    bsz = bf.sz;
+  }
+  // q[k][j]: column j = dy*2+dx, plane 2Z-1+k (k = 0..3)
+  T q[4][4];
+  {
+    const long long z = (long long)(2 * Zb - 1 - of[2]) * fpz;
 #pragma unroll
-  for (int dz = 0; dz < 2; ++dz)
+    for (int k = 0; k < 2; ++k)
 #pragma unroll
-    for (int dy = 0; dy < 2; ++dy)
+      for (int j = 0; j < 4; ++j) q[k][j] = u[z + k * fpz + (j >> 1) * fpy + (j & 1)];
+  }
+  for (int Z = Zb; Z < Ze; ++Z) {
+    const long long z0 = (long long)(2 * Z - of[2]) * fpz;
 #pragma unroll
-      for (int dx = 0; dx < 2; ++dx) {
-        int g[3] = {2 * I[0] + dx, 2 * I[1] + dy, 2 * I[2] + dz};
-        int a[3] = {g[0] - of[0], g[1] - of[1], g[2] - of[2]};
-        const long long off = loc_off(Lf, s, a[0], a[1], a[2]);
-        su += uf[off];
-        sr += view_at(bf, s, a, g) - apply_A(Lf, uf, off, g);
-      }
-  const long long co = loc_off(Lc, cs, I[0] - oc[0], I[1] - oc[1], I[2] - oc[2]);
-  uc[co] = su * T(0.125);
-  rc[co] = sr * T(0.125);
+    for (int k = 2; k < 4; ++k)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[k][j] = u[z0 + (k - 1) * fpz + (j >> 1) * fpy + (j & 1)];
+    const bool zmo = Z > 0, zpo = Z < Lc.N[2] - 1;
+    T su = T(0), sr = T(0);
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz) {
+      const long long zf = z0 + dz * fpz;
+      const long long bz = bf.global ? (long long)(2 * Z + dz) * bsz
+                                     : (long long)(2 * Z + dz - of[2]) * bsz;
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const int j = dy * 2 + dx;
+          const T v = q[dz + 1][j];
+          T sum = (dz == 0) ? (zmo ? q[0][j] : -v) : q[1][j];
+          sum += (dz == 0) ? q[2][j] : (zpo ? q[3][j] : -v);
+          const long long yo = zf + dy * fpy + dx;
+          sum += (dy == 0) ? (ym ? u[yo - fpy] : -v) : q[dz + 1][dx];
+          sum += (dy == 0) ? q[dz + 1][2 + dx] : (yp ? u[yo + fpy] : -v);
+          sum += (dx == 0) ? (xm ? u[yo - 1] : -v) : q[dz + 1][dy * 2];
+          sum += (dx == 0) ? q[dz + 1][dy * 2 + 1] : (xp ? u[yo + 1] : -v);
+          const T bv = bcol[bz + dy * bf.sy + dx];
+          su += v;
+          sr += bv - (T(6) * v - sum) * T(Lf.inv_h2);
+        }
+    }
+    const long long co = (long long)cs * Lc.ss + (long long)(Z - oc[2]) * Lc.pz +
+                         (long long)(Y - oc[1]) * Lc.py + (X - oc[0]);
+    uc[co] = su * T(0.125);
+    rc[co] = sr * T(0.125);
+    // planes 2Z+1, 2Z+2 are planes 2(Z+1)-1, 2(Z+1) of the next step
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      q[0][j] = q[2][j];
+      q[1][j] = q[3][j];
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------
 // FAS coarse right-hand side and t snapshot on a coarse level (Eq. 4; fig:mgv L116-117;
 // fig:mgvsr L234-236; R18):
-//   t = u                              on the whole storage box
+//   t = u                              on storage ∩ Omega
 //   rhs = R + A u                      on F   (R = restricted residual already in rhs)
 //   rhs = A u                          on C \ F
 // F = grow(V, jr) ∩ Omega (jr = floor(J_fine/2) on SR levels; 0 -> F = V = Omega on
@@ -168,33 +250,46 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restri
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_tau(Lvl L, const T* __restrict__ u,
                                                   T* __restrict__ rhs, T* __restrict__ t,
-                                                  int jr) {
+                                                  int jr, int ntx, int zchunk) {
+  Col c;
+  if (!col_index(L.E[0], L.E[1], L.E[2], ntx, zchunk, c)) return;
   const int s = blockIdx.y;
-  const int Ex = L.E[0], Ey = L.E[1], Ez = L.E[2];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= Ex * Ey * Ez) return;
-  int a[3];
-  a[0] = idx % Ex;
-  const int tt = idx / Ex;
-  a[1] = tt % Ey;
-  a[2] = tt / Ey;
-  int p[3], o[3], g[3];
+  int p[3], o[3];
   seg_coords(L, s, p);
   seg_origin(L, p, o);
-  const long long off = loc_off(L, s, a[0], a[1], a[2]);
-  t[off] = u[off];
-  bool in = true, interior = true, inF = true;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    g[d] = o[d] + a[d];
-    in = in && (g[d] >= 0) && (g[d] < L.N[d]);
-    interior = interior && (a[d] >= 1) && (a[d] <= L.E[d] - 2);
-    const int vlo = p[d] * L.S[d];
-    inF = inF && (g[d] >= vlo - jr) && (g[d] < vlo + L.S[d] + jr);
+  const int gx = o[0] + c.ax, gy = o[1] + c.ay;
+  if (gx < 0 || gx >= L.N[0] || gy < 0 || gy >= L.N[1]) return;
+  const bool cxy = c.ax >= 1 && c.ax <= L.E[0] - 2 && c.ay >= 1 && c.ay <= L.E[1] - 2;
+  const bool fxy = gx >= p[0] * L.S[0] - jr && gx < (p[0] + 1) * L.S[0] + jr &&
+                   gy >= p[1] * L.S[1] - jr && gy < (p[1] + 1) * L.S[1] + jr;
+  const int fz0 = p[2] * L.S[2] - jr, fz1 = (p[2] + 1) * L.S[2] + jr;
+  const bool xm = gx > 0, xp = gx < L.N[0] - 1, ym = gy > 0, yp = gy < L.N[1] - 1;
+  const long long col = (long long)s * L.ss + (long long)c.ay * L.py + c.ax;
+  const T* cc = u + col;
+  const long long pz = L.pz, py = L.py;
+  T zm = c.z0 > 0 ? cc[(long long)(c.z0 - 1) * pz] : T(0);
+  T v0 = cc[(long long)c.z0 * pz];
+  for (int az = c.z0; az < c.z1; ++az) {
+    const long long zo = (long long)az * pz;
+    const T zp = (az + 1 < L.E[2]) ? cc[zo + pz] : T(0);
+    const int gz = o[2] + az;
+    if (gz >= 0 && gz < L.N[2]) {
+      t[col + zo] = v0;
+      if (cxy && az >= 1 && az <= L.E[2] - 2) {
+        T sum = (gz > 0) ? zm : -v0;
+        sum += (gz < L.N[2] - 1) ? zp : -v0;
+        sum += ym ? cc[zo - py] : -v0;
+        sum += yp ? cc[zo + py] : -v0;
+        sum += xm ? cc[zo - 1] : -v0;
+        sum += xp ? cc[zo + 1] : -v0;
+        const T Au = (T(6) * v0 - sum) * T(L.inv_h2);
+        const bool inF = fxy && gz >= fz0 && gz < fz1;
+        rhs[col + zo] = inF ? rhs[col + zo] + Au : Au;
+      }
+    }
+    zm = v0;
+    v0 = zp;
   }
-  if (!in || !interior) return;
-  const T Au = apply_A(L, u, off, g);
-  rhs[off] = inF ? rhs[off] + Au : Au;
 }
 
 // ------------------------------------------------------------------------------------
@@ -205,65 +300,98 @@ __global__ void __launch_bounds__(kThreads) k_tau(Lvl L, const T* __restrict__ u
 // Coarse cells just outside Omega_c are reflected ghosts -(value at the mirror) (R3).
 // The coarse source is the fine segment's own coarse storage (SR level below) or the
 // single global coarse array (transition / conventional level below).
+// One thread per fine (x, y) column; it marches the coarse planes P and produces the fine
+// planes 2P, 2P+1 from a register queue of coarse planes P-1, P, P+1.
 // ------------------------------------------------------------------------------------
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_prolong(Lvl Lf, T* __restrict__ uf, Lvl Lc,
                                                       const T* __restrict__ w,
-                                                      const T* __restrict__ tc, int add) {
+                                                      const T* __restrict__ tc, int add, int ntx,
+                                                      int zchunk) {
+  Col c;
+  if (!col_index(Lf.E[0], Lf.E[1], Lf.E[2], ntx, zchunk, c)) return;
   const int s = blockIdx.y;
-  const int Ex = Lf.E[0], Ey = Lf.E[1], Ez = Lf.E[2];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= Ex * Ey * Ez) return;
-  int a[3];
-  a[0] = idx % Ex;
-  const int tt = idx / Ex;
-  a[1] = tt % Ey;
-  a[2] = tt / Ey;
-  int p[3], o[3], g[3];
+  int p[3], o[3];
   seg_coords(Lf, s, p);
   seg_origin(Lf, p, o);
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    g[d] = o[d] + a[d];
-    if (g[d] < 0 || g[d] >= Lf.N[d]) return;
-  }
+  const int gx = o[0] + c.ax, gy = o[1] + c.ay;
+  if (gx < 0 || gx >= Lf.N[0] || gy < 0 || gy >= Lf.N[1]) return;
+  const int gz0 = max(o[2] + c.z0, 0), gz1 = min(o[2] + c.z1, Lf.N[2]);
+  if (gz0 >= gz1) return;
   const int cs = (Lc.nsegs == 1) ? 0 : s;
   int pc[3], oc[3];
   seg_coords(Lc, cs, pc);
   seg_origin(Lc, pc, oc);
-  // per dimension: coarse local index and sign of the parent (k=0) and neighbour (k=1)
-  int ci[3][2];
-  T sg[3][2];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const int P = g[d] >> 1;
-    const int Q = P + ((g[d] & 1) ? 1 : -1);
+  // x / y: parent (k=0) and neighbour (k=1) coarse local index and sign
+  int cx[2], cy[2];
+  T sx1 = T(1), sy1 = T(1);
+  {
+    const int P = gx >> 1, Q = P + ((gx & 1) ? 1 : -1);
     int Qm = Q;
-    T sq = T(1);
-    if (Q < 0) { Qm = 0; sq = T(-1); }
-    if (Q >= Lc.N[d]) { Qm = Lc.N[d] - 1; sq = T(-1); }
-    ci[d][0] = P - oc[d];
-    ci[d][1] = Qm - oc[d];
-    sg[d][0] = T(1);
-    sg[d][1] = sq;
+    if (Q < 0) { Qm = 0; sx1 = T(-1); }
+    if (Q >= Lc.N[0]) { Qm = Lc.N[0] - 1; sx1 = T(-1); }
+    cx[0] = P - oc[0];
+    cx[1] = Qm - oc[0];
   }
+  {
+    const int P = gy >> 1, Q = P + ((gy & 1) ? 1 : -1);
+    int Qm = Q;
+    if (Q < 0) { Qm = 0; sy1 = T(-1); }
+    if (Q >= Lc.N[1]) { Qm = Lc.N[1] - 1; sy1 = T(-1); }
+    cy[0] = P - oc[1];
+    cy[1] = Qm - oc[1];
+  }
+  const long long cbase = (long long)cs * Lc.ss;
+  long long coff[4];  // j = ky*2 + kx
+#pragma unroll
+  for (int j = 0; j < 4; ++j) coff[j] = cbase + (long long)cy[j >> 1] * Lc.py + cx[j & 1];
+  const T sxy[4] = {T(1), sx1, sy1, sy1 * sx1};
   const T W[2] = {T(0.75), T(0.25)};
-  const long long base = (long long)cs * Lc.ss;
-  T acc = T(0);
+  auto load_plane = [&](int P, T* dst) {  // coarse plane P (reflected if outside Omega_c)
+    T sg = T(1);
+    int Pm = P;
+    if (P < 0) { Pm = 0; sg = T(-1); }
+    if (P >= Lc.N[2]) { Pm = Lc.N[2] - 1; sg = T(-1); }
+    // planes the fine chunk's first/last cell does not use may lie outside the coarse
+    // storage box (small J): clamp them into it (their values are never used)
+    const int lz = min(max(Pm - oc[2], 0), Lc.E[2] - 1);
+    const long long zo = (long long)lz * Lc.pz;
 #pragma unroll
-  for (int kz = 0; kz < 2; ++kz)
+    for (int j = 0; j < 4; ++j) {
+      T v = w[coff[j] + zo];
+      if (add) v = v - tc[coff[j] + zo];
+      dst[j] = sg * v;
+    }
+  };
+  T qm[4], q0[4], qp[4];
+  int P = gz0 >> 1;
+  load_plane(P - 1, qm);
+  load_plane(P, q0);
+  const long long fcol = (long long)s * Lf.ss + (long long)c.ay * Lf.py + c.ax;
+  for (; 2 * P < gz1; ++P) {
+    load_plane(P + 1, qp);
 #pragma unroll
-    for (int ky = 0; ky < 2; ++ky)
+    for (int e = 0; e < 2; ++e) {
+      const int gz = 2 * P + e;
+      if (gz < gz0 || gz >= gz1) continue;
+      const T* qn = e ? qp : qm;
+      T acc = T(0);
 #pragma unroll
-      for (int kx = 0; kx < 2; ++kx) {
-        const long long co = base + (long long)ci[2][kz] * Lc.pz + (long long)ci[1][ky] * Lc.py +
-                             ci[0][kx];
-        T v = w[co];
-        if (add) v = v - tc[co];
-        acc += (W[kz] * W[ky] * W[kx]) * ((sg[2][kz] * sg[1][ky] * sg[0][kx]) * v);
-      }
-  const long long off = loc_off(Lf, s, a[0], a[1], a[2]);
-  uf[off] = add ? uf[off] + acc : acc;
+      for (int kz = 0; kz < 2; ++kz)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const T v = kz ? qn[j] : q0[j];
+          acc += (W[kz] * W[j >> 1] * W[j & 1]) * (sxy[j] * v);
+        }
+      const long long off = fcol + (long long)(gz - o[2]) * Lf.pz;
+      uf[off] = add ? uf[off] + acc : acc;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      qm[j] = q0[j];
+      q0[j] = qp[j];
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -312,60 +440,78 @@ __global__ void __launch_bounds__(kThreads) k_pyramid(const T* __restrict__ ff, 
   }
 }
 
-// output: genuine cells of each segment -> user u (R19)
+// output: genuine cells of each segment -> user u (R19); one thread per
+// genuine (x, y) column of a segment, marching z.
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_gather(Lvl L, const T* __restrict__ useg,
-                                                     T* __restrict__ out) {
-  const long long n = (long long)L.N[0] * L.N[1] * L.N[2];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    int g[3];
-    g[0] = i % L.N[0];
-    g[1] = (i / L.N[0]) % L.N[1];
-    g[2] = i / ((long long)L.N[0] * L.N[1]);
-    int p[3], a[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      p[d] = g[d] / L.S[d];
-      a[d] = g[d] - (p[d] * L.S[d] - (L.J + 1));
-    }
-    const int s = (p[2] * L.ns[1] + p[1]) * L.ns[0] + p[0];
-    out[i] = useg[loc_off(L, s, a[0], a[1], a[2])];
-  }
+                                                     T* __restrict__ out, int ntx, int zchunk) {
+  Col c;
+  if (!col_index(L.S[0], L.S[1], L.S[2], ntx, zchunk, c)) return;
+  const int s = blockIdx.y;
+  int p[3];
+  seg_coords(L, s, p);
+  const int h = L.J + 1;
+  const T* src = useg + (long long)s * L.ss + (long long)(c.ay + h) * L.py + (c.ax + h);
+  T* dst = out + ((long long)(p[1] * L.S[1] + c.ay)) * L.N[0] + (p[0] * L.S[0] + c.ax);
+  const long long plane = (long long)L.N[0] * L.N[1];
+  for (int z = c.z0; z < c.z1; ++z)
+    dst[(long long)(p[2] * L.S[2] + z) * plane] = src[(long long)(z + h) * L.pz];
 }
 
-inline unsigned nblk(long long n) { return (unsigned)((n + kThreads - 1) / kThreads); }
-inline long long ecount(const Lvl& L) { return (long long)L.E[0] * L.E[1] * L.E[2]; }
 
 }  // namespace
+
+// column-layout launch geometry: (bx, by) tile over an (ex, ey) plane, z split into
+// chunks so that small levels still fill the GPU
+struct ColCfg {
+  dim3 grid, block;
+  int ntx, zchunk;
+};
+
+ColCfg col_cfg(int ex, int ey, int ez, int nsegs) {
+  ColCfg c;
+  const int bx = std::min(ex, 128);
+  const int by = std::max(1, std::min(ey, kThreads / bx));
+  c.ntx = (ex + bx - 1) / bx;
+  const int nty = (ey + by - 1) / by;
+  const long long cols = (long long)nsegs * ex * ey;
+  int zsplit = (int)std::min<long long>((200000 + cols - 1) / cols, std::max(1, ez / 4));
+  zsplit = std::max(zsplit, 1);
+  c.zchunk = (ez + zsplit - 1) / zsplit;
+  zsplit = (ez + c.zchunk - 1) / c.zchunk;
+  c.grid = dim3(c.ntx * nty, nsegs, zsplit);
+  c.block = dim3(bx, by, 1);
+  return c;
+}
 
 template <class T>
 void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* out, double c_mom,
                       double c_res, int copy_gsr, cudaStream_t st) {
-  dim3 grid(nblk(ecount(L)), L.nsegs);
-  k_cheb_step<T><<<grid, kThreads, 0, st>>>(L, cur, prev, b, out, (T)c_mom, (T)c_res, copy_gsr);
+  const ColCfg c = col_cfg(L.E[0], L.E[1], L.E[2], L.nsegs);
+  k_cheb_step<T><<<c.grid, c.block, 0, st>>>(L, cur, prev, b, out, (T)c_mom, (T)c_res, copy_gsr,
+                                             c.ntx, c.zchunk);
 }
 
 template <class T>
 void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc, int jr,
                      cudaStream_t st) {
-  long long B = 1;
-  for (int d = 0; d < 3; ++d) B *= (Lf.S[d] / 2 + 2 * jr);
-  dim3 grid(nblk(B), Lf.nsegs);
-  k_restrict<T><<<grid, kThreads, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr);
+  int B[3];
+  for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
+  const ColCfg c = col_cfg(B[0], B[1], B[2], Lf.nsegs);
+  k_restrict<T><<<c.grid, c.block, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr, c.ntx, c.zchunk);
 }
 
 template <class T>
 void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st) {
-  dim3 grid(nblk(ecount(Lc)), Lc.nsegs);
-  k_tau<T><<<grid, kThreads, 0, st>>>(Lc, u, rhs, t, jr);
+  const ColCfg c = col_cfg(Lc.E[0], Lc.E[1], Lc.E[2], Lc.nsegs);
+  k_tau<T><<<c.grid, c.block, 0, st>>>(Lc, u, rhs, t, jr, c.ntx, c.zchunk);
 }
 
 template <class T>
 void launch_prolong(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
                     cudaStream_t st) {
-  dim3 grid(nblk(ecount(Lf)), Lf.nsegs);
-  k_prolong<T><<<grid, kThreads, 0, st>>>(Lf, uf, Lc, w, t, add);
+  const ColCfg c = col_cfg(Lf.E[0], Lf.E[1], Lf.E[2], Lf.nsegs);
+  k_prolong<T><<<c.grid, c.block, 0, st>>>(Lf, uf, Lc, w, t, add, c.ntx, c.zchunk);
 }
 
 template <class T>
@@ -385,10 +531,8 @@ void launch_pyramid(const T* ff, int nfx, int nfy, int nfz, T* fc, cudaStream_t 
 
 template <class T>
 void launch_gather(const Lvl& L, const T* useg, T* out, cudaStream_t st) {
-  const long long n = (long long)L.N[0] * L.N[1] * L.N[2];
-  const long long cap = 148LL * 16;
-  const unsigned g = (unsigned)std::min<long long>(cap, (n + kThreads - 1) / kThreads);
-  k_gather<T><<<g, kThreads, 0, st>>>(L, useg, out);
+  const ColCfg c = col_cfg(L.S[0], L.S[1], L.S[2], L.nsegs);
+  k_gather<T><<<c.grid, c.block, 0, st>>>(L, useg, out, c.ntx, c.zchunk);
 }
 
 #define SRFMG_INST(T)                                                                          \

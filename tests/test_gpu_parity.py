@@ -308,3 +308,16 @@ def test_full_size_symmetry():
     sc = np.abs(u).max()
     assert np.abs(u - u[:, :, ::-1]).max() <= 1e-12 * sc
     assert np.abs(u - np.transpose(u, (0, 2, 1))).max() <= 1e-12 * sc
+
+
+def test_full_size_c3_matches_oracle():
+    # BASELINE configs[2] (C3) at its full size, fp64, in bench.py's launch configuration
+    # (graph replay), against the oracle run at the same size (~75 s, ~7.5 GB host RAM)
+    n = (512, 512, 512)
+    f = W.make_rhs("manufactured+noise", n)
+    ref = O.solve(f, O.Config(n=n, M=8, seg=64, buffer=2, K=4))
+    with Solver(n, 8, seg=64, buffer=2, K=4) as s:
+        ft = torch.from_numpy(f).cuda()
+        s.solve(ft)
+        u = s.solve(ft).cpu().numpy()
+    assert rel_l2(u, ref) <= TOL64, rel_l2(u, ref)
