@@ -1,2 +1,365 @@
-// Fused multi-stage stencil passes (filled in by later milestones).
+// Fused, TMA-fed degree-2 Chebyshev pass (both sweeps of R8 in one HBM pass), sm_100a.
+//
+// Work unit: one y-band of one segment's storage box (rows [r0, r1) of every plane).  The
+// CTA marches z.  The inputs of each plane -- the band's u rows (+-2 halo rows) and the
+// rhs rows (+-1) -- are contiguous in HBM (segment storage) or a box of the dense f, and
+// are streamed into a 4-deep shared-memory ring by ONE thread with cp.async.bulk /
+// cp.async.bulk.tensor (TMA) completing on mbarriers, so the loads of the next planes are
+// in flight while the CTA computes (no register-bound memory-level parallelism).
+//
+// Per plane z:   stage 1 at plane z     u1 = u0 + (b - A u0)/theta          (rows r0-1..r1)
+//                stage 2 at plane z-1   u2 = u1 + rho1 rho0 (u1 - u0) + (2 rho1/delta)(b - A u1)
+// Each thread owns up to MAXS fixed (x, y) cells of the band and keeps their z-columns of
+// u0 (z-1, z, z+1) and u1 (z-2, z-1, z) in registers; x/y neighbours come from the smem
+// planes (u0 ring; u1 double buffer).  Stage 1 is recomputed on one halo row each side so
+// stage 2 needs no exchange between bands.  GSR cells (frozen) are
+// copied; A = -Lap_h with reflected ghosts at the domain boundary (R1-R3).
+// Output goes to the other ping-pong buffer (bands of one segment run concurrently, so an
+// in-place write could race with a neighbour band's halo loads).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
 #include "fused.cuh"
+
+namespace srfmg {
+
+namespace {
+
+constexpr int kRing = 4;
+constexpr int kMaxThreads = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <class T>
+struct Cheb2Args {
+  Lvl L;
+  const T* uin;
+  T* uout;
+  const T* rhs_seg;  // segment-storage rhs (rhs_global == 0)
+  int rhs_global;
+  int BH;            // output rows per band
+  int u0_stride;     // elements per u0 ring plane buffer
+  int s_stride;      // elements per f / u1 plane buffer
+  T c0, cm, cr;
+};
+
+long long round_up_ll(long long v, long long m) { return (v + m - 1) / m * m; }
+
+template <class T, int MAXS>
+__global__ void __launch_bounds__(kMaxThreads, 1)
+    k_cheb2(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const Lvl& L = a.L;
+  const int Ex = L.E[0], Ey = L.E[1], Ez = L.E[2];
+  const int py = L.py;
+  const long long pz = L.pz;
+  const int s = blockIdx.y;
+  const int r0 = blockIdx.x * a.BH, r1 = min(Ey, r0 + a.BH);  // output rows
+  const int s0 = max(0, r0 - 1), s1 = min(Ey, r1 + 1);         // stage-1 rows
+  const int q0 = max(0, r0 - 2), q1 = min(Ey, r1 + 2);         // u0 rows
+  T* u0s = reinterpret_cast<T*>(sm);
+  T* fs = u0s + kRing * a.u0_stride;
+  T* u1s = fs + kRing * a.s_stride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + 2 * a.s_stride);
+
+  const int px = s % L.ns[0];
+  const int pyy = (s / L.ns[0]) % L.ns[1];
+  const int pzz = s / (L.ns[0] * L.ns[1]);
+  const int ox = px * L.S[0] - (L.J + 1);
+  const int oy = pyy * L.S[1] - (L.J + 1);
+  const int oz = pzz * L.S[2] - (L.J + 1);
+  const T* useg = a.uin + (long long)s * L.ss;
+  T* oseg = a.uout + (long long)s * L.ss;
+  const T* rseg = a.rhs_global ? nullptr : a.rhs_seg + (long long)s * L.ss;
+  const uint32_t u0_bytes = (uint32_t)((q1 - q0) * py * sizeof(T));
+  const uint32_t f_bytes = a.rhs_global ? (uint32_t)((a.BH + 2) * py * sizeof(T))
+                                        : (uint32_t)((s1 - s0) * py * sizeof(T));
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2 * kRing; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // producer (thread 0 only): plane z of u rows [q0, q1) and of rhs rows [s0, s0 + BH + 2)
+#define ISSUE_U0(z)                                                                          \
+  do {                                                                                       \
+    const int sl_ = (z) % kRing;                                                             \
+    mbar_expect_tx(&bars[sl_], u0_bytes);                                                    \
+    bulk_g2s(u0s + sl_ * a.u0_stride, useg + (long long)(z) * pz + (long long)q0 * py,       \
+             u0_bytes, &bars[sl_]);                                                          \
+  } while (0)
+#define ISSUE_F(z)                                                                           \
+  do {                                                                                       \
+    const int sl_ = (z) % kRing;                                                             \
+    mbar_expect_tx(&bars[kRing + sl_], f_bytes);                                             \
+    if (a.rhs_global)                                                                        \
+      tma_3d(fs + sl_ * a.s_stride, &fmap, ox, oy + s0, oz + (z), &bars[kRing + sl_]);       \
+    else                                                                                     \
+      bulk_g2s(fs + sl_ * a.s_stride, rseg + (long long)(z) * pz + (long long)s0 * py,       \
+               f_bytes, &bars[kRing + sl_]);                                                 \
+  } while (0)
+  if (threadIdx.x == 0) {
+    for (int z = 0; z < min(kRing, Ez); ++z) {
+      ISSUE_U0(z);
+      ISSUE_F(z);
+    }
+  }
+
+  // ---- fixed cells of this thread: column tx, rows s0 + tr + k*TR (k < MAXS)
+  const int TR = (s1 - s0 + MAXS - 1) / MAXS;
+  const int tx = threadIdx.x % Ex, tr = threadIdx.x / Ex;
+  const int gxv = ox + tx;
+  // x part of the region tests (constant per thread)
+  const bool tin = tr < TR && gxv >= 0 && gxv < L.N[0];
+  const bool tcx = tx >= 1 && tx <= Ex - 2;
+  const bool txm = gxv > 0, txp = gxv < L.N[0] - 1;
+  // y part per slot k, packed 8 bits per slot: b0 exists&in, b1 C_y, b2 output row,
+  // b3 y-1 in Omega, b4 y+1 in Omega
+  unsigned long long yfl = 0;
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    const int y = s0 + tr + k * TR;
+    const int gy = oy + y;
+    const bool ex = tin && y < s1 && gy >= 0 && gy < L.N[1];
+    const unsigned b = (ex ? 1u : 0u) | ((tcx && y >= 1 && y <= Ey - 2) ? 2u : 0u) |
+                       ((y >= r0 && y < r1) ? 4u : 0u) | ((gy > 0) ? 8u : 0u) |
+                       ((gy < L.N[1] - 1) ? 16u : 0u);
+    yfl |= (unsigned long long)b << (8 * k);
+  }
+#define FL(k) ((unsigned)(yfl >> (8 * (k))) & 0xffu)
+  const int off0 = tr * py + tx;
+  const int offk = TR * py;
+  const int u0sh = (s0 - q0) * py;
+  T u0q[MAXS][3], u1q[MAXS][3];
+  mbar_wait(&bars[0], 0);
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    u0q[k][0] = T(0);
+    u0q[k][1] = (FL(k) & 1u) ? u0s[u0sh + off0 + k * offk] : T(0);
+    u0q[k][2] = T(0);
+    u1q[k][0] = u1q[k][1] = u1q[k][2] = T(0);
+  }
+  const T ih2 = T(L.inv_h2);
+  for (int z = 0; z <= Ez; ++z) {
+    // ------------------------------------------------------------ stage 1 at plane z
+    if (z < Ez) {
+      if (z + 1 < Ez) mbar_wait(&bars[(z + 1) % kRing], ((z + 1) / kRing) & 1);
+      mbar_wait(&bars[kRing + z % kRing], (z / kRing) & 1);
+      const T* pl = u0s + (z % kRing) * a.u0_stride + u0sh;      // plane z, row s0 origin
+      const T* pn = u0s + ((z + 1) % kRing) * a.u0_stride + u0sh;
+      const T* fp = fs + (z % kRing) * a.s_stride;
+      T* u1w = u1s + (z & 1) * a.s_stride;
+      const int gz = oz + z;
+      const bool zin = gz >= 0 && gz < L.N[2];
+      const bool zc = zin && z >= 1 && z <= Ez - 2;
+      const bool zmo = gz > 0, zpo = gz < L.N[2] - 1;
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) {
+        const unsigned f = FL(k);
+        const int o = off0 + k * offk;
+        u0q[k][2] = (z + 1 < Ez && (f & 1u)) ? pn[o] : T(0);
+        const T v0 = u0q[k][1];
+        T v1 = v0;
+        if (zc && (f & 2u) && (f & 1u)) {
+          T sum = zmo ? u0q[k][0] : -v0;
+          sum += zpo ? u0q[k][2] : -v0;
+          sum += (f & 8u) ? pl[o - py] : -v0;
+          sum += (f & 16u) ? pl[o + py] : -v0;
+          sum += txm ? pl[o - 1] : -v0;
+          sum += txp ? pl[o + 1] : -v0;
+          v1 = v0 + a.c0 * (fp[o] - (T(6) * v0 - sum) * ih2);
+        }
+        u1q[k][0] = u1q[k][1];
+        u1q[k][1] = u1q[k][2];
+        u1q[k][2] = v1;
+        if (f & 1u) u1w[o] = v1;
+      }
+    }
+    __syncthreads();  // (A) u1 plane z complete; u0 plane z no longer read
+    if (threadIdx.x == 0 && z < Ez && z + kRing < Ez) ISSUE_U0(z + kRing);
+    // ------------------------------------------------------------ stage 2 at plane z-1
+    if (z >= 1) {
+      const int zz = z - 1;
+      const int gz = oz + zz;
+      const bool zin = gz >= 0 && gz < L.N[2];
+      const bool zc = zin && zz >= 1 && zz <= Ez - 2;
+      const bool zmo = gz > 0, zpo = gz < L.N[2] - 1;
+      const T* u1r = u1s + (zz & 1) * a.s_stride;
+      const T* fp = fs + (zz % kRing) * a.s_stride;
+      // (at z == Ez, plane Ez-1 is a storage boundary plane: copy branch only)
+      T* orow = oseg + (long long)zz * pz + (long long)s0 * py;
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) {
+        const unsigned f = FL(k);
+        if ((f & 5u) != 5u || !zin) continue;
+        const int o = off0 + k * offk;
+        const T u0v = (z == Ez) ? u0q[k][1] : u0q[k][0];
+        T v2 = u0v;
+        if (zc && (f & 2u)) {
+          const T c1 = u1q[k][1];
+          T sum = zmo ? u1q[k][0] : -c1;
+          sum += zpo ? u1q[k][2] : -c1;
+          sum += (f & 8u) ? u1r[o - py] : -c1;
+          sum += (f & 16u) ? u1r[o + py] : -c1;
+          sum += txm ? u1r[o - 1] : -c1;
+          sum += txp ? u1r[o + 1] : -c1;
+          v2 = c1 + a.cm * (c1 - u0v) + a.cr * (fp[o] - (T(6) * c1 - sum) * ih2);
+        }
+        orow[o] = v2;
+      }
+    }
+    __syncthreads();  // (B) u1 buffer and f plane z-1 free
+    if (threadIdx.x == 0 && z >= 1 && z - 1 + kRing < Ez) ISSUE_F(z - 1 + kRing);
+    if (z < Ez) {
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) {
+        u0q[k][0] = u0q[k][1];
+        u0q[k][1] = u0q[k][2];
+      }
+    }
+  }
+#undef ISSUE_U0
+#undef ISSUE_F
+#undef FL
+}
+
+// ---- host side ---------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+struct Plan {
+  int BH, nbands, NT, maxs;
+  size_t smem;
+  int u0_stride, s_stride;
+};
+
+template <class T>
+Plan make_plan(const Lvl& L) {
+  constexpr int MAXS = sizeof(T) == 8 ? 6 : 8;
+  Plan pl{};
+  pl.maxs = MAXS;
+  const int Ey = L.E[1], Ex = L.E[0];
+  for (int nb = 1; nb <= Ey; ++nb) {
+    const int BH = (Ey + nb - 1) / nb;
+    const long long u0s = round_up_ll((long long)(BH + 4) * L.py * sizeof(T), 128) / sizeof(T);
+    const long long ss = round_up_ll((long long)(BH + 2) * L.py * sizeof(T), 128) / sizeof(T);
+    const size_t smem = (size_t)(kRing * u0s + kRing * ss + 2 * ss) * sizeof(T) + 2 * kRing * 8;
+    const int rows = std::min(Ey, BH + 2);
+    const int NT = (int)round_up_ll((long long)Ex * ((rows + MAXS - 1) / MAXS), 32);
+    if (smem <= 227 * 1024 && NT <= kMaxThreads && BH + 2 <= 256) {
+      pl.BH = BH;
+      pl.nbands = (Ey + BH - 1) / BH;
+      pl.NT = NT;
+      pl.smem = smem;
+      pl.u0_stride = (int)u0s;
+      pl.s_stride = (int)ss;
+      return pl;
+    }
+  }
+  pl.BH = 0;
+  return pl;
+}
+
+}  // namespace
+
+template <class T>
+bool cheb2_fused_ok(const Lvl& L) {
+  if (L.py > 256 || L.E[0] > 256) return false;
+  if (((long long)L.N[0] * sizeof(T)) % 16) return false;
+  if (!get_encode()) return false;
+  return make_plan<T>(L).BH > 0;
+}
+
+template <class T>
+void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
+                        double cr, cudaStream_t st) {
+  constexpr int MAXS = sizeof(T) == 8 ? 6 : 8;
+  const Plan pl = make_plan<T>(L);
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (b.global) {
+    const cuuint64_t dims[3] = {(cuuint64_t)L.N[0], (cuuint64_t)L.N[1], (cuuint64_t)L.N[2]};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.N[0] * sizeof(T),
+                                   (cuuint64_t)L.N[0] * L.N[1] * sizeof(T)};
+    const cuuint32_t box[3] = {(cuuint32_t)L.py, (cuuint32_t)(pl.BH + 2), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    get_encode()(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                 3, const_cast<T*>(b.p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  Cheb2Args<T> a;
+  a.L = L;
+  a.uin = u_in;
+  a.uout = u_out;
+  a.rhs_seg = b.global ? nullptr : b.p;
+  a.rhs_global = b.global;
+  a.BH = pl.BH;
+  a.u0_stride = pl.u0_stride;
+  a.s_stride = pl.s_stride;
+  a.c0 = (T)c0;
+  a.cm = (T)cm;
+  a.cr = (T)cr;
+  auto kern = k_cheb2<T, MAXS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  dim3 grid(pl.nbands, L.nsegs);
+  kern<<<grid, pl.NT, pl.smem, st>>>(map, a);
+}
+
+template void launch_cheb2_fused<double>(const Lvl&, const double*, double*, FusedRhs<double>,
+                                         double, double, double, cudaStream_t);
+template void launch_cheb2_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>, double,
+                                        double, double, cudaStream_t);
+template bool cheb2_fused_ok<double>(const Lvl&);
+template bool cheb2_fused_ok<float>(const Lvl&);
+
+}  // namespace srfmg

@@ -1,3 +1,26 @@
-// Fused multi-sweep kernels (see fused.cu).
+// Fused, TMA-fed multi-sweep kernels of the SR-FMG schedule (see fused.cu).
 #pragma once
 #include "kernels.cuh"
+
+namespace srfmg {
+
+// A right-hand side the fused kernels can stream with TMA: either a dense global array
+// (tensor map built per launch from `p`) or a level's segment storage (1-D bulk copies).
+template <class T>
+struct FusedRhs {
+  const T* p;
+  int global;  // 1: dense Omega_l array (x fastest), 0: segment storage of the level
+};
+
+// One degree-2 Chebyshev application (two sweeps, R8) on C of every segment of level L,
+// in ONE pass over HBM: u_in (complete: C and GSR) -> u_out (C updated, GSR copied).
+// c0 = 1/theta (first step), cm = rho1 rho0, cr = 2 rho1 / delta (second step).
+template <class T>
+void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
+                        double cr, cudaStream_t st);
+
+// Fused-kernel availability for a level (smem budget etc.); false -> use the step kernels.
+template <class T>
+bool cheb2_fused_ok(const Lvl& L);
+
+}  // namespace srfmg

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restri
                                                         const T* prev, View<T> b, T* out,
                                                         T c_mom, T c_res, int copy_gsr, int ntx,
                                                         int zchunk) {
+  constexpr int U = 4;  // planes per batch: all loads of a batch are issued before any use
   Col c;
   if (!col_index(L.E[0], L.E[1], L.E[2], ntx, zchunk, c)) return;
   const int s = blockIdx.y;
@@ -107,31 +108,57 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restri
   const T* bc = b.global ? b.p + (long long)gy * b.sy + gx : b.p + (long long)s * b.ss +
                                                                  (long long)c.ay * b.sy + c.ax;
   const long long pz = L.pz, py = L.py;
-  T zm = c.z0 > 0 ? cc[(long long)(c.z0 - 1) * pz] : T(0);
-  T v0 = cc[(long long)c.z0 * pz];
-  for (int az = c.z0; az < c.z1; ++az) {
-    const long long zo = (long long)az * pz;
-    const T zp = (az + 1 < L.E[2]) ? cc[zo + pz] : T(0);
-    const int gz = o[2] + az;
-    if (gz >= 0 && gz < L.N[2]) {
-      if (cxy && az >= 1 && az <= L.E[2] - 2) {
-        T sum = (gz > 0) ? zm : -v0;
-        sum += (gz < L.N[2] - 1) ? zp : -v0;
-        sum += ym ? cc[zo - py] : -v0;
-        sum += yp ? cc[zo + py] : -v0;
-        sum += xm ? cc[zo - 1] : -v0;
-        sum += xp ? cc[zo + 1] : -v0;
-        const long long bz = b.global ? (long long)gz * b.sz : (long long)az * b.sz;
-        const T r = bc[bz] - (T(6) * v0 - sum) * T(L.inv_h2);
+  const int E2 = L.E[2], N2 = L.N[2];
+  T zq[U + 2];  // zq[k] = u at local plane az - 1 + k
+  zq[0] = c.z0 > 0 ? cc[(long long)(c.z0 - 1) * pz] : T(0);
+  zq[1] = cc[(long long)c.z0 * pz];
+  for (int az = c.z0; az < c.z1; az += U) {
+    T nb[U][4], bv[U], pv[U];
+    bool act[U], inn[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int zz = az + 1 + k;
+      zq[k + 2] = (zz < E2) ? cc[(long long)zz * pz] : T(0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int z = az + k;
+      const int gz = o[2] + z;
+      act[k] = z < c.z1 && gz >= 0 && gz < N2;
+      inn[k] = act[k] && cxy && z >= 1 && z <= E2 - 2;
+      const long long zo = (long long)z * pz;
+      if (inn[k]) {
+        nb[k][0] = ym ? cc[zo - py] : T(0);
+        nb[k][1] = yp ? cc[zo + py] : T(0);
+        nb[k][2] = xm ? cc[zo - 1] : T(0);
+        nb[k][3] = xp ? cc[zo + 1] : T(0);
+        bv[k] = bc[b.global ? (long long)gz * b.sz : (long long)z * b.sz];
+        pv[k] = prev != nullptr ? prev[col + zo] : T(0);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int z = az + k;
+      const int gz = o[2] + z;
+      const long long zo = (long long)z * pz;
+      const T v0 = zq[k + 1];
+      if (inn[k]) {
+        T sum = (gz > 0) ? zq[k] : -v0;
+        sum += (gz < N2 - 1) ? zq[k + 2] : -v0;
+        sum += ym ? nb[k][0] : -v0;
+        sum += yp ? nb[k][1] : -v0;
+        sum += xm ? nb[k][2] : -v0;
+        sum += xp ? nb[k][3] : -v0;
+        const T r = bv[k] - (T(6) * v0 - sum) * T(L.inv_h2);
         T v = v0 + c_res * r;
-        if (prev != nullptr) v = v0 + c_mom * (v0 - prev[col + zo]) + c_res * r;
+        if (prev != nullptr) v = v0 + c_mom * (v0 - pv[k]) + c_res * r;
         out[col + zo] = v;
-      } else if (copy_gsr) {
+      } else if (act[k] && copy_gsr) {
         out[col + zo] = v0;
       }
     }
-    zm = v0;
-    v0 = zp;
+    zq[0] = zq[U];
+    zq[1] = zq[U + 1];
   }
 }
 

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "fused.cuh"
 #include "kernels.cuh"
 #include "sr_fmg.h"
 
@@ -68,6 +69,7 @@ struct sr_fmg {
   void* host_u = nullptr;
   long long launches = 0;
   bool sync_debug = false;
+  bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
   int prof_cls = -1, prof_level = -1;
   std::vector<ProfRec> prof;
   size_t prof_used = 0;
@@ -322,6 +324,17 @@ struct Schedule {
     const Lvl& L = h->L[l];
     LevelBufs& bb = h->B[l];
     const CellCounts& c = h->cells[l];
+    if (deg == 2 && h->fused && srfmg::cheb2_fused_ok<T>(L)) {
+      // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
+      const double rho0 = 1.0 / h->sigma[l];
+      const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
+      Launch g(h, st, KC_CHEB, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
+      srfmg::launch_cheb2_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
+                                   srfmg::FusedRhs<T>{b.p, b.global}, 1.0 / h->theta[l],
+                                   rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
+      bb.cur = 1 - bb.cur;
+      return;
+    }
     int lat = bb.cur, oth = 1 - bb.cur;
     {
       Launch g(h, st, KC_CHEB, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
@@ -528,6 +541,8 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   }
   const char* sd = std::getenv("SR_FMG_SYNC");
   h->sync_debug = sd && sd[0] == '1';
+  const char* fu = std::getenv("SR_FMG_FUSED");
+  h->fused = !(fu && fu[0] == '0');
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {
