@@ -134,7 +134,8 @@ const char *sr_fmg_kernel_name(int32_t i);
 
 /* ---- test-only hooks (not part of the solver contract) ---------------------------------
  * sr_fmg_debug_level_io: copy the internal storage of (level, field) of ALL segments
- * between the device and a host buffer of nseg*storage_pitch[level][2] elements
+ * between the device and a host buffer of nseg*storage_pitch[level][2] elements; cells
+ * outside the domain must be written as zero (the kernels rely on that invariant)
  * (field 0 = current u, 1 = rhs, 2 = t; write != 0 copies host -> device).
  * sr_fmg_debug_op: run one kernel of the schedule on the internal buffers:
  *   op 0 = CHEB(deg) on level with rhs = internal rhs buffer (or user f when level == M),

@@ -21,7 +21,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "fused.cuh"
 
@@ -30,7 +32,6 @@ namespace srfmg {
 namespace {
 
 constexpr int kRing = 4;
-constexpr int kMaxThreads = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -78,14 +79,16 @@ struct Cheb2Args {
   int rhs_global;
   int BH;            // output rows per band
   int u0_stride;     // elements per u0 ring plane buffer
-  int s_stride;      // elements per f / u1 plane buffer
+  int s_stride;      // elements per u1 plane buffer
+  int f_stride;      // elements per rhs plane buffer
+  int bw;            // rhs tensor-map box width (global rhs; 16-byte aligned start)
   T c0, cm, cr;
 };
 
 long long round_up_ll(long long v, long long m) { return (v + m - 1) / m * m; }
 
-template <class T, int MAXS>
-__global__ void __launch_bounds__(kMaxThreads, 1)
+template <class T, int MAXS, int NTMAX>
+__global__ void __launch_bounds__(NTMAX, 1)
     k_cheb2(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
   extern __shared__ __align__(128) unsigned char sm[];
   const Lvl& L = a.L;
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   const int q0 = max(0, r0 - 2), q1 = min(Ey, r1 + 2);         // u0 rows
   T* u0s = reinterpret_cast<T*>(sm);
   T* fs = u0s + kRing * a.u0_stride;
-  T* u1s = fs + kRing * a.s_stride;
+  T* u1s = fs + kRing * a.f_stride;
   uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + 2 * a.s_stride);
 
   const int px = s % L.ns[0];
@@ -111,7 +114,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   T* oseg = a.uout + (long long)s * L.ss;
   const T* rseg = a.rhs_global ? nullptr : a.rhs_seg + (long long)s * L.ss;
   const uint32_t u0_bytes = (uint32_t)((q1 - q0) * py * sizeof(T));
-  const uint32_t f_bytes = a.rhs_global ? (uint32_t)((a.BH + 2) * py * sizeof(T))
+  // TMA tensor loads need a 16-byte aligned start in x: load from the aligned-down
+  // column and shift the smem index by fsh; the rhs buffer row pitch is then bw
+  constexpr int kAl = 16 / (int)sizeof(T);
+  const int oxa = ox & ~(kAl - 1);
+  const int fpitch = a.rhs_global ? a.bw : py;
+  const int fsh = a.rhs_global ? ox - oxa : 0;
+  const uint32_t f_bytes = a.rhs_global ? (uint32_t)((a.BH + 2) * a.bw * sizeof(T))
                                         : (uint32_t)((s1 - s0) * py * sizeof(T));
 
   if (threadIdx.x == 0) {
@@ -132,9 +141,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const int sl_ = (z) % kRing;                                                             \
     mbar_expect_tx(&bars[kRing + sl_], f_bytes);                                             \
     if (a.rhs_global)                                                                        \
-      tma_3d(fs + sl_ * a.s_stride, &fmap, ox, oy + s0, oz + (z), &bars[kRing + sl_]);       \
+      tma_3d(fs + sl_ * a.f_stride, &fmap, oxa, oy + s0, oz + (z), &bars[kRing + sl_]);      \
     else                                                                                     \
-      bulk_g2s(fs + sl_ * a.s_stride, rseg + (long long)(z) * pz + (long long)s0 * py,       \
+      bulk_g2s(fs + sl_ * a.f_stride, rseg + (long long)(z) * pz + (long long)s0 * py,       \
                f_bytes, &bars[kRing + sl_]);                                                 \
   } while (0)
   if (threadIdx.x == 0) {
@@ -145,73 +154,75 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   }
 
   // ---- fixed cells of this thread: column tx, rows s0 + tr + k*TR (k < MAXS)
+  // Boundary handling is branch-free: storage cells outside Omega are ZERO (invariant of
+  // every kernel: none writes outside Omega; buffers are zeroed at create), so a reflected
+  // ghost -u_i (R3) adds +1 to the diagonal of A instead:
+  //   (A u)_i = ((6 + n_out(i)) u_i - sum of the in-domain neighbours) / h^2.
   const int TR = (s1 - s0 + MAXS - 1) / MAXS;
   const int tx = threadIdx.x % Ex, tr = threadIdx.x / Ex;
   const int gxv = ox + tx;
-  // x part of the region tests (constant per thread)
   const bool tin = tr < TR && gxv >= 0 && gxv < L.N[0];
   const bool tcx = tx >= 1 && tx <= Ex - 2;
-  const bool txm = gxv > 0, txp = gxv < L.N[0] - 1;
-  // y part per slot k, packed 8 bits per slot: b0 exists&in, b1 C_y, b2 output row,
-  // b3 y-1 in Omega, b4 y+1 in Omega
-  unsigned long long yfl = 0;
+  const int dx = (gxv == 0 ? 1 : 0) + (gxv == L.N[0] - 1 ? 1 : 0);
+  unsigned ex_mask = 0, c_mask = 0, w_mask = 0;  // slot exists / computes (C_xy) / writes
+  T diag[MAXS];
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) {
     const int y = s0 + tr + k * TR;
     const int gy = oy + y;
-    const bool ex = tin && y < s1 && gy >= 0 && gy < L.N[1];
-    const unsigned b = (ex ? 1u : 0u) | ((tcx && y >= 1 && y <= Ey - 2) ? 2u : 0u) |
-                       ((y >= r0 && y < r1) ? 4u : 0u) | ((gy > 0) ? 8u : 0u) |
-                       ((gy < L.N[1] - 1) ? 16u : 0u);
-    yfl |= (unsigned long long)b << (8 * k);
+    const bool ex = tr < TR && y < s1;
+    const bool in = tin && ex && gy >= 0 && gy < L.N[1];
+    if (ex) ex_mask |= 1u << k;
+    if (in && tcx && y >= 1 && y <= Ey - 2) c_mask |= 1u << k;
+    if (in && y >= r0 && y < r1) w_mask |= 1u << k;
+    diag[k] = T(6 + dx + (gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0));
   }
-#define FL(k) ((unsigned)(yfl >> (8 * (k))) & 0xffu)
   const int off0 = tr * py + tx;
   const int offk = TR * py;
+  const int fo0 = tr * fpitch + tx + fsh;
+  const int fok = TR * fpitch;
   const int u0sh = (s0 - q0) * py;
+  // register queues: plane p of u0 / u1 lives in slot p % 3 (no shifting)
   T u0q[MAXS][3], u1q[MAXS][3];
   mbar_wait(&bars[0], 0);
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) {
-    u0q[k][0] = T(0);
-    u0q[k][1] = (FL(k) & 1u) ? u0s[u0sh + off0 + k * offk] : T(0);
+    u0q[k][0] = ((ex_mask >> k) & 1u) ? u0s[u0sh + off0 + k * offk] : T(0);
+    u0q[k][1] = T(0);
     u0q[k][2] = T(0);
     u1q[k][0] = u1q[k][1] = u1q[k][2] = T(0);
   }
   const T ih2 = T(L.inv_h2);
-  for (int z = 0; z <= Ez; ++z) {
+  const T c0 = a.c0, cm = a.cm, cr = a.cr;
+
+  auto step = [&](auto RR, int z) {
+    constexpr int R = decltype(RR)::value;  // z % 3
+    constexpr int IM = (R + 2) % 3, I0 = R, IP = (R + 1) % 3;
     // ------------------------------------------------------------ stage 1 at plane z
     if (z < Ez) {
       if (z + 1 < Ez) mbar_wait(&bars[(z + 1) % kRing], ((z + 1) / kRing) & 1);
       mbar_wait(&bars[kRing + z % kRing], (z / kRing) & 1);
-      const T* pl = u0s + (z % kRing) * a.u0_stride + u0sh;      // plane z, row s0 origin
-      const T* pn = u0s + ((z + 1) % kRing) * a.u0_stride + u0sh;
-      const T* fp = fs + (z % kRing) * a.s_stride;
-      T* u1w = u1s + (z & 1) * a.s_stride;
+      const T* pl = u0s + (z % kRing) * a.u0_stride + u0sh + off0;
+      const T* pn = u0s + ((z + 1) % kRing) * a.u0_stride + u0sh + off0;
+      const T* fp = fs + (z % kRing) * a.f_stride + fo0;
+      T* u1w = u1s + (z & 1) * a.s_stride + off0;
       const int gz = oz + z;
-      const bool zin = gz >= 0 && gz < L.N[2];
-      const bool zc = zin && z >= 1 && z <= Ez - 2;
-      const bool zmo = gz > 0, zpo = gz < L.N[2] - 1;
+      const bool zc = gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2;
+      const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
-        const unsigned f = FL(k);
-        const int o = off0 + k * offk;
-        u0q[k][2] = (z + 1 < Ez && (f & 1u)) ? pn[o] : T(0);
-        const T v0 = u0q[k][1];
+        const int o = k * offk;
+        u0q[k][IP] = (z + 1 < Ez && ((ex_mask >> k) & 1u)) ? pn[o] : T(0);
+        const T v0 = u0q[k][I0];
         T v1 = v0;
-        if (zc && (f & 2u) && (f & 1u)) {
-          T sum = zmo ? u0q[k][0] : -v0;
-          sum += zpo ? u0q[k][2] : -v0;
-          sum += (f & 8u) ? pl[o - py] : -v0;
-          sum += (f & 16u) ? pl[o + py] : -v0;
-          sum += txm ? pl[o - 1] : -v0;
-          sum += txp ? pl[o + 1] : -v0;
-          v1 = v0 + a.c0 * (fp[o] - (T(6) * v0 - sum) * ih2);
+        if (zc && ((c_mask >> k) & 1u)) {
+          const T sum = ((u0q[k][IM] + u0q[k][IP]) + (pl[o - py] + pl[o + py])) +
+                        (pl[o - 1] + pl[o + 1]);
+          const T r = fp[k * fok] - ((diag[k] + dz) * v0 - sum) * ih2;
+          v1 = v0 + c0 * r;
         }
-        u1q[k][0] = u1q[k][1];
-        u1q[k][1] = u1q[k][2];
-        u1q[k][2] = v1;
-        if (f & 1u) u1w[o] = v1;
+        u1q[k][I0] = v1;
+        if ((ex_mask >> k) & 1u) u1w[o] = v1;
       }
     }
     __syncthreads();  // (A) u1 plane z complete; u0 plane z no longer read
@@ -222,44 +233,40 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const int gz = oz + zz;
       const bool zin = gz >= 0 && gz < L.N[2];
       const bool zc = zin && zz >= 1 && zz <= Ez - 2;
-      const bool zmo = gz > 0, zpo = gz < L.N[2] - 1;
-      const T* u1r = u1s + (zz & 1) * a.s_stride;
-      const T* fp = fs + (zz % kRing) * a.s_stride;
-      // (at z == Ez, plane Ez-1 is a storage boundary plane: copy branch only)
-      T* orow = oseg + (long long)zz * pz + (long long)s0 * py;
+      const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+      const T* u1r = u1s + (zz & 1) * a.s_stride + off0;
+      const T* fp = fs + (zz % kRing) * a.f_stride + fo0;
+      T* orow = oseg + (long long)zz * pz + (long long)s0 * py + off0;
+      // u1 planes z-2, z-1, z are in slots (R+1)%3, (R+2)%3, R; u0 plane z-1 in (R+2)%3
+      constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
+      if (zin) {
 #pragma unroll
-      for (int k = 0; k < MAXS; ++k) {
-        const unsigned f = FL(k);
-        if ((f & 5u) != 5u || !zin) continue;
-        const int o = off0 + k * offk;
-        const T u0v = (z == Ez) ? u0q[k][1] : u0q[k][0];
-        T v2 = u0v;
-        if (zc && (f & 2u)) {
-          const T c1 = u1q[k][1];
-          T sum = zmo ? u1q[k][0] : -c1;
-          sum += zpo ? u1q[k][2] : -c1;
-          sum += (f & 8u) ? u1r[o - py] : -c1;
-          sum += (f & 16u) ? u1r[o + py] : -c1;
-          sum += txm ? u1r[o - 1] : -c1;
-          sum += txp ? u1r[o + 1] : -c1;
-          v2 = c1 + a.cm * (c1 - u0v) + a.cr * (fp[o] - (T(6) * c1 - sum) * ih2);
+        for (int k = 0; k < MAXS; ++k) {
+          if (!((w_mask >> k) & 1u)) continue;
+          const int o = k * offk;
+          const T u0v = u0q[k][J1];
+          T v2 = u0v;
+          if (zc && ((c_mask >> k) & 1u)) {
+            const T c1 = u1q[k][J1];
+            const T sum = ((u1q[k][J2] + u1q[k][J0]) + (u1r[o - py] + u1r[o + py])) +
+                          (u1r[o - 1] + u1r[o + 1]);
+            const T r = fp[k * fok] - ((diag[k] + dz) * c1 - sum) * ih2;
+            v2 = c1 + cm * (c1 - u0v) + cr * r;
+          }
+          orow[o] = v2;
         }
-        orow[o] = v2;
       }
     }
     __syncthreads();  // (B) u1 buffer and f plane z-1 free
     if (threadIdx.x == 0 && z >= 1 && z - 1 + kRing < Ez) ISSUE_F(z - 1 + kRing);
-    if (z < Ez) {
-#pragma unroll
-      for (int k = 0; k < MAXS; ++k) {
-        u0q[k][0] = u0q[k][1];
-        u0q[k][1] = u0q[k][2];
-      }
-    }
+  };
+  for (int zb = 0; zb <= Ez; zb += 3) {
+    step(std::integral_constant<int, 0>{}, zb);
+    if (zb + 1 <= Ez) step(std::integral_constant<int, 1>{}, zb + 1);
+    if (zb + 2 <= Ez) step(std::integral_constant<int, 2>{}, zb + 2);
   }
 #undef ISSUE_U0
 #undef ISSUE_F
-#undef FL
 }
 
 // ---- host side ---------------------------------------------------------------------
@@ -276,32 +283,57 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// kernel variants (cells per thread, max threads): picked by SR_FMG_CHEB2_VARIANT
+struct Variant {
+  int maxs, nt;
+};
+template <class T>
+Variant variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SR_FMG_CHEB2_VARIANT");
+    v = e ? std::atoi(e) : 0;
+    if (v < 0 || v > 2) v = 0;
+  }
+  if (sizeof(T) == 8) {
+    const Variant t[3] = {{6, 512}, {3, 1024}, {4, 768}};
+    return t[v];
+  }
+  const Variant t[3] = {{8, 512}, {4, 1024}, {6, 768}};
+  return t[v];
+}
+
 struct Plan {
   int BH, nbands, NT, maxs;
   size_t smem;
-  int u0_stride, s_stride;
+  int u0_stride, s_stride, f_stride, bw;
 };
 
 template <class T>
-Plan make_plan(const Lvl& L) {
-  constexpr int MAXS = sizeof(T) == 8 ? 6 : 8;
+Plan make_plan(const Lvl& L, int MAXS, int NTMAX) {
   Plan pl{};
   pl.maxs = MAXS;
   const int Ey = L.E[1], Ex = L.E[0];
+  constexpr int kAl = 16 / (int)sizeof(T);
+  const int bw = (int)round_up_ll(Ex + kAl - 1, kAl);  // covers [align_down(ox), ox + Ex)
   for (int nb = 1; nb <= Ey; ++nb) {
     const int BH = (Ey + nb - 1) / nb;
     const long long u0s = round_up_ll((long long)(BH + 4) * L.py * sizeof(T), 128) / sizeof(T);
     const long long ss = round_up_ll((long long)(BH + 2) * L.py * sizeof(T), 128) / sizeof(T);
-    const size_t smem = (size_t)(kRing * u0s + kRing * ss + 2 * ss) * sizeof(T) + 2 * kRing * 8;
+    const long long fsz =
+        round_up_ll((long long)(BH + 2) * std::max(bw, L.py) * sizeof(T), 128) / sizeof(T);
+    const size_t smem = (size_t)(kRing * u0s + kRing * fsz + 2 * ss) * sizeof(T) + 2 * kRing * 8;
     const int rows = std::min(Ey, BH + 2);
     const int NT = (int)round_up_ll((long long)Ex * ((rows + MAXS - 1) / MAXS), 32);
-    if (smem <= 227 * 1024 && NT <= kMaxThreads && BH + 2 <= 256) {
+    if (smem <= 227 * 1024 && NT <= NTMAX && BH + 2 <= 256 && bw <= 256) {
       pl.BH = BH;
       pl.nbands = (Ey + BH - 1) / BH;
       pl.NT = NT;
       pl.smem = smem;
       pl.u0_stride = (int)u0s;
       pl.s_stride = (int)ss;
+      pl.f_stride = (int)fsz;
+      pl.bw = bw;
       return pl;
     }
   }
@@ -316,26 +348,33 @@ bool cheb2_fused_ok(const Lvl& L) {
   if (L.py > 256 || L.E[0] > 256) return false;
   if (((long long)L.N[0] * sizeof(T)) % 16) return false;
   if (!get_encode()) return false;
-  return make_plan<T>(L).BH > 0;
+  const Variant v = variant<T>();
+  return make_plan<T>(L, v.maxs, v.nt).BH > 0;
 }
 
 template <class T>
 void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
                         double cr, cudaStream_t st) {
-  constexpr int MAXS = sizeof(T) == 8 ? 6 : 8;
-  const Plan pl = make_plan<T>(L);
+  const Variant v = variant<T>();
+  const Plan pl = make_plan<T>(L, v.maxs, v.nt);
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   if (b.global) {
     const cuuint64_t dims[3] = {(cuuint64_t)L.N[0], (cuuint64_t)L.N[1], (cuuint64_t)L.N[2]};
     const cuuint64_t strides[2] = {(cuuint64_t)L.N[0] * sizeof(T),
                                    (cuuint64_t)L.N[0] * L.N[1] * sizeof(T)};
-    const cuuint32_t box[3] = {(cuuint32_t)L.py, (cuuint32_t)(pl.BH + 2), 1};
+    const cuuint32_t box[3] = {(cuuint32_t)pl.bw, (cuuint32_t)(pl.BH + 2), 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    get_encode()(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                 3, const_cast<T*>(b.p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = get_encode()(
+        &map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+        const_cast<T*>(b.p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      fprintf(stderr, "sr_fmg: cuTensorMapEncodeTiled failed (%d) dims %llu %llu %llu box %u %u\n",
+              (int)r, (unsigned long long)dims[0], (unsigned long long)dims[1],
+              (unsigned long long)dims[2], box[0], box[1]);
+    }
   }
   Cheb2Args<T> a;
   a.L = L;
@@ -346,13 +385,20 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
   a.BH = pl.BH;
   a.u0_stride = pl.u0_stride;
   a.s_stride = pl.s_stride;
+  a.f_stride = pl.f_stride;
+  a.bw = pl.bw;
   a.c0 = (T)c0;
   a.cm = (T)cm;
   a.cr = (T)cr;
-  auto kern = k_cheb2<T, MAXS>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   dim3 grid(pl.nbands, L.nsegs);
-  kern<<<grid, pl.NT, pl.smem, st>>>(map, a);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    kern<<<grid, pl.NT, pl.smem, st>>>(map, a);
+  };
+  constexpr bool D = sizeof(T) == 8;
+  if (v.nt == 512) go(k_cheb2<T, D ? 6 : 8, 512>);
+  else if (v.nt == 1024) go(k_cheb2<T, D ? 3 : 4, 1024>);
+  else go(k_cheb2<T, D ? 4 : 6, 768>);
 }
 
 template void launch_cheb2_fused<double>(const Lvl&, const double*, double*, FusedRhs<double>,

@@ -49,3 +49,19 @@ def oracle_seg_index(li, s):
 
 def rel_l2(a, b):
     return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+def zero_outside(buf, li):
+    """Zero every storage cell outside Omega_l (the library's invariant: storage cells
+    outside the domain are zero; kernels never write them)."""
+    nsegs = li.nseg[0] * li.nseg[1] * li.nseg[2]
+    for s in range(nsegs):
+        box = storage_box(li, s)
+        a = seg_array(buf, li, s)
+        for d, ax in ((0, 2), (1, 1), (2, 0)):   # li.n is (x, y, z); array axes (z, y, x)
+            g = np.arange(box.lo[ax], box.hi[ax])
+            bad = (g < 0) | (g >= li.n[d])
+            sl = [slice(None)] * 3
+            sl[ax] = bad
+            a[tuple(sl)] = 0.0
+    return buf

@@ -11,7 +11,7 @@ import oracle as O
 import workloads as W
 from oracle import Box, Field
 from tests.gpu_helpers import (from_fields, oracle_seg_index, rel_l2, seg_array, storage_box,
-                               to_fields)
+                               to_fields, zero_outside)
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -130,7 +130,7 @@ def _random_fields(s, l, seed):
     rng = np.random.default_rng(seed)
     nsegs = li.nseg[0] * li.nseg[1] * li.nseg[2]
     buf = rng.standard_normal(nsegs * li.pitch[2])
-    return li, buf
+    return li, zero_outside(buf, li)
 
 
 def _dom(l):
