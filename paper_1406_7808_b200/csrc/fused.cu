@@ -153,41 +153,46 @@ __global__ void __launch_bounds__(NTMAX, 1)
     }
   }
 
-  // ---- fixed cells of this thread: column tx, rows s0 + tr + k*TR (k < MAXS)
+  // ---- fixed cells of this thread: column tx, MAXS consecutive rows y0 .. y0+MAXS-1.
+  // The y-neighbours of all but the edge slots are the register queues of the thread's
+  // own neighbouring slots; x-neighbours and edge y-neighbours come from shared memory.
   // Boundary handling is branch-free: storage cells outside Omega are ZERO (invariant of
   // every kernel: none writes outside Omega; buffers are zeroed at create), so a reflected
   // ghost -u_i (R3) adds +1 to the diagonal of A instead:
   //   (A u)_i = ((6 + n_out(i)) u_i - sum of the in-domain neighbours) / h^2.
-  const int TR = (s1 - s0 + MAXS - 1) / MAXS;
-  const int tx = threadIdx.x % Ex, tr = threadIdx.x / Ex;
+  const int NG = (s1 - s0 + MAXS - 1) / MAXS;
+  const int tx = threadIdx.x % Ex, g = threadIdx.x / Ex;
+  const int y0 = s0 + g * MAXS;
   const int gxv = ox + tx;
-  const bool tin = tr < TR && gxv >= 0 && gxv < L.N[0];
+  const bool tok = g < NG;
+  const bool tin = tok && gxv >= 0 && gxv < L.N[0];
   const bool tcx = tx >= 1 && tx <= Ex - 2;
-  const int dx = (gxv == 0 ? 1 : 0) + (gxv == L.N[0] - 1 ? 1 : 0);
-  unsigned ex_mask = 0, c_mask = 0, w_mask = 0;  // slot exists / computes (C_xy) / writes
+  const int dxo = (gxv == 0 ? 1 : 0) + (gxv == L.N[0] - 1 ? 1 : 0);
+  // slot masks: ld (u0 row loaded), ex (stage-1 row: u1 written), c (C cell), w (output)
+  unsigned ld_mask = 0, ex_mask = 0, c_mask = 0, w_mask = 0;
   T diag[MAXS];
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) {
-    const int y = s0 + tr + k * TR;
+    const int y = y0 + k;
     const int gy = oy + y;
-    const bool ex = tr < TR && y < s1;
-    const bool in = tin && ex && gy >= 0 && gy < L.N[1];
-    if (ex) ex_mask |= 1u << k;
+    const bool in = tin && y < s1 && gy >= 0 && gy < L.N[1];
+    if (tok && y < q1) ld_mask |= 1u << k;
+    if (tok && y < s1) ex_mask |= 1u << k;
     if (in && tcx && y >= 1 && y <= Ey - 2) c_mask |= 1u << k;
     if (in && y >= r0 && y < r1) w_mask |= 1u << k;
-    diag[k] = T(6 + dx + (gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0));
+    diag[k] = T(6 + dxo + (gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0));
   }
-  const int off0 = tr * py + tx;
-  const int offk = TR * py;
-  const int fo0 = tr * fpitch + tx + fsh;
-  const int fok = TR * fpitch;
-  const int u0sh = (s0 - q0) * py;
+  const int off0 = (y0 - s0) * py + tx;
+  const T* const u0b = u0s + (s0 - q0) * py + off0;  // slot 0 of ring slot 0
+  const T* const fb = fs + (y0 - s0) * fpitch + tx + fsh;
+  T* const u1b = u1s + off0;
+  T* const ob = oseg + (long long)y0 * py + tx;
   // register queues: plane p of u0 / u1 lives in slot p % 3 (no shifting)
   T u0q[MAXS][3], u1q[MAXS][3];
   mbar_wait(&bars[0], 0);
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) {
-    u0q[k][0] = ((ex_mask >> k) & 1u) ? u0s[u0sh + off0 + k * offk] : T(0);
+    u0q[k][0] = ((ld_mask >> k) & 1u) ? u0b[k * py] : T(0);
     u0q[k][1] = T(0);
     u0q[k][2] = T(0);
     u1q[k][0] = u1q[k][1] = u1q[k][2] = T(0);
@@ -202,27 +207,34 @@ __global__ void __launch_bounds__(NTMAX, 1)
     if (z < Ez) {
       if (z + 1 < Ez) mbar_wait(&bars[(z + 1) % kRing], ((z + 1) / kRing) & 1);
       mbar_wait(&bars[kRing + z % kRing], (z / kRing) & 1);
-      const T* pl = u0s + (z % kRing) * a.u0_stride + u0sh + off0;
-      const T* pn = u0s + ((z + 1) % kRing) * a.u0_stride + u0sh + off0;
-      const T* fp = fs + (z % kRing) * a.f_stride + fo0;
-      T* u1w = u1s + (z & 1) * a.s_stride + off0;
+      const T* pl = u0b + (z % kRing) * a.u0_stride;
+      const T* pn = u0b + ((z + 1) % kRing) * a.u0_stride;
+      const T* fp = fb + (z % kRing) * a.f_stride;
+      T* u1w = u1b + (z & 1) * a.s_stride;
       const int gz = oz + z;
       const bool zc = gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2;
       const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+      if (z + 1 < Ez) {
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k)
+          if ((ld_mask >> k) & 1u) u0q[k][IP] = pn[k * py];
+      } else {
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) u0q[k][IP] = T(0);
+      }
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
-        const int o = k * offk;
-        u0q[k][IP] = (z + 1 < Ez && ((ex_mask >> k) & 1u)) ? pn[o] : T(0);
         const T v0 = u0q[k][I0];
         T v1 = v0;
         if (zc && ((c_mask >> k) & 1u)) {
-          const T sum = ((u0q[k][IM] + u0q[k][IP]) + (pl[o - py] + pl[o + py])) +
-                        (pl[o - 1] + pl[o + 1]);
-          const T r = fp[k * fok] - ((diag[k] + dz) * v0 - sum) * ih2;
+          const T ym = (k == 0) ? pl[-py] : u0q[k > 0 ? k - 1 : 0][I0];
+          const T yp = (k == MAXS - 1) ? pl[MAXS * py] : u0q[k + 1 < MAXS ? k + 1 : k][I0];
+          const T sum = ((u0q[k][IM] + u0q[k][IP]) + (ym + yp)) + (pl[k * py - 1] + pl[k * py + 1]);
+          const T r = fp[k * fpitch] - ((diag[k] + dz) * v0 - sum) * ih2;
           v1 = v0 + c0 * r;
         }
         u1q[k][I0] = v1;
-        if ((ex_mask >> k) & 1u) u1w[o] = v1;
+        if ((ex_mask >> k) & 1u) u1w[k * py] = v1;
       }
     }
     __syncthreads();  // (A) u1 plane z complete; u0 plane z no longer read
@@ -231,29 +243,28 @@ __global__ void __launch_bounds__(NTMAX, 1)
     if (z >= 1) {
       const int zz = z - 1;
       const int gz = oz + zz;
-      const bool zin = gz >= 0 && gz < L.N[2];
-      const bool zc = zin && zz >= 1 && zz <= Ez - 2;
-      const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
-      const T* u1r = u1s + (zz & 1) * a.s_stride + off0;
-      const T* fp = fs + (zz % kRing) * a.f_stride + fo0;
-      T* orow = oseg + (long long)zz * pz + (long long)s0 * py + off0;
-      // u1 planes z-2, z-1, z are in slots (R+1)%3, (R+2)%3, R; u0 plane z-1 in (R+2)%3
-      constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
-      if (zin) {
+      if (gz >= 0 && gz < L.N[2]) {
+        const bool zc = zz >= 1 && zz <= Ez - 2;
+        const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+        const T* u1r = u1b + (zz & 1) * a.s_stride;
+        const T* fp = fb + (zz % kRing) * a.f_stride;
+        T* orow = ob + (long long)zz * pz;
+        // u1 planes z-2, z-1, z are in slots (R+1)%3, (R+2)%3, R; u0 plane z-1 in (R+2)%3
+        constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) {
           if (!((w_mask >> k) & 1u)) continue;
-          const int o = k * offk;
           const T u0v = u0q[k][J1];
           T v2 = u0v;
           if (zc && ((c_mask >> k) & 1u)) {
             const T c1 = u1q[k][J1];
-            const T sum = ((u1q[k][J2] + u1q[k][J0]) + (u1r[o - py] + u1r[o + py])) +
-                          (u1r[o - 1] + u1r[o + 1]);
-            const T r = fp[k * fok] - ((diag[k] + dz) * c1 - sum) * ih2;
+            const T ym = (k == 0) ? u1r[-py] : u1q[k > 0 ? k - 1 : 0][J1];
+            const T yp = (k == MAXS - 1) ? u1r[MAXS * py] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
+            const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * py - 1] + u1r[k * py + 1]);
+            const T r = fp[k * fpitch] - ((diag[k] + dz) * c1 - sum) * ih2;
             v2 = c1 + cm * (c1 - u0v) + cr * r;
           }
-          orow[o] = v2;
+          orow[k * py] = v2;
         }
       }
     }
@@ -267,6 +278,198 @@ __global__ void __launch_bounds__(NTMAX, 1)
   }
 #undef ISSUE_U0
 #undef ISSUE_F
+}
+
+// =====================================================================================
+// Geometry-specialised variant: compile-time row pitch PY and band height BH, so every
+// smem/register offset is an immediate; ONE barrier per plane (u1 triple-buffered, u0 ring
+// of 3 planes indexed by z % 3, rhs ring of 4).  RG = 1: rhs is a dense global array
+// (tensor TMA, smem pitch PY + 16 B so the 16-byte aligned box start fits); RG = 0: rhs
+// is segment storage (1-D bulk copies, pitch PY).  Same arithmetic as k_cheb2.
+// =====================================================================================
+template <class T, int PY, int BH, int MAXS, int RG>
+struct SpecGeom {
+  static constexpr int kAl = 16 / (int)sizeof(T);
+  static constexpr int FP = RG ? PY + kAl : PY;
+  static constexpr int NG = (BH + 2 + MAXS - 1) / MAXS;
+  static constexpr int NT = PY * NG;
+  static constexpr int A = 128 / (int)sizeof(T);
+  static constexpr int U0S = ((BH + 4) * PY + A - 1) / A * A;
+  static constexpr int FS = ((BH + 2) * FP + A - 1) / A * A;
+  static constexpr int U1S = ((BH + 2) * PY + A - 1) / A * A;
+  static constexpr int RU = 3, RF = 4;
+  static constexpr size_t SMEM = (size_t)(RU * U0S + RF * FS + 3 * U1S) * sizeof(T) + 8 * (RU + RF);
+};
+
+template <class T, int PY, int BH, int MAXS, int RG>
+__global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
+    k_cheb2s(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
+  using G = SpecGeom<T, PY, BH, MAXS, RG>;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const Lvl& L = a.L;
+  const int Ex = L.E[0], Ey = L.E[1], Ez = L.E[2];
+  const long long pz = L.pz;
+  const int s = blockIdx.y;
+  const int r0 = blockIdx.x * BH, r1 = min(Ey, r0 + BH);
+  const int s0 = max(0, r0 - 1), s1 = min(Ey, r1 + 1);
+  const int q0 = max(0, r0 - 2), q1 = min(Ey, r1 + 2);
+  T* u0s = reinterpret_cast<T*>(sm);
+  T* fs = u0s + G::RU * G::U0S;
+  T* u1s = fs + G::RF * G::FS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + 3 * G::U1S);  // [0,3) u0, [3,7) f
+
+  const int px = s % L.ns[0];
+  const int pyy = (s / L.ns[0]) % L.ns[1];
+  const int pzz = s / (L.ns[0] * L.ns[1]);
+  const int ox = px * L.S[0] - (L.J + 1);
+  const int oy = pyy * L.S[1] - (L.J + 1);
+  const int oz = pzz * L.S[2] - (L.J + 1);
+  const T* useg = a.uin + (long long)s * L.ss;
+  T* oseg = a.uout + (long long)s * L.ss;
+  const T* rseg = RG ? nullptr : a.rhs_seg + (long long)s * L.ss;
+  const uint32_t u0_bytes = (uint32_t)((q1 - q0) * PY * sizeof(T));
+  const int oxa = ox & ~(G::kAl - 1);
+  const int fsh = RG ? ox - oxa : 0;
+  const uint32_t f_bytes = RG ? (uint32_t)((BH + 2) * G::FP * sizeof(T))
+                              : (uint32_t)((s1 - s0) * PY * sizeof(T));
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < G::RU + G::RF; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue_u0 = [=](int z) {
+    const int sl = z % 3;
+    mbar_expect_tx(&bars[sl], u0_bytes);
+    bulk_g2s(u0s + sl * G::U0S, useg + (long long)z * pz + (long long)q0 * PY, u0_bytes,
+             &bars[sl]);
+  };
+  auto issue_f = [=, &fmap](int z) {
+    const int sl = z & 3;
+    mbar_expect_tx(&bars[3 + sl], f_bytes);
+    if (RG)
+      tma_3d(fs + sl * G::FS, &fmap, oxa, oy + s0, oz + z, &bars[3 + sl]);
+    else
+      bulk_g2s(fs + sl * G::FS, rseg + (long long)z * pz + (long long)s0 * PY, f_bytes,
+               &bars[3 + sl]);
+  };
+  if (threadIdx.x == 0) {
+    for (int z = 0; z < min(3, Ez); ++z) {
+      issue_u0(z);
+      issue_f(z);
+    }
+  }
+
+  const int tx = threadIdx.x % PY, g = threadIdx.x / PY;
+  const int y0 = s0 + g * MAXS;
+  const int gxv = ox + tx;
+  const bool tok = tx < Ex && y0 < s1;
+  const bool tin = tok && gxv >= 0 && gxv < L.N[0];
+  const bool tcx = tx >= 1 && tx <= Ex - 2;
+  const int dxo = (gxv == 0 ? 1 : 0) + (gxv == L.N[0] - 1 ? 1 : 0);
+  unsigned ld_mask = 0, ex_mask = 0, c_mask = 0, w_mask = 0, yb_mask = 0;
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    const int y = y0 + k;
+    const int gy = oy + y;
+    const bool in = tin && y < s1 && gy >= 0 && gy < L.N[1];
+    if (tok && y < q1) ld_mask |= 1u << k;
+    if (tok && y < s1) ex_mask |= 1u << k;
+    if (in && tcx && y >= 1 && y <= Ey - 2) c_mask |= 1u << k;
+    if (in && y >= r0 && y < r1) w_mask |= 1u << k;
+    yb_mask |= (unsigned)((gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0)) << (2 * k);
+  }
+  const T* const u0b = u0s + (y0 - q0) * PY + tx;
+  const T* const fb = fs + (y0 - s0) * G::FP + tx + fsh;
+  T* const u1b = u1s + (y0 - s0) * PY + tx;
+  T* const ob = oseg + (long long)y0 * PY + tx;
+  T u0q[MAXS][3], u1q[MAXS][3];
+  mbar_wait(&bars[0], 0);
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    u0q[k][0] = ((ld_mask >> k) & 1u) ? u0b[k * PY] : T(0);
+    u0q[k][1] = u0q[k][2] = T(0);
+    u1q[k][0] = u1q[k][1] = u1q[k][2] = T(0);
+  }
+  const T ih2 = T(L.inv_h2);
+  const T c0 = a.c0, cm = a.cm, cr = a.cr;
+  const T six = T(6 + dxo);
+
+  auto step = [&](auto RR, int z) {
+    constexpr int R = decltype(RR)::value;  // z % 3: u0 ring slot, u1 buffer, queue slot
+    constexpr int IM = (R + 2) % 3, I0 = R, IP = (R + 1) % 3;
+    if (z < Ez) {
+      if (z + 1 < Ez) mbar_wait(&bars[IP], ((z + 1) / 3) & 1);
+      mbar_wait(&bars[3 + (z & 3)], (z >> 2) & 1);
+      const T* pl = u0b + R * G::U0S;
+      const T* pn = u0b + IP * G::U0S;
+      const T* fp = fb + (z & 3) * G::FS;
+      T* u1w = u1b + R * G::U1S;
+      const int gz = oz + z;
+      const bool zc = gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2;
+      const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+      if (z + 1 < Ez) {
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k)
+          if ((ld_mask >> k) & 1u) u0q[k][IP] = pn[k * PY];
+      } else {
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) u0q[k][IP] = T(0);
+      }
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) {
+        const T v0 = u0q[k][I0];
+        T v1 = v0;
+        if (zc && ((c_mask >> k) & 1u)) {
+          const T ym = (k == 0) ? pl[-PY] : u0q[k > 0 ? k - 1 : 0][I0];
+          const T yp = (k == MAXS - 1) ? pl[MAXS * PY] : u0q[k + 1 < MAXS ? k + 1 : k][I0];
+          const T sum = ((u0q[k][IM] + u0q[k][IP]) + (ym + yp)) + (pl[k * PY - 1] + pl[k * PY + 1]);
+          const T d = dg + T((yb_mask >> (2 * k)) & 3u);
+          const T r = fp[k * G::FP] - (d * v0 - sum) * ih2;
+          v1 = v0 + c0 * r;
+        }
+        u1q[k][I0] = v1;
+        if ((ex_mask >> k) & 1u) u1w[k * PY] = v1;
+      }
+    }
+    __syncthreads();  // the only barrier of the plane step
+    if (threadIdx.x == 0) {
+      if (z + 3 < Ez) issue_u0(z + 3);                  // u0 slot z%3 is free
+      if (z >= 1 && z + 2 < Ez) issue_f(z + 2);         // rhs slot (z-2)&3 is free
+    }
+    if (z >= 1) {
+      const int zz = z - 1;
+      const int gz = oz + zz;
+      if (gz >= 0 && gz < L.N[2]) {
+        const bool zc = zz >= 1 && zz <= Ez - 2;
+        const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+        constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
+        const T* u1r = u1b + J1 * G::U1S;
+        const T* fp = fb + (zz & 3) * G::FS;
+        T* orow = ob + (long long)zz * pz;
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) {
+          if (!((w_mask >> k) & 1u)) continue;
+          const T u0v = u0q[k][J1];
+          T v2 = u0v;
+          if (zc && ((c_mask >> k) & 1u)) {
+            const T c1 = u1q[k][J1];
+            const T ym = (k == 0) ? u1r[-PY] : u1q[k > 0 ? k - 1 : 0][J1];
+            const T yp = (k == MAXS - 1) ? u1r[MAXS * PY] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
+            const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
+            const T d = dg + T((yb_mask >> (2 * k)) & 3u);
+            const T r = fp[k * G::FP] - (d * c1 - sum) * ih2;
+            v2 = c1 + cm * (c1 - u0v) + cr * r;
+          }
+          orow[k * PY] = v2;
+        }
+      }
+    }
+  };
+  for (int zb = 0; zb <= Ez; zb += 3) {
+    step(std::integral_constant<int, 0>{}, zb);
+    if (zb + 1 <= Ez) step(std::integral_constant<int, 1>{}, zb + 1);
+    if (zb + 2 <= Ez) step(std::integral_constant<int, 2>{}, zb + 2);
+  }
 }
 
 // ---- host side ---------------------------------------------------------------------
@@ -323,7 +526,7 @@ Plan make_plan(const Lvl& L, int MAXS, int NTMAX) {
     const long long fsz =
         round_up_ll((long long)(BH + 2) * std::max(bw, L.py) * sizeof(T), 128) / sizeof(T);
     const size_t smem = (size_t)(kRing * u0s + kRing * fsz + 2 * ss) * sizeof(T) + 2 * kRing * 8;
-    const int rows = std::min(Ey, BH + 2);
+    const int rows = std::min(Ey, BH + 2);  // stage-1 rows of a band (upper bound)
     const int NT = (int)round_up_ll((long long)Ex * ((rows + MAXS - 1) / MAXS), 32);
     if (smem <= 227 * 1024 && NT <= NTMAX && BH + 2 <= 256 && bw <= 256) {
       pl.BH = BH;
@@ -352,9 +555,84 @@ bool cheb2_fused_ok(const Lvl& L) {
   return make_plan<T>(L, v.maxs, v.nt).BH > 0;
 }
 
+namespace {
+
+bool spec_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SR_FMG_CHEB2_SPEC");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <class T>
+bool encode_rhs_map(CUtensorMap* map, const Lvl& L, const T* p, int bw, int rows) {
+  const cuuint64_t dims[3] = {(cuuint64_t)L.N[0], (cuuint64_t)L.N[1], (cuuint64_t)L.N[2]};
+  const cuuint64_t strides[2] = {(cuuint64_t)L.N[0] * sizeof(T),
+                                 (cuuint64_t)L.N[0] * L.N[1] * sizeof(T)};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = get_encode()(
+      map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+      const_cast<T*>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fprintf(stderr, "sr_fmg: cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+  return r == CUDA_SUCCESS;
+}
+
+// geometry-specialised launch if (T, row pitch) has an instantiation
+template <class T, int PY, int BH, int MAXS>
+bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, cudaStream_t st) {
+  if (L.py != PY || L.E[0] > PY) return false;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  dim3 grid((L.E[1] + BH - 1) / BH, L.nsegs);
+  if (b.global) {
+    using G = SpecGeom<T, PY, BH, MAXS, 1>;
+    if (!encode_rhs_map<T>(&map, L, b.p, G::FP, BH + 2)) return false;
+    auto kern = k_cheb2s<T, PY, BH, MAXS, 1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    kern<<<grid, G::NT, G::SMEM, st>>>(map, a);
+  } else {
+    using G = SpecGeom<T, PY, BH, MAXS, 0>;
+    auto kern = k_cheb2s<T, PY, BH, MAXS, 0>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    kern<<<grid, G::NT, G::SMEM, st>>>(map, a);
+  }
+  return true;
+}
+
+template <class T>
+bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, cudaStream_t st) {
+  if (!spec_enabled()) return false;
+  if constexpr (sizeof(T) == 8)
+    return try_spec<T, 72, 35, 4>(L, a, b, st) || try_spec<T, 40, 19, 3>(L, a, b, st) ||
+           try_spec<T, 24, 22, 3>(L, a, b, st) || try_spec<T, 16, 14, 2>(L, a, b, st);
+  else
+    return try_spec<T, 72, 70, 6>(L, a, b, st) || try_spec<T, 40, 38, 4>(L, a, b, st) ||
+         try_spec<T, 24, 22, 3>(L, a, b, st) || try_spec<T, 16, 14, 2>(L, a, b, st);
+}
+
+}  // namespace
+
 template <class T>
 void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
                         double cr, cudaStream_t st) {
+  {
+    Cheb2Args<T> a{};
+    a.L = L;
+    a.uin = u_in;
+    a.uout = u_out;
+    a.rhs_seg = b.global ? nullptr : b.p;
+    a.rhs_global = b.global;
+    a.c0 = (T)c0;
+    a.cm = (T)cm;
+    a.cr = (T)cr;
+    if (launch_spec<T>(L, a, b, st)) return;
+  }
   const Variant v = variant<T>();
   const Plan pl = make_plan<T>(L, v.maxs, v.nt);
   CUtensorMap map;
