@@ -39,7 +39,7 @@ WORKLOADS = {
 # bounded CPU sample of C3 for the oracle: the same 8^3 segment grid, K = 4, J = 2, at
 # 128^3 (1/64 of the cells); about 7 s of numpy per solve on one core
 ORACLE_SAMPLE = dict(n=(128, 128, 128), M=6, seg=16, buffer=2, K=4, rhs="manufactured+noise")
-KC_CHEB = 0  # kernel class index of k_cheb_step (sr_fmg_kernel_name)
+KC_CHEB_FUSED = 7  # kernel class index of the fused TMA Chebyshev pass (sr_fmg_kernel_name)
 
 
 def parse():
@@ -185,7 +185,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K solves; CUDA events around every fine-level Chebyshev sweep
-    solver.profile_select(KC_CHEB, solver.M)
+    solver.profile_select(KC_CHEB_FUSED, solver.M)
     solver.solve(f, u)  # re-capture the graph with the profiling events (untimed)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -254,7 +254,7 @@ def main():
                    "parallelism": "independent replicas per GPU" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (f %.2f GB, workspace %.2f GB)"
                          % (nbytes / 1e9, solver.workspace_bytes / 1e9)},
-        "roofline": {"bound": "hbm", "kernel": "k_cheb_step @ finest level",
+        "roofline": {"bound": "hbm", "kernel": "k_cheb2/k_cheb2s (fused TMA Chebyshev pass) @ finest level",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                      "traffic": traffic,

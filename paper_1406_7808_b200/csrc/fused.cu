@@ -301,7 +301,7 @@ struct SpecGeom {
   static constexpr size_t SMEM = (size_t)(RU * U0S + RF * FS + 3 * U1S) * sizeof(T) + 8 * (RU + RF);
 };
 
-template <class T, int PY, int BH, int MAXS, int RG>
+template <class T, int PY, int BH, int MAXS, int RG, int NST>
 __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
     k_cheb2s(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
   using G = SpecGeom<T, PY, BH, MAXS, RG>;
@@ -427,8 +427,14 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
           const T r = fp[k * G::FP] - (d * v0 - sum) * ih2;
           v1 = v0 + c0 * r;
         }
-        u1q[k][I0] = v1;
-        if ((ex_mask >> k) & 1u) u1w[k * PY] = v1;
+        if constexpr (NST == 2) {
+          u1q[k][I0] = v1;
+          if ((ex_mask >> k) & 1u) u1w[k * PY] = v1;
+        } else {
+          // degree 1: the first step is the result (C updated, GSR copied)
+          if (((w_mask >> k) & 1u) && gz >= 0 && gz < L.N[2])
+            ob[(long long)z * pz + k * PY] = v1;
+        }
       }
     }
     __syncthreads();  // the only barrier of the plane step
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
       if (z + 3 < Ez) issue_u0(z + 3);                  // u0 slot z%3 is free
       if (z >= 1 && z + 2 < Ez) issue_f(z + 2);         // rhs slot (z-2)&3 is free
     }
-    if (z >= 1) {
+    if (NST == 2 && z >= 1) {
       const int zz = z - 1;
       const int gz = oz + zz;
       if (gz >= 0 && gz < L.N[2]) {
@@ -585,35 +591,37 @@ bool encode_rhs_map(CUtensorMap* map, const Lvl& L, const T* p, int bw, int rows
 
 // geometry-specialised launch if (T, row pitch) has an instantiation
 template <class T, int PY, int BH, int MAXS>
-bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, cudaStream_t st) {
+bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
   if (L.py != PY || L.E[0] > PY) return false;
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   dim3 grid((L.E[1] + BH - 1) / BH, L.nsegs);
+  auto go = [&](auto kern, size_t smem, int nt) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, nt, smem, st>>>(map, a);
+  };
   if (b.global) {
     using G = SpecGeom<T, PY, BH, MAXS, 1>;
     if (!encode_rhs_map<T>(&map, L, b.p, G::FP, BH + 2)) return false;
-    auto kern = k_cheb2s<T, PY, BH, MAXS, 1>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    kern<<<grid, G::NT, G::SMEM, st>>>(map, a);
+    if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 1, 2>, G::SMEM, G::NT);
+    else go(k_cheb2s<T, PY, BH, MAXS, 1, 1>, G::SMEM, G::NT);
   } else {
     using G = SpecGeom<T, PY, BH, MAXS, 0>;
-    auto kern = k_cheb2s<T, PY, BH, MAXS, 0>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    kern<<<grid, G::NT, G::SMEM, st>>>(map, a);
+    if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 0, 2>, G::SMEM, G::NT);
+    else go(k_cheb2s<T, PY, BH, MAXS, 0, 1>, G::SMEM, G::NT);
   }
   return true;
 }
 
 template <class T>
-bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, cudaStream_t st) {
+bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
   if (!spec_enabled()) return false;
   if constexpr (sizeof(T) == 8)
-    return try_spec<T, 72, 35, 4>(L, a, b, st) || try_spec<T, 40, 19, 3>(L, a, b, st) ||
-           try_spec<T, 24, 22, 3>(L, a, b, st) || try_spec<T, 16, 14, 2>(L, a, b, st);
+    return try_spec<T, 72, 35, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
+           try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);
   else
-    return try_spec<T, 72, 70, 6>(L, a, b, st) || try_spec<T, 40, 38, 4>(L, a, b, st) ||
-         try_spec<T, 24, 22, 3>(L, a, b, st) || try_spec<T, 16, 14, 2>(L, a, b, st);
+    return try_spec<T, 72, 70, 6>(L, a, b, nst, st) || try_spec<T, 40, 38, 4>(L, a, b, nst, st) ||
+           try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);
 }
 
 }  // namespace
@@ -631,7 +639,7 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
     a.c0 = (T)c0;
     a.cm = (T)cm;
     a.cr = (T)cr;
-    if (launch_spec<T>(L, a, b, st)) return;
+    if (launch_spec<T>(L, a, b, 2, st)) return;
   }
   const Variant v = variant<T>();
   const Plan pl = make_plan<T>(L, v.maxs, v.nt);
@@ -679,6 +687,35 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
   else go(k_cheb2<T, D ? 4 : 6, 768>);
 }
 
+template <class T>
+bool cheb_spec_ok(const Lvl& L) {
+  if (!spec_enabled() || !get_encode() || ((long long)L.N[0] * sizeof(T)) % 16) return false;
+  const int pys[4] = {72, 40, 24, 16};
+  for (int p : pys)
+    if (L.py == p && L.E[0] <= p) return true;
+  return false;
+}
+template bool cheb_spec_ok<double>(const Lvl&);
+template bool cheb_spec_ok<float>(const Lvl&);
+
+template <class T>
+bool launch_cheb1_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0,
+                        cudaStream_t st) {
+  if (!get_encode()) return false;
+  Cheb2Args<T> a{};
+  a.L = L;
+  a.uin = u_in;
+  a.uout = u_out;
+  a.rhs_seg = b.global ? nullptr : b.p;
+  a.rhs_global = b.global;
+  a.c0 = (T)c0;
+  return launch_spec<T>(L, a, b, 1, st);
+}
+
+template bool launch_cheb1_fused<double>(const Lvl&, const double*, double*, FusedRhs<double>,
+                                         double, cudaStream_t);
+template bool launch_cheb1_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>, double,
+                                        cudaStream_t);
 template void launch_cheb2_fused<double>(const Lvl&, const double*, double*, FusedRhs<double>,
                                          double, double, double, cudaStream_t);
 template void launch_cheb2_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>, double,

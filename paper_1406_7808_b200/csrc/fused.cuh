@@ -19,6 +19,16 @@ template <class T>
 void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
                         double cr, cudaStream_t st);
 
+// One degree-1 Chebyshev step (single stencil stage) with the same TMA pipeline; returns
+// false (nothing launched) when no geometry-specialised instantiation matches the level.
+template <class T>
+bool launch_cheb1_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0,
+                        cudaStream_t st);
+
+// A geometry-specialised instantiation exists for this level's row pitch.
+template <class T>
+bool cheb_spec_ok(const Lvl& L);
+
 // Fused-kernel availability for a level (smem budget etc.); false -> use the step kernels.
 template <class T>
 bool cheb2_fused_ok(const Lvl& L);

@@ -10,9 +10,9 @@
 
 namespace srfmg {
 
-const char* const kKernelNames[] = {"k_cheb_step", "k_restrict", "k_tau", "k_prolong",
-                                    "k_coarsest", "k_pyramid", "k_gather"};
-const int kNumKernelNames = 7;
+const char* const kKernelNames[] = {"k_cheb_step", "k_restrict", "k_tau",     "k_prolong",
+                                    "k_coarsest",  "k_pyramid",  "k_gather",  "k_cheb2"};
+const int kNumKernelNames = 8;
 
 namespace {
 
@@ -390,33 +390,44 @@ __global__ void __launch_bounds__(kThreads) k_prolong(Lvl Lf, T* __restrict__ uf
       dst[j] = sg * v;
     }
   };
-  T qm[4], q0[4], qp[4];
+  // coarse planes P-1 .. P+2 (queue), fine planes 2P .. 2P+3 per batch: all loads of a
+  // batch are issued before any use (memory-level parallelism)
+  T q[4][4];
   int P = gz0 >> 1;
-  load_plane(P - 1, qm);
-  load_plane(P, q0);
+  load_plane(P - 1, q[0]);
+  load_plane(P, q[1]);
   const long long fcol = (long long)s * Lf.ss + (long long)c.ay * Lf.py + c.ax;
-  for (; 2 * P < gz1; ++P) {
-    load_plane(P + 1, qp);
+  for (; 2 * P < gz1; P += 2) {
+    load_plane(P + 1, q[2]);
+    load_plane(P + 2, q[3]);
+    T uo[4];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
+    for (int e = 0; e < 4; ++e) {
+      const int gz = 2 * P + e;
+      uo[e] = T(0);
+      if (add && gz >= gz0 && gz < gz1) uo[e] = uf[fcol + (long long)(gz - o[2]) * Lf.pz];
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
       const int gz = 2 * P + e;
       if (gz < gz0 || gz >= gz1) continue;
-      const T* qn = e ? qp : qm;
+      const T* qp = q[1 + (e >> 1)];                             // parent plane P + e/2
+      const T* qn = (e & 1) ? q[2 + (e >> 1)] : q[e >> 1];       // neighbour on the child's side
       T acc = T(0);
 #pragma unroll
       for (int kz = 0; kz < 2; ++kz)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const T v = kz ? qn[j] : q0[j];
+          const T v = kz ? qn[j] : qp[j];
           acc += (W[kz] * W[j >> 1] * W[j & 1]) * (sxy[j] * v);
         }
       const long long off = fcol + (long long)(gz - o[2]) * Lf.pz;
-      uf[off] = add ? uf[off] + acc : acc;
+      uf[off] = add ? uo[e] + acc : acc;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      qm[j] = q0[j];
-      q0[j] = qp[j];
+      q[0][j] = q[2][j];
+      q[1][j] = q[3][j];
     }
   }
 }

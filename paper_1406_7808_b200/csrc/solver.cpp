@@ -22,8 +22,9 @@ namespace {
 
 thread_local std::string g_tls_err = "no error";
 
+// indices into srfmg::kKernelNames (sr_fmg_kernel_name)
 enum KernelClass { KC_CHEB = 0, KC_RESTRICT, KC_TAU, KC_PROLONG, KC_COARSEST, KC_PYRAMID,
-                   KC_GATHER, KC_COUNT };
+                   KC_GATHER, KC_CHEB_FUSED, KC_COUNT };
 
 struct LevelBufs {
   void* u[2] = {nullptr, nullptr};  // two solution buffers (Chebyshev ping-pong)
@@ -324,14 +325,25 @@ struct Schedule {
     const Lvl& L = h->L[l];
     LevelBufs& bb = h->B[l];
     const CellCounts& c = h->cells[l];
-    if (deg == 2 && h->fused && srfmg::cheb2_fused_ok<T>(L)) {
+    // the fused pass marches z inside a CTA: use it only when segments x bands fill the
+    // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
+    if (deg == 2 && h->fused && (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
+        srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
       const double rho0 = 1.0 / h->sigma[l];
       const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
-      Launch g(h, st, KC_CHEB, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
+      Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb2_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
                                    srfmg::FusedRhs<T>{b.p, b.global}, 1.0 / h->theta[l],
                                    rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
+      bb.cur = 1 - bb.cur;
+      return;
+    }
+    if (deg == 1 && h->fused && (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
+        srfmg::cheb_spec_ok<T>(L)) {
+      Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
+      srfmg::launch_cheb1_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
+                                   srfmg::FusedRhs<T>{b.p, b.global}, 1.0 / h->theta[l], st);
       bb.cur = 1 - bb.cur;
       return;
     }
