@@ -372,9 +372,11 @@ __global__ void __launch_bounds__(kThreads) k_prolong(Lvl Lf, T* __restrict__ uf
   long long coff[4];  // j = ky*2 + kx
 #pragma unroll
   for (int j = 0; j < 4; ++j) coff[j] = cbase + (long long)cy[j >> 1] * Lc.py + cx[j & 1];
-  const T sxy[4] = {T(1), sx1, sy1, sy1 * sx1};
+  // separable trilinear: the (x, y) interpolation of coarse plane P is shared by the two
+  // fine planes 2P, 2P+1 (weights 3/4 parent, 1/4 neighbour; signs of reflected ghosts)
   const T W[2] = {T(0.75), T(0.25)};
-  auto load_plane = [&](int P, T* dst) {  // coarse plane P (reflected if outside Omega_c)
+  const T wxy[4] = {W[0] * W[0], W[0] * W[1] * sx1, W[1] * W[0] * sy1, W[1] * W[1] * (sy1 * sx1)};
+  auto load_plane = [&](int P) -> T {  // xy-interpolant of coarse plane P (reflected outside)
     T sg = T(1);
     int Pm = P;
     if (P < 0) { Pm = 0; sg = T(-1); }
@@ -383,23 +385,24 @@ __global__ void __launch_bounds__(kThreads) k_prolong(Lvl Lf, T* __restrict__ uf
     // storage box (small J): clamp them into it (their values are never used)
     const int lz = min(max(Pm - oc[2], 0), Lc.E[2] - 1);
     const long long zo = (long long)lz * Lc.pz;
+    T v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      T v = w[coff[j] + zo];
-      if (add) v = v - tc[coff[j] + zo];
-      dst[j] = sg * v;
+      v[j] = w[coff[j] + zo];
+      if (add) v[j] = v[j] - tc[coff[j] + zo];
     }
+    return sg * ((wxy[0] * v[0] + wxy[1] * v[1]) + (wxy[2] * v[2] + wxy[3] * v[3]));
   };
   // coarse planes P-1 .. P+2 (queue), fine planes 2P .. 2P+3 per batch: all loads of a
   // batch are issued before any use (memory-level parallelism)
-  T q[4][4];
+  T q[4];
   int P = gz0 >> 1;
-  load_plane(P - 1, q[0]);
-  load_plane(P, q[1]);
+  q[0] = load_plane(P - 1);
+  q[1] = load_plane(P);
   const long long fcol = (long long)s * Lf.ss + (long long)c.ay * Lf.py + c.ax;
   for (; 2 * P < gz1; P += 2) {
-    load_plane(P + 1, q[2]);
-    load_plane(P + 2, q[3]);
+    q[2] = load_plane(P + 1);
+    q[3] = load_plane(P + 2);
     T uo[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -411,24 +414,14 @@ __global__ void __launch_bounds__(kThreads) k_prolong(Lvl Lf, T* __restrict__ uf
     for (int e = 0; e < 4; ++e) {
       const int gz = 2 * P + e;
       if (gz < gz0 || gz >= gz1) continue;
-      const T* qp = q[1 + (e >> 1)];                             // parent plane P + e/2
-      const T* qn = (e & 1) ? q[2 + (e >> 1)] : q[e >> 1];       // neighbour on the child's side
-      T acc = T(0);
-#pragma unroll
-      for (int kz = 0; kz < 2; ++kz)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const T v = kz ? qn[j] : qp[j];
-          acc += (W[kz] * W[j >> 1] * W[j & 1]) * (sxy[j] * v);
-        }
+      const T qp = q[1 + (e >> 1)];                            // parent plane P + e/2
+      const T qn = (e & 1) ? q[2 + (e >> 1)] : q[e >> 1];      // neighbour on the child's side
+      const T acc = W[0] * qp + W[1] * qn;
       const long long off = fcol + (long long)(gz - o[2]) * Lf.pz;
       uf[off] = add ? uo[e] + acc : acc;
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      q[0][j] = q[2][j];
-      q[1][j] = q[3][j];
-    }
+    q[0] = q[2];
+    q[1] = q[3];
   }
 }
 

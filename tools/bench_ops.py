@@ -27,7 +27,7 @@ f = torch.from_numpy(W.make_rhs(rhs, n).astype(np.float64 if a.dtype == "f64" el
 u = torch.empty_like(f)
 s.solve(f, u)
 torch.cuda.synchronize()
-l = M if a.level < 0 else a.level
+l = (M - 1 if a.op == 'tau' else M) if a.level < 0 else a.level
 op, deg = {"cheb1": (0, 1), "cheb2": (0, 2), "restrict": (1, 0), "tau": (2, 0),
            "prolong": (3, 0), "correct": (4, 0)}[a.op]
 for _ in range(2):
