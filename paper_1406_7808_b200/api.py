@@ -106,7 +106,8 @@ class Solver:
 
     @property
     def launches_per_solve(self) -> int:
-        return self._info.launches_per_solve
+        """Kernel launches of the last solve (exact once a solve has been enqueued)."""
+        return self._get_info().launches_per_solve
 
     @property
     def alg_bytes_per_solve(self) -> float:

@@ -83,6 +83,7 @@ struct Cheb2Args {
   int f_stride;      // elements per rhs plane buffer
   int bw;            // rhs tensor-map box width (global rhs; 16-byte aligned start)
   T c0, cm, cr;
+  T* ufinal;         // non-null: write only genuine cells, to this dense user array (last pass)
 };
 
 long long round_up_ll(long long v, long long m) { return (v + m - 1) / m * m; }
@@ -466,7 +467,16 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
             const T r = fp[k * G::FP] - (d * c1 - sum) * ih2;
             v2 = c1 + cm * (c1 - u0v) + cr * r;
           }
-          orow[k * PY] = v2;
+          if (a.ufinal == nullptr) {
+            orow[k * PY] = v2;
+          } else {
+            // last pass of the solve (R19): genuine cells straight to the user's u
+            const int y = y0 + k;
+            const int vlo = L.J + 1;
+            if (tx >= vlo && tx < vlo + L.S[0] && y >= vlo && y < vlo + L.S[1] &&
+                zz >= vlo && zz < vlo + L.S[2])
+              a.ufinal[((long long)gz * L.N[1] + (oy + y)) * L.N[0] + gxv] = v2;
+          }
         }
       }
     }
@@ -627,10 +637,18 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
 }  // namespace
 
 template <class T>
+bool cheb2_final_ok(const Lvl& L) {
+  return cheb_spec_ok<T>(L);
+}
+template bool cheb2_final_ok<double>(const Lvl&);
+template bool cheb2_final_ok<float>(const Lvl&);
+
+template <class T>
 void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
-                        double cr, cudaStream_t st) {
+                        double cr, cudaStream_t st, T* ufinal) {
   {
     Cheb2Args<T> a{};
+    a.ufinal = ufinal;
     a.L = L;
     a.uin = u_in;
     a.uout = u_out;
@@ -662,7 +680,7 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
               (unsigned long long)dims[2], box[0], box[1]);
     }
   }
-  Cheb2Args<T> a;
+  Cheb2Args<T> a{};
   a.L = L;
   a.uin = u_in;
   a.uout = u_out;
@@ -717,9 +735,9 @@ template bool launch_cheb1_fused<double>(const Lvl&, const double*, double*, Fus
 template bool launch_cheb1_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>, double,
                                         cudaStream_t);
 template void launch_cheb2_fused<double>(const Lvl&, const double*, double*, FusedRhs<double>,
-                                         double, double, double, cudaStream_t);
+                                         double, double, double, cudaStream_t, double*);
 template void launch_cheb2_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>, double,
-                                        double, double, cudaStream_t);
+                                        double, double, cudaStream_t, float*);
 template bool cheb2_fused_ok<double>(const Lvl&);
 template bool cheb2_fused_ok<float>(const Lvl&);
 

@@ -15,9 +15,13 @@ struct FusedRhs {
 // One degree-2 Chebyshev application (two sweeps, R8) on C of every segment of level L,
 // in ONE pass over HBM: u_in (complete: C and GSR) -> u_out (C updated, GSR copied).
 // c0 = 1/theta (first step), cm = rho1 rho0, cr = 2 rho1 / delta (second step).
+// ufinal != nullptr: the last smoothing of the solve -- write only the genuine cells, to the
+// user's dense u (R19), and not the segment storage (only for cheb2_final_ok levels).
 template <class T>
 void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
-                        double cr, cudaStream_t st);
+                        double cr, cudaStream_t st, T* ufinal = nullptr);
+template <class T>
+bool cheb2_final_ok(const Lvl& L);
 
 // One degree-1 Chebyshev step (single stencil stage) with the same TMA pipeline; returns
 // false (nothing launched) when no geometry-specialised instantiation matches the level.

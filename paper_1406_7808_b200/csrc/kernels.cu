@@ -294,28 +294,55 @@ __global__ void __launch_bounds__(kThreads) k_tau(Lvl L, const T* __restrict__ u
   const long long col = (long long)s * L.ss + (long long)c.ay * L.py + c.ax;
   const T* cc = u + col;
   const long long pz = L.pz, py = L.py;
-  T zm = c.z0 > 0 ? cc[(long long)(c.z0 - 1) * pz] : T(0);
-  T v0 = cc[(long long)c.z0 * pz];
-  for (int az = c.z0; az < c.z1; ++az) {
-    const long long zo = (long long)az * pz;
-    const T zp = (az + 1 < L.E[2]) ? cc[zo + pz] : T(0);
-    const int gz = o[2] + az;
-    if (gz >= 0 && gz < L.N[2]) {
-      t[col + zo] = v0;
-      if (cxy && az >= 1 && az <= L.E[2] - 2) {
-        T sum = (gz > 0) ? zm : -v0;
-        sum += (gz < L.N[2] - 1) ? zp : -v0;
-        sum += ym ? cc[zo - py] : -v0;
-        sum += yp ? cc[zo + py] : -v0;
-        sum += xm ? cc[zo - 1] : -v0;
-        sum += xp ? cc[zo + 1] : -v0;
-        const T Au = (T(6) * v0 - sum) * T(L.inv_h2);
-        const bool inF = fxy && gz >= fz0 && gz < fz1;
-        rhs[col + zo] = inF ? rhs[col + zo] + Au : Au;
+  const int E2 = L.E[2], N2 = L.N[2];
+  constexpr int U = 4;  // planes per batch: all loads of a batch are issued before any use
+  T zq[U + 2];
+  zq[0] = c.z0 > 0 ? cc[(long long)(c.z0 - 1) * pz] : T(0);
+  zq[1] = cc[(long long)c.z0 * pz];
+  for (int az = c.z0; az < c.z1; az += U) {
+    T nb[U][4], rv[U];
+    bool act[U], inn[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int zz = az + 1 + k;
+      zq[k + 2] = (zz < E2) ? cc[(long long)zz * pz] : T(0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int z = az + k;
+      const int gz = o[2] + z;
+      act[k] = z < c.z1 && gz >= 0 && gz < N2;
+      inn[k] = act[k] && cxy && z >= 1 && z <= E2 - 2;
+      const long long zo = (long long)z * pz;
+      if (inn[k]) {
+        nb[k][0] = ym ? cc[zo - py] : T(0);
+        nb[k][1] = yp ? cc[zo + py] : T(0);
+        nb[k][2] = xm ? cc[zo - 1] : T(0);
+        nb[k][3] = xp ? cc[zo + 1] : T(0);
+        rv[k] = (fxy && gz >= fz0 && gz < fz1) ? rhs[col + zo] : T(0);
       }
     }
-    zm = v0;
-    v0 = zp;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int z = az + k;
+      const int gz = o[2] + z;
+      const long long zo = (long long)z * pz;
+      const T v0 = zq[k + 1];
+      if (act[k]) t[col + zo] = v0;
+      if (inn[k]) {
+        T sum = (gz > 0) ? zq[k] : -v0;
+        sum += (gz < N2 - 1) ? zq[k + 2] : -v0;
+        sum += ym ? nb[k][0] : -v0;
+        sum += yp ? nb[k][1] : -v0;
+        sum += xm ? nb[k][2] : -v0;
+        sum += xp ? nb[k][3] : -v0;
+        const T Au = (T(6) * v0 - sum) * T(L.inv_h2);
+        const bool inF = fxy && gz >= fz0 && gz < fz1;
+        rhs[col + zo] = inF ? rv[k] + Au : Au;
+      }
+    }
+    zq[0] = zq[U];
+    zq[1] = zq[U + 1];
   }
 }
 

@@ -320,7 +320,10 @@ struct Schedule {
   }
 
   // S^deg(L_l, u_l, b) on C_l of every segment (R8): ping-pong between the two buffers
-  void cheb(int l, int deg, View<T> b) {
+  T* final_out = nullptr;  // user u: the last level-M smoothing writes it directly (R19)
+  bool final_done = false;
+
+  void cheb(int l, int deg, View<T> b, bool last = false) {
     if (deg <= 0) return;
     const Lvl& L = h->L[l];
     LevelBufs& bb = h->B[l];
@@ -332,11 +335,17 @@ struct Schedule {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
       const double rho0 = 1.0 / h->sigma[l];
       const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
-      Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
+      const bool fin = last && final_out != nullptr && srfmg::cheb2_final_ok<T>(L);
+      const double nv = (double)L.N[0] * L.N[1] * L.N[2];
+      Launch g(h, st, KC_CHEB_FUSED, l,
+               fin ? w * (2.0 * c.compute + nv)
+                   : w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb2_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
                                    srfmg::FusedRhs<T>{b.p, b.global}, 1.0 / h->theta[l],
-                                   rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
+                                   rho1 * rho0, 2.0 * rho1 / h->delta[l], st,
+                                   fin ? final_out : nullptr);
       bb.cur = 1 - bb.cur;
+      if (fin) final_done = true;
       return;
     }
     if (deg == 1 && h->fused && (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
@@ -410,11 +419,13 @@ struct Schedule {
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
     prolong(l, 1);                // L118 / L241
-    cheb(l, h->d.nu2, b);         // L119 / L242
+    cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
   }
 
   void run(T* uout) {
     const int M = h->M;
+    final_out = uout;
+    final_done = false;
     for (int l = M; l >= 1; --l) {  // R6: f pyramid
       const Lvl& L = h->L[l];
       Launch g(h, st, KC_PYRAMID, l, w * (double)L.N[0] * L.N[1] * L.N[2] * (1.0 + 1.0 / 8));
@@ -427,7 +438,7 @@ struct Schedule {
       cheb(l, h->d.alpha, fview(l));
       vcycle(l, fview(l));
     }
-    {
+    if (!final_done) {
       const Lvl& L = h->L[M];
       Launch g(h, st, KC_GATHER, M, w * 2.0 * L.N[0] * (double)L.N[1] * L.N[2]);
       srfmg::launch_gather<T>(L, U(M), uout, st);  // R19
@@ -698,7 +709,8 @@ sr_status_t sr_fmg_get_info(const sr_fmg_t* h, sr_fmg_info_t* info) {
     n = h->M + 1 + 1;
     for (int l = 1; l <= h->M; ++l) n += 1 + cheb_n(h->d.alpha) + vc[l];
   }
-  info->launches_per_solve = n;
+  // launches of the last enqueued solve (exact), else the unfused schedule's count
+  info->launches_per_solve = h->launches > 0 ? h->launches : n;
   info->alg_bytes_per_solve = alg_bytes(h);
   return SR_OK;
 }
