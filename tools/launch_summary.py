@@ -55,5 +55,26 @@ def main(path):
               f"{t*1e3:7.3f} ms  {b/1e9:6.3f} GB  {b/t/1e9 if t else 0:6.0f} GB/s")
 
 
+
+
+def by_grid(path):
+    """Group launches by (kernel, grid) ~ (kernel, level)."""
+    L = load(path)
+    agg = collections.OrderedDict()
+    for r in L:
+        k = (short(r["name"]), r["grid"], r["block"])
+        a = agg.setdefault(k, [0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += r.get("gpu__time_duration.sum", 0.0)
+        a[2] += r.get("dram__bytes_read.sum", 0.0) + r.get("dram__bytes_write.sum", 0.0)
+    T = sum(v[1] for v in agg.values())
+    for (k, g, b), (n, t, by) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{k:14s} {g:>16s} {b:>12s} n={n:3d} {t*1e3:8.3f} ms {100*t/T:5.1f}%  "
+              f"{t/n*1e6:8.1f} us/launch  {by/t/1e9 if t else 0:6.0f} GB/s")
+
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    if len(sys.argv) > 2 and sys.argv[2] == "grid":
+        by_grid(sys.argv[1])
+    else:
+        main(sys.argv[1])

@@ -23,7 +23,7 @@ from paper_1406_7808_b200 import Solver  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--dtype", default="f64")
-ap.add_argument("--what", default="solve", choices=["solve", "cheb", "restrict", "prolong"])
+ap.add_argument("--what", default="solve", choices=["solve", "cheb", "restrict", "prolong", "correct"])
 ap.add_argument("--graph", type=int, default=1)
 a = ap.parse_args()
 n, M, seg, buf, K, rhs = WORKLOADS[a.config]
@@ -41,6 +41,8 @@ elif a.what == "cheb":
 elif a.what == "restrict":
     s.debug_op(1, M, 0, f)
 elif a.what == "prolong":
+    s.debug_op(3, M, 0, f)
+elif a.what == "correct":
     s.debug_op(4, M, 0, f)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
