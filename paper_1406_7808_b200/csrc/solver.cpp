@@ -71,6 +71,7 @@ struct sr_fmg {
   long long launches = 0;
   bool sync_debug = false;
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
+  bool force = false; // SR_FMG_FORCE_FUSED=1: use them even on levels too small to fill the GPU
   int prof_cls = -1, prof_level = -1;
   std::vector<ProfRec> prof;
   size_t prof_used = 0;
@@ -330,7 +331,7 @@ struct Schedule {
     const CellCounts& c = h->cells[l];
     // the fused pass marches z inside a CTA: use it only when segments x bands fill the
     // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
-    if (deg == 2 && h->fused && (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
+    if (deg == 2 && h->fused && (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
         srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
       const double rho0 = 1.0 / h->sigma[l];
@@ -348,7 +349,7 @@ struct Schedule {
       if (fin) final_done = true;
       return;
     }
-    if (deg == 1 && h->fused && (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
+    if (deg == 1 && h->fused && (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
         srfmg::cheb_spec_ok<T>(L)) {
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb1_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
@@ -391,8 +392,12 @@ struct Schedule {
     const CellCounts& c = h->cells[l];
     Launch g(h, st, KC_PROLONG, l,
              w * (add ? 2.0 : 1.0) * c.cg + w * (add ? 2.0 : 1.0) * h->cells[l - 1].cg / 8.0);
-    srfmg::launch_prolong<T>(h->L[l], U(l), h->L[l - 1], U(l - 1), (const T*)h->B[l - 1].t, add,
-                             st);
+    if (h->fused && (h->force || srfmg::prolong_tma_ok<T>(h->L[l], h->L[l - 1])))
+      srfmg::launch_prolong_tma<T>(h->L[l], U(l), h->L[l - 1], U(l - 1), (const T*)h->B[l - 1].t,
+                                   add, st);
+    else
+      srfmg::launch_prolong<T>(h->L[l], U(l), h->L[l - 1], U(l - 1), (const T*)h->B[l - 1].t, add,
+                               st);
   }
 
   // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors
@@ -566,6 +571,8 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->sync_debug = sd && sd[0] == '1';
   const char* fu = std::getenv("SR_FMG_FUSED");
   h->fused = !(fu && fu[0] == '0');
+  const char* ff = std::getenv("SR_FMG_FORCE_FUSED");
+  h->force = ff && ff[0] == '1';
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {

@@ -143,9 +143,18 @@ def _h(l):
     return (1.0 / N0[0]) * 2 ** (M0 - l)
 
 
-@pytest.fixture(scope="module")
-def ksolver():
+@pytest.fixture(scope="module", params=["default", "forced-fused"])
+def ksolver(request):
+    # "forced-fused": the TMA kernels run even on these small levels (SR_FMG_FORCE_FUSED)
+    import os
+    old = os.environ.get("SR_FMG_FORCE_FUSED")
+    if request.param == "forced-fused":
+        os.environ["SR_FMG_FORCE_FUSED"] = "1"
     s = Solver(N0, M0, seg=S0, buffer=J0, K=K0, use_graph=False)
+    if old is None:
+        os.environ.pop("SR_FMG_FORCE_FUSED", None)
+    else:
+        os.environ["SR_FMG_FORCE_FUSED"] = old
     yield s
     s.close()
 
@@ -325,13 +334,15 @@ def test_full_size_c3_matches_oracle():
     assert rel_l2(u, ref) <= TOL64, rel_l2(u, ref)
 
 
+@pytest.mark.parametrize("force", ["0", "1"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_fused_and_step_kernels_agree(dtype, monkeypatch):
+def test_fused_and_step_kernels_agree(dtype, force, monkeypatch):
     # the TMA-fed fused degree-2 pass vs two unfused Chebyshev steps (SR_FMG_FUSED=0):
     # same arithmetic per cell, so the solves agree to rounding
     n = (64, 64, 64)
     f = W.make_rhs("manufactured+noise", n).astype(np.float64 if dtype == "f64" else np.float32)
     ft = torch.from_numpy(f).cuda()
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", force)
     with Solver(n, 5, seg=16, buffer=2, K=3, dtype=dtype) as s:
         a = s.solve(ft).double().cpu().numpy()
     monkeypatch.setenv("SR_FMG_FUSED", "0")
