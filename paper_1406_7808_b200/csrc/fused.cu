@@ -343,10 +343,6 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
     if (in && y >= r0 && y < r1) w_mask |= 1u << k;
     yb_mask |= (unsigned)((gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0)) << (2 * k);
   }
-  constexpr unsigned kAll = (1u << MAXS) - 1u;
-  // fast paths: all slots are C cells with no reflected x/y neighbour
-  const bool fast1 = ld_mask == kAll && ex_mask == kAll && c_mask == kAll && yb_mask == 0u && dxo == 0;
-  const bool fast2 = fast1 && w_mask == kAll;
   const T* const u0b = u0s + (y0 - q0) * PY + tx;
   const T* const fb = fs + (y0 - s0) * G::FP + tx + fsh;
   T* const u1b = u1s + (y0 - s0) * PY + tx;
@@ -375,8 +371,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
       T* u1w = u1b + R * G::U1S;
       const int gz = oz + z;
       const bool zc = gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2;
-      const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
-      const T dg = six + dz;
+      const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
       if (z + 1 < Ez) {
 #pragma unroll
         for (int k = 0; k < MAXS; ++k)
@@ -385,26 +380,6 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) u0q[k][IP] = T(0);
       }
-      if (zc && fast1) {
-        // common case: every slot is a C cell away from the domain boundary -- no per-slot
-        // tests (diag = 6 + dz, uniform)
-        const T d = T(6) + dz;
-#pragma unroll
-        for (int k = 0; k < MAXS; ++k) {
-          const T v0 = u0q[k][I0];
-          const T ym = (k == 0) ? pl[-PY] : u0q[k > 0 ? k - 1 : 0][I0];
-          const T yp = (k == MAXS - 1) ? pl[MAXS * PY] : u0q[k + 1 < MAXS ? k + 1 : k][I0];
-          const T sum = ((u0q[k][IM] + u0q[k][IP]) + (ym + yp)) + (pl[k * PY - 1] + pl[k * PY + 1]);
-          const T r = fp[k * G::FP] - (d * v0 - sum) * ih2;
-          const T v1 = v0 + c0 * r;
-          if constexpr (NST == 2) {
-            u1q[k][I0] = v1;
-            u1w[k * PY] = v1;
-          } else {
-            if (((w_mask >> k) & 1u) && gz >= 0 && gz < L.N[2]) ob[(long long)z * pz + k * PY] = v1;
-          }
-        }
-      } else {
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
         const T v0 = u0q[k][I0];
@@ -426,7 +401,6 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
             ob[(long long)z * pz + k * PY] = v1;
         }
       }
-      }
     }
     __syncthreads();  // the only barrier of the plane step
     if (threadIdx.x == 0) {
@@ -438,25 +412,11 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
       const int gz = oz + zz;
       if (gz >= 0 && gz < L.N[2]) {
         const bool zc = zz >= 1 && zz <= Ez - 2;
-        const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
-        const T dg = six + dz;
+        const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
         constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
         const T* u1r = u1b + J1 * G::U1S;
         const T* fp = fb + (zz & 3) * G::FS;
         T* orow = ob + (long long)zz * pz;
-        if (zc && fast2 && a.ufinal == nullptr) {
-          const T d = T(6) + dz;
-#pragma unroll
-          for (int k = 0; k < MAXS; ++k) {
-            const T u0v = u0q[k][J1];
-            const T c1 = u1q[k][J1];
-            const T ym = (k == 0) ? u1r[-PY] : u1q[k > 0 ? k - 1 : 0][J1];
-            const T yp = (k == MAXS - 1) ? u1r[MAXS * PY] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
-            const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
-            const T r = fp[k * G::FP] - (d * c1 - sum) * ih2;
-            orow[k * PY] = c1 + cm * (c1 - u0v) + cr * r;
-          }
-        } else
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) {
           if (!((w_mask >> k) & 1u)) continue;
