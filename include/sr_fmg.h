@@ -81,6 +81,7 @@ typedef struct {
   int32_t device;     /* CUDA device ordinal; -1 = current device                        */
   void *stream;       /* cudaStream_t; NULL = legacy default stream                      */
   int32_t use_graph;  /* 1 (default): capture a solve into a CUDA graph and replay it    */
+  int32_t comm;       /* world > 1: 0 = NCCL (default), 1 = test replay store (see below) */
 } sr_fmg_desc_t;
 
 typedef struct {
@@ -98,7 +99,27 @@ typedef struct {
   int64_t workspace_bytes;
   int64_t launches_per_solve;              /* kernel launches in one solve               */
   double alg_bytes_per_solve;              /* B_alg of DESIGN.md §6 (fused-design bytes) */
+  int32_t world, rank;                     /* multi-GPU: this rank's block (see partition) */
+  int64_t block_lo[3], block_n[3];         /* fine cells owned (output block of u)        */
+  int32_t f_halo;                          /* halo width of the local f block             */
+  int64_t f_dims[3];                       /* local f array dims = block_n + 2 f_halo     */
+  int64_t exchanges_per_solve;             /* collective (all-gather) calls per solve     */
 } sr_fmg_info_t;
+
+/* Multi-GPU partition of a descriptor (pure host arithmetic, no GPU needed).  The
+ * segment grid (n_d/seg per dimension) is split into pgrid blocks; rank r has block
+ * coordinates (r % P1, (r / P1) % P2, r / (P1 P2)).  Each rank solves the SR levels of its
+ * own segments with no communication; the transition level and below are
+ * solved redundantly on every rank (the paper's "redundant coarse grid")
+ * after one all-gather of the level-T blocks per SR V-cycle. */
+typedef struct {
+  int32_t world, rank, coord[3];
+  int32_t segs_per_rank[3];          /* SR segments per dimension owned by this rank     */
+  int64_t block_lo[3], block_n[3];   /* fine genuine cells owned: [lo, lo + n)           */
+  int32_t f_halo;                    /* f must be given on [lo - halo, lo + n + halo)     */
+  int64_t f_dims[3];                 /* = block_n + 2 f_halo (x1 fastest)                 */
+  int64_t level_T_lo[3], level_T_n[3]; /* this rank's block of the transition level T     */
+} sr_fmg_partition_t;
 
 /* Fill *d with defaults: cube 0, M 0, seg 0, buffer 2, K 0, sched (-1,-1), fp64,
  * h 0, F(1,2,2), interval [1/6, 1], world 1, device -1, stream NULL, use_graph 1. */
@@ -110,7 +131,10 @@ sr_status_t sr_fmg_create(int64_t N, int32_t M, int32_t seg, int32_t buffer,
 sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t *d, sr_fmg_t **out);
 
 /* One FMG+SR solve.  f: device pointer to the fine right-hand side; u: device pointer to
- * the output (every cell written).  Asynchronous on the handle's stream. */
+ * the output (every cell written).  Asynchronous on the handle's stream.
+ * world > 1: f is this rank's block WITH a halo of f_halo cells on every side
+ * (sr_fmg_partition; halo cells outside the domain are ignored), u is the rank's block
+ * without halo.  Collective: every rank must call it (NCCL all-gathers inside). */
 sr_status_t sr_fmg_solve(sr_fmg_t *h, const void *f, void *u);
 
 /* The same solve from HOST buffers: copies f to the device, solves, copies u back,
@@ -121,6 +145,12 @@ sr_status_t sr_fmg_solve_host(sr_fmg_t *h, const void *f_host, void *u_host);
 sr_status_t sr_fmg_set_stream(sr_fmg_t *h, void *stream);
 
 void sr_fmg_destroy(sr_fmg_t *h); /* NULL-safe; synchronises the handle's stream */
+
+/* Partition arithmetic of a (validated) descriptor; no GPU needed. */
+sr_status_t sr_fmg_partition(const sr_fmg_desc_t *d, sr_fmg_partition_t *out);
+
+/* 128-byte ncclUniqueId for sr_fmg_desc_t.nccl_id (call on rank 0, broadcast). */
+sr_status_t sr_fmg_nccl_unique_id(void *out128);
 
 sr_status_t sr_fmg_get_info(const sr_fmg_t *h, sr_fmg_info_t *info);
 
@@ -146,6 +176,15 @@ sr_status_t sr_fmg_debug_level_io(sr_fmg_t *h, int32_t level, int32_t field, int
                                   void *host);
 sr_status_t sr_fmg_debug_op(sr_fmg_t *h, int32_t op, int32_t level, int32_t deg,
                             const void *f_dev);
+
+/* Test-only comm backend (desc.comm = 1): instead of NCCL, every all-gather records this
+ * rank's block into a host-side store shared by the handles of all ranks in one process
+ * and fills the other ranks' blocks from it.  Running every rank's solve repeatedly
+ * (exchanges_per_solve + 1 rounds) reproduces the distributed solve on ONE GPU, so the
+ * rank-local logic is validated without NCCL.  Forces eager (non-graph) execution. */
+void *sr_fmg_replay_store_create(int32_t world);
+void sr_fmg_replay_store_destroy(void *store);
+sr_status_t sr_fmg_set_replay(sr_fmg_t *h, void *store);
 
 /* Profiling hooks used by bench.py: select one kernel class (index into
  * sr_fmg_kernel_name) at one level; later solves record a CUDA event pair around every

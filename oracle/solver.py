@@ -86,6 +86,10 @@ class Oracle:
         self.ts = {l: {} for l in range(self.T + 1, M + 1)}
         self.f = None
         self.counters = {"vconv_visits": [0] * (M + 1), "vsr_visits": [0] * (M + 1)}
+        # decomposition hook (tests of the multi-rank path): a rank processes only its own
+        # `segs`; at the k = 1 hand-off exchange_T(u_T, R_T) fills the other ranks' V_T^p
+        # blocks (the levels <= T are then solved redundantly on every rank)
+        self.exchange_T = None
 
     # ------------------------------------------------------------------------------
     # SR regions (readings R13-R15)
@@ -187,6 +191,8 @@ class Oracle:
                 else:
                     uT[VT] = 0.0
                 RT[VT] = restrict_avg8(r[p], VT)                      # L235 I(r)
+            if self.exchange_T is not None:
+                self.exchange_T(uT, RT)
             t = uT.copy()                                             # L234
             fill_bc_ghosts(uT, domT)
             bT = Field(domT, array=RT[domT] + apply_A(uT, domT, hT))  # L235 (+ L u)

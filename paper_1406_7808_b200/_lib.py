@@ -23,6 +23,8 @@ EXPORTED = [
     "sr_fmg_solve_host", "sr_fmg_set_stream", "sr_fmg_destroy", "sr_fmg_get_info",
     "sr_fmg_last_error", "sr_fmg_kernel_count", "sr_fmg_kernel_name",
     "sr_fmg_debug_level_io", "sr_fmg_debug_op", "sr_fmg_profile_select", "sr_fmg_profile_read",
+    "sr_fmg_partition", "sr_fmg_nccl_unique_id", "sr_fmg_replay_store_create",
+    "sr_fmg_replay_store_destroy", "sr_fmg_set_replay",
 ]
 
 
@@ -35,7 +37,7 @@ class Desc(ctypes.Structure):
         ("nu2", ctypes.c_int32), ("cheb_lo", ctypes.c_double), ("cheb_hi", ctypes.c_double),
         ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("pgrid", ctypes.c_int32 * 3),
         ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
-        ("use_graph", ctypes.c_int32),
+        ("use_graph", ctypes.c_int32), ("comm", ctypes.c_int32),
     ]
 
 
@@ -55,6 +57,20 @@ class Info(ctypes.Structure):
         ("workspace_bytes", ctypes.c_int64),
         ("launches_per_solve", ctypes.c_int64),
         ("alg_bytes_per_solve", ctypes.c_double),
+        ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+        ("block_lo", ctypes.c_int64 * 3), ("block_n", ctypes.c_int64 * 3),
+        ("f_halo", ctypes.c_int32), ("f_dims", ctypes.c_int64 * 3),
+        ("exchanges_per_solve", ctypes.c_int64),
+    ]
+
+
+class Partition(ctypes.Structure):
+    _fields_ = [
+        ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("coord", ctypes.c_int32 * 3),
+        ("segs_per_rank", ctypes.c_int32 * 3),
+        ("block_lo", ctypes.c_int64 * 3), ("block_n", ctypes.c_int64 * 3),
+        ("f_halo", ctypes.c_int32), ("f_dims", ctypes.c_int64 * 3),
+        ("level_T_lo", ctypes.c_int64 * 3), ("level_T_n", ctypes.c_int64 * 3),
     ]
 
 
@@ -82,6 +98,11 @@ def _load():
         "sr_fmg_profile_select": (I32, [P, I32, I32]),
         "sr_fmg_profile_read": (I32, [P, ctypes.POINTER(D), ctypes.POINTER(D),
                                       ctypes.POINTER(I32)]),
+        "sr_fmg_partition": (I32, [ctypes.POINTER(Desc), ctypes.POINTER(Partition)]),
+        "sr_fmg_nccl_unique_id": (I32, [P]),
+        "sr_fmg_replay_store_create": (P, [I32]),
+        "sr_fmg_replay_store_destroy": (None, [P]),
+        "sr_fmg_set_replay": (I32, [P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -13,7 +13,7 @@ from typing import Optional, Tuple
 import numpy as np
 
 from . import _lib
-from ._lib import Desc, Info, check, lib
+from ._lib import Desc, Info, Partition, check, lib
 
 
 @dataclass
@@ -29,6 +29,58 @@ class LevelInfo:
     visits: int
 
 
+def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha=1, nu1=2,
+              nu2=2, cheb=(1.0 / 6.0, 1.0), device=None, use_graph=True, world=1, rank=0,
+              pgrid=(1, 1, 1)) -> Desc:
+    if isinstance(n, int):
+        n = (n, n, n)
+    d = Desc()
+    lib.sr_fmg_desc_init(ctypes.byref(d))
+    for i in range(3):
+        d.n[i] = int(n[i])
+        d.pgrid[i] = int(pgrid[i])
+    d.M, d.seg, d.buffer, d.sr_levels = int(M), int(seg), int(buffer), int(K)
+    if sched is not None:
+        d.sched_A, d.sched_B = int(sched[0]), int(sched[1])
+    d.dtype = {"f64": _lib.SR_F64, "f32": _lib.SR_F32}[dtype]
+    d.h = 0.0 if h is None else float(h)
+    d.alpha, d.nu1, d.nu2 = int(alpha), int(nu1), int(nu2)
+    d.cheb_lo, d.cheb_hi = float(cheb[0]), float(cheb[1])
+    d.device = -1 if device is None else int(device)
+    d.use_graph = 1 if use_graph else 0
+    d.world, d.rank = int(world), int(rank)
+    return d
+
+
+def partition(n, M, seg, buffer, K, world, rank, pgrid, sched=None) -> dict:
+    """This rank's block of a multi-GPU descriptor (host arithmetic, no GPU)."""
+    d = make_desc(n, M, seg, buffer, K, sched=sched, world=world, rank=rank, pgrid=pgrid)
+    p = Partition()
+    check(lib.sr_fmg_partition(ctypes.byref(d), ctypes.byref(p)))
+    return dict(world=p.world, rank=p.rank, coord=tuple(p.coord),
+                segs_per_rank=tuple(p.segs_per_rank), block_lo=tuple(p.block_lo),
+                block_n=tuple(p.block_n), f_halo=p.f_halo, f_dims=tuple(p.f_dims),
+                level_T_lo=tuple(p.level_T_lo), level_T_n=tuple(p.level_T_n))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib.sr_fmg_nccl_unique_id(buf))
+    return buf.raw
+
+
+class ReplayStore:
+    """Test-only in-process stand-in for the all-gathers of a multi-rank solve."""
+
+    def __init__(self, world):
+        self.ptr = ctypes.c_void_p(lib.sr_fmg_replay_store_create(int(world)))
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and self.ptr.value:
+            lib.sr_fmg_replay_store_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+
 class Solver:
     """One FMG+SR solver instance (a handle of the C ABI).
 
@@ -38,29 +90,36 @@ class Solver:
     """
 
     def __init__(self, n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None,
-                 alpha=1, nu1=2, nu2=2, cheb=(1.0 / 6.0, 1.0), device=None, use_graph=True):
+                 alpha=1, nu1=2, nu2=2, cheb=(1.0 / 6.0, 1.0), device=None, use_graph=True,
+                 world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, replay_store=None):
         if isinstance(n, int):
             n = (n, n, n)
-        d = Desc()
-        lib.sr_fmg_desc_init(ctypes.byref(d))
-        for i in range(3):
-            d.n[i] = int(n[i])
-        d.M, d.seg, d.buffer, d.sr_levels = int(M), int(seg), int(buffer), int(K)
-        if sched is not None:
-            d.sched_A, d.sched_B = int(sched[0]), int(sched[1])
-        d.dtype = {"f64": _lib.SR_F64, "f32": _lib.SR_F32}[dtype]
-        d.h = 0.0 if h is None else float(h)
-        d.alpha, d.nu1, d.nu2 = int(alpha), int(nu1), int(nu2)
-        d.cheb_lo, d.cheb_hi = float(cheb[0]), float(cheb[1])
-        d.device = -1 if device is None else int(device)
-        d.use_graph = 1 if use_graph else 0
+        d = make_desc(n, M, seg, buffer, K, dtype, h, sched, alpha, nu1, nu2, cheb, device,
+                      use_graph, world, rank, pgrid)
+        if world > 1 and replay_store is None:
+            if nccl_id is None:
+                raise ValueError("world > 1 needs nccl_id (see nccl_unique_id) or replay_store")
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            d.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
+        if replay_store is not None:
+            d.comm = 1
         self._h = ctypes.c_void_p()
         check(lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(self._h)))
+        if replay_store is not None:
+            check(lib.sr_fmg_set_replay(self._h, replay_store.ptr), self._h)
+            self._store = replay_store
         self.n = tuple(int(v) for v in n)
-        self.shape = (self.n[2], self.n[1], self.n[0])
         self.dtype = dtype
         self.np_dtype = np.float64 if dtype == "f64" else np.float32
         self._info = self._get_info()
+        i = self._info
+        self.world = i.world
+        self.block_lo = tuple(i.block_lo)
+        self.block_n = tuple(i.block_n)
+        self.f_halo = i.f_halo
+        # array shapes (x1 fastest): output block and (haloed) input block
+        self.shape = (i.block_n[2], i.block_n[1], i.block_n[0])
+        self.f_shape = (i.f_dims[2], i.f_dims[1], i.f_dims[0])
 
     # -- lifetime ------------------------------------------------------------------------
     def close(self):
@@ -117,23 +176,44 @@ class Solver:
     def workspace_bytes(self) -> int:
         return self._info.workspace_bytes
 
+    @property
+    def exchanges_per_solve(self) -> int:
+        return self._info.exchanges_per_solve
+
+    def local_f(self, f_global):
+        """This rank's haloed block of a global f (numpy, shape (n3, n2, n1)); cells of the
+        halo outside the domain are zero."""
+        H = self.f_halo
+        lo = self.block_lo
+        out = np.zeros(self.f_shape, dtype=f_global.dtype)
+        n = self.n
+        src = [(max(lo[d] - H, 0), min(lo[d] + self.block_n[d] + H, n[d])) for d in range(3)]
+        dst = [(a - (lo[d] - H), b - (lo[d] - H)) for d, (a, b) in enumerate(src)]
+        out[dst[2][0]:dst[2][1], dst[1][0]:dst[1][1], dst[0][0]:dst[0][1]] = \
+            f_global[src[2][0]:src[2][1], src[1][0]:src[1][1], src[0][0]:src[0][1]]
+        return out
+
+    def block_of(self, u_global):
+        lo, nb = self.block_lo, self.block_n
+        return u_global[lo[2]:lo[2] + nb[2], lo[1]:lo[1] + nb[1], lo[0]:lo[0] + nb[0]]
+
     # -- solves --------------------------------------------------------------------------
-    def _check_tensor(self, t, name):
+    def _check_tensor(self, t, name, shape):
         import torch
         if not isinstance(t, torch.Tensor) or not t.is_cuda:
             raise TypeError(f"{name} must be a CUDA torch.Tensor")
         want = torch.float64 if self.dtype == "f64" else torch.float32
-        if t.dtype != want or tuple(t.shape) != self.shape or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous {want} tensor of shape {self.shape}")
+        if t.dtype != want or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {want} tensor of shape {shape}")
 
     def solve(self, f, out=None):
         """u = FMG+SR solve of A u = f.  f, out: CUDA tensors of shape (n3, n2, n1).
         Ordered on torch's current stream; returns `out`."""
         import torch
-        self._check_tensor(f, "f")
+        self._check_tensor(f, "f", self.f_shape)
         if out is None:
-            out = torch.empty_like(f)
-        self._check_tensor(out, "out")
+            out = torch.empty(self.shape, dtype=f.dtype, device=f.device)
+        self._check_tensor(out, "out", self.shape)
         check(lib.sr_fmg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
               self._h)
         check(lib.sr_fmg_solve(self._h, ctypes.c_void_p(f.data_ptr()),
@@ -148,9 +228,9 @@ class Solver:
             f = torch.from_numpy(np.ascontiguousarray(f, dtype=self.np_dtype))
         if out is None:
             out = torch.empty(self.shape, dtype=f.dtype, pin_memory=f.is_pinned())
-        for t, nm in ((f, "f"), (out, "out")):
-            if t.is_cuda or tuple(t.shape) != self.shape or not t.is_contiguous():
-                raise ValueError(f"{nm} must be a contiguous host tensor of shape {self.shape}")
+        for t, nm, shp in ((f, "f", self.f_shape), (out, "out", self.shape)):
+            if t.is_cuda or tuple(t.shape) != tuple(shp) or not t.is_contiguous():
+                raise ValueError(f"{nm} must be a contiguous host tensor of shape {shp}")
         check(lib.sr_fmg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
               self._h)
         check(lib.sr_fmg_solve_host(self._h, ctypes.c_void_p(f.data_ptr()),

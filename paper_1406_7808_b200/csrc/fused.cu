@@ -47,7 +47,8 @@ struct Cheb2Args {
   int f_stride;      // elements per rhs plane buffer
   int bw;            // rhs tensor-map box width (global rhs; 16-byte aligned start)
   T c0, cm, cr;
-  T* ufinal;         // non-null: write only genuine cells, to this dense user array (last pass)
+  FinalOut<T> fin;   // fin.p non-null: write only genuine cells, to the user's u block (last pass)
+  int foff[3];       // global index of the dense rhs array's first element (tensor coords)
 };
 
 long long round_up_ll(long long v, long long m) { return (v + m - 1) / m * m; }
@@ -69,9 +70,9 @@ __global__ void __launch_bounds__(NTMAX, 1)
   T* u1s = fs + kRing * a.f_stride;
   uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + 2 * a.s_stride);
 
-  const int px = s % L.ns[0];
-  const int pyy = (s / L.ns[0]) % L.ns[1];
-  const int pzz = s / (L.ns[0] * L.ns[1]);
+  const int px = s % L.ns[0] + L.so[0];
+  const int pyy = (s / L.ns[0]) % L.ns[1] + L.so[1];
+  const int pzz = s / (L.ns[0] * L.ns[1]) + L.so[2];
   const int ox = px * L.S[0] - (L.J + 1);
   const int oy = pyy * L.S[1] - (L.J + 1);
   const int oz = pzz * L.S[2] - (L.J + 1);
@@ -82,9 +83,10 @@ __global__ void __launch_bounds__(NTMAX, 1)
   // TMA tensor loads need a 16-byte aligned start in x: load from the aligned-down
   // column and shift the smem index by fsh; the rhs buffer row pitch is then bw
   constexpr int kAl = 16 / (int)sizeof(T);
-  const int oxa = ox & ~(kAl - 1);
+  const int oxt = ox - a.foff[0];              // x in tensor coordinates
+  const int oxa = oxt & ~(kAl - 1);            // 16-byte aligned box start
   const int fpitch = a.rhs_global ? a.bw : py;
-  const int fsh = a.rhs_global ? ox - oxa : 0;
+  const int fsh = a.rhs_global ? oxt - oxa : 0;
   const uint32_t f_bytes = a.rhs_global ? (uint32_t)((a.BH + 2) * a.bw * sizeof(T))
                                         : (uint32_t)((s1 - s0) * py * sizeof(T));
 
@@ -106,7 +108,8 @@ __global__ void __launch_bounds__(NTMAX, 1)
     const int sl_ = (z) % kRing;                                                             \
     mbar_expect_tx(&bars[kRing + sl_], f_bytes);                                             \
     if (a.rhs_global)                                                                        \
-      tma_3d(fs + sl_ * a.f_stride, &fmap, oxa, oy + s0, oz + (z), &bars[kRing + sl_]);      \
+      tma_3d(fs + sl_ * a.f_stride, &fmap, oxa, oy + s0 - a.foff[1], oz + (z) - a.foff[2],  \
+             &bars[kRing + sl_]);                                                            \
     else                                                                                     \
       bulk_g2s(fs + sl_ * a.f_stride, rseg + (long long)(z) * pz + (long long)s0 * py,       \
                f_bytes, &bars[kRing + sl_]);                                                 \
@@ -283,9 +286,9 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
   T* u1s = fs + G::RF * G::FS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + 3 * G::U1S);  // [0,3) u0, [3,7) f
 
-  const int px = s % L.ns[0];
-  const int pyy = (s / L.ns[0]) % L.ns[1];
-  const int pzz = s / (L.ns[0] * L.ns[1]);
+  const int px = s % L.ns[0] + L.so[0];
+  const int pyy = (s / L.ns[0]) % L.ns[1] + L.so[1];
+  const int pzz = s / (L.ns[0] * L.ns[1]) + L.so[2];
   const int ox = px * L.S[0] - (L.J + 1);
   const int oy = pyy * L.S[1] - (L.J + 1);
   const int oz = pzz * L.S[2] - (L.J + 1);
@@ -293,8 +296,9 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
   T* oseg = a.uout + (long long)s * L.ss;
   const T* rseg = RG ? nullptr : a.rhs_seg + (long long)s * L.ss;
   const uint32_t u0_bytes = (uint32_t)((q1 - q0) * PY * sizeof(T));
-  const int oxa = ox & ~(G::kAl - 1);
-  const int fsh = RG ? ox - oxa : 0;
+  const int oxt = ox - a.foff[0];              // x in tensor coordinates
+  const int oxa = oxt & ~(G::kAl - 1);         // 16-byte aligned box start
+  const int fsh = RG ? oxt - oxa : 0;
   const uint32_t f_bytes = RG ? (uint32_t)((BH + 2) * G::FP * sizeof(T))
                               : (uint32_t)((s1 - s0) * PY * sizeof(T));
   if (threadIdx.x == 0) {
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
     const int sl = z & 3;
     mbar_expect_tx(&bars[3 + sl], f_bytes);
     if (RG)
-      tma_3d(fs + sl * G::FS, &fmap, oxa, oy + s0, oz + z, &bars[3 + sl]);
+      tma_3d(fs + sl * G::FS, &fmap, oxa, oy + s0 - a.foff[1], oz + z - a.foff[2], &bars[3 + sl]);
     else
       bulk_g2s(fs + sl * G::FS, rseg + (long long)z * pz + (long long)s0 * PY, f_bytes,
                &bars[3 + sl]);
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
             const T r = fp[k * G::FP] - (d * c1 - sum) * ih2;
             v2 = c1 + cm * (c1 - u0v) + cr * r;
           }
-          if (a.ufinal == nullptr) {
+          if (a.fin.p == nullptr) {
             orow[k * PY] = v2;
           } else {
             // last pass of the solve (R19): genuine cells straight to the user's u
@@ -439,7 +443,8 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
             const int vlo = L.J + 1;
             if (tx >= vlo && tx < vlo + L.S[0] && y >= vlo && y < vlo + L.S[1] &&
                 zz >= vlo && zz < vlo + L.S[2])
-              a.ufinal[((long long)gz * L.N[1] + (oy + y)) * L.N[0] + gxv] = v2;
+              a.fin.p[(long long)(gz - a.fin.bo[2]) * a.fin.sz +
+                      (long long)(oy + y - a.fin.bo[1]) * a.fin.sy + (gxv - a.fin.bo[0])] = v2;
           }
         }
       }
@@ -547,10 +552,12 @@ bool spec_enabled() {
 }
 
 template <class T>
-bool encode_rhs_map(CUtensorMap* map, const Lvl& L, const T* p, int bw, int rows) {
-  const cuuint64_t dims[3] = {(cuuint64_t)L.N[0], (cuuint64_t)L.N[1], (cuuint64_t)L.N[2]};
-  const cuuint64_t strides[2] = {(cuuint64_t)L.N[0] * sizeof(T),
-                                 (cuuint64_t)L.N[0] * L.N[1] * sizeof(T)};
+bool encode_rhs_map(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows) {
+  const T* p = rb.base;
+  const cuuint64_t dims[3] = {(cuuint64_t)rb.dims[0], (cuuint64_t)rb.dims[1],
+                              (cuuint64_t)rb.dims[2]};
+  const cuuint64_t strides[2] = {(cuuint64_t)rb.dims[0] * sizeof(T),
+                                 (cuuint64_t)rb.dims[0] * rb.dims[1] * sizeof(T)};
   const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)rows, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = get_encode()(
@@ -576,7 +583,7 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
   };
   if (b.global) {
     using G = SpecGeom<T, PY, BH, MAXS, 1>;
-    if (!encode_rhs_map<T>(&map, L, b.p, G::FP, BH + 2)) return false;
+    if (!encode_rhs_map<T>(&map, b, G::FP, BH + 2)) return false;
     if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 1, 2>, G::SMEM, G::NT);
     else go(k_cheb2s<T, PY, BH, MAXS, 1, 1>, G::SMEM, G::NT);
   } else {
@@ -609,10 +616,11 @@ template bool cheb2_final_ok<float>(const Lvl&);
 
 template <class T>
 void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
-                        double cr, cudaStream_t st, T* ufinal) {
+                        double cr, cudaStream_t st, FinalOut<T> fin) {
   {
     Cheb2Args<T> a{};
-    a.ufinal = ufinal;
+    a.fin = fin;
+    for (int d = 0; d < 3; ++d) a.foff[d] = b.global ? b.off[d] : 0;
     a.L = L;
     a.uin = u_in;
     a.uout = u_out;
@@ -627,29 +635,14 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
   const Plan pl = make_plan<T>(L, v.maxs, v.nt);
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
-  if (b.global) {
-    const cuuint64_t dims[3] = {(cuuint64_t)L.N[0], (cuuint64_t)L.N[1], (cuuint64_t)L.N[2]};
-    const cuuint64_t strides[2] = {(cuuint64_t)L.N[0] * sizeof(T),
-                                   (cuuint64_t)L.N[0] * L.N[1] * sizeof(T)};
-    const cuuint32_t box[3] = {(cuuint32_t)pl.bw, (cuuint32_t)(pl.BH + 2), 1};
-    const cuuint32_t es[3] = {1, 1, 1};
-    const CUresult r = get_encode()(
-        &map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-        const_cast<T*>(b.p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      fprintf(stderr, "sr_fmg: cuTensorMapEncodeTiled failed (%d) dims %llu %llu %llu box %u %u\n",
-              (int)r, (unsigned long long)dims[0], (unsigned long long)dims[1],
-              (unsigned long long)dims[2], box[0], box[1]);
-    }
-  }
+  if (b.global) encode_rhs_map<T>(&map, b, pl.bw, pl.BH + 2);
   Cheb2Args<T> a{};
   a.L = L;
   a.uin = u_in;
   a.uout = u_out;
   a.rhs_seg = b.global ? nullptr : b.p;
   a.rhs_global = b.global;
+  for (int d = 0; d < 3; ++d) a.foff[d] = b.global ? b.off[d] : 0;
   a.BH = pl.BH;
   a.u0_stride = pl.u0_stride;
   a.s_stride = pl.s_stride;
@@ -690,6 +683,7 @@ bool launch_cheb1_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
   a.uout = u_out;
   a.rhs_seg = b.global ? nullptr : b.p;
   a.rhs_global = b.global;
+  for (int d = 0; d < 3; ++d) a.foff[d] = b.global ? b.off[d] : 0;
   a.c0 = (T)c0;
   return launch_spec<T>(L, a, b, 1, st);
 }
@@ -699,9 +693,9 @@ template bool launch_cheb1_fused<double>(const Lvl&, const double*, double*, Fus
 template bool launch_cheb1_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>, double,
                                         cudaStream_t);
 template void launch_cheb2_fused<double>(const Lvl&, const double*, double*, FusedRhs<double>,
-                                         double, double, double, cudaStream_t, double*);
+                                         double, double, double, cudaStream_t, FinalOut<double>);
 template void launch_cheb2_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>, double,
-                                        double, double, cudaStream_t, float*);
+                                        double, double, cudaStream_t, FinalOut<float>);
 template bool cheb2_fused_ok<double>(const Lvl&);
 template bool cheb2_fused_ok<float>(const Lvl&);
 

@@ -8,8 +8,19 @@ namespace srfmg {
 // (tensor map built per launch from `p`) or a level's segment storage (1-D bulk copies).
 template <class T>
 struct FusedRhs {
-  const T* p;
-  int global;  // 1: dense Omega_l array (x fastest), 0: segment storage of the level
+  const T* p;     // segment storage (global == 0) or unused
+  int global;     // 1: dense array (x fastest), 0: segment storage of the level
+  const T* base;  // dense array: first element of the (possibly haloed, local) array
+  int dims[3];    // dense array dims
+  int off[3];     // global index of base[0] (tensor coordinate = global - off)
+};
+
+// Dense output of the last pass: the rank's block of u, global origin bo, strides sy, sz.
+template <class T>
+struct FinalOut {
+  T* p;
+  int bo[3];
+  long long sy, sz;
 };
 
 // One degree-2 Chebyshev application (two sweeps, R8) on C of every segment of level L,
@@ -19,7 +30,7 @@ struct FusedRhs {
 // user's dense u (R19), and not the segment storage (only for cheb2_final_ok levels).
 template <class T>
 void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0, double cm,
-                        double cr, cudaStream_t st, T* ufinal = nullptr);
+                        double cr, cudaStream_t st, FinalOut<T> fin = FinalOut<T>{});
 template <class T>
 bool cheb2_final_ok(const Lvl& L);
 

@@ -18,11 +18,12 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// GLOBAL segment coordinates of local segment s (this rank's block starts at L.so)
 __device__ __forceinline__ void seg_coords(const Lvl& L, int s, int p[3]) {
-  p[0] = s % L.ns[0];
+  p[0] = s % L.ns[0] + L.so[0];
   const int t = s / L.ns[0];
-  p[1] = t % L.ns[1];
-  p[2] = t / L.ns[1];
+  p[1] = t % L.ns[1] + L.so[1];
+  p[2] = t / L.ns[1] + L.so[2];
 }
 
 // storage origin (global index of local cell 0) of a segment: p*S - (J+1)
@@ -502,7 +503,9 @@ __global__ void __launch_bounds__(kThreads) k_pyramid(const T* __restrict__ ff, 
 // genuine (x, y) column of a segment, marching z.
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_gather(Lvl L, const T* __restrict__ useg,
-                                                     T* __restrict__ out, int ntx, int zchunk) {
+                                                     T* __restrict__ out, int bo0, int bo1, int bo2,
+                                                     long long osy, long long osz, int ntx,
+                                                     int zchunk) {
   Col c;
   if (!col_index(L.S[0], L.S[1], L.S[2], ntx, zchunk, c)) return;
   const int s = blockIdx.y;
@@ -510,12 +513,28 @@ __global__ void __launch_bounds__(kThreads) k_gather(Lvl L, const T* __restrict_
   seg_coords(L, s, p);
   const int h = L.J + 1;
   const T* src = useg + (long long)s * L.ss + (long long)(c.ay + h) * L.py + (c.ax + h);
-  T* dst = out + ((long long)(p[1] * L.S[1] + c.ay)) * L.N[0] + (p[0] * L.S[0] + c.ax);
-  const long long plane = (long long)L.N[0] * L.N[1];
+  T* dst = out + (long long)(p[1] * L.S[1] + c.ay - bo1) * osy + (p[0] * L.S[0] + c.ax - bo0);
   for (int z = c.z0; z < c.z1; ++z)
-    dst[(long long)(p[2] * L.S[2] + z) * plane] = src[(long long)(z + h) * L.pz];
+    dst[(long long)(p[2] * L.S[2] + z - bo2) * osz] = src[(long long)(z + h) * L.pz];
 }
 
+// box copy between a strided array and a contiguous buffer (multi-GPU packing)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_box_copy(T* __restrict__ base, long long sy,
+                                                       long long sz, int lx, int ly, int lz,
+                                                       int nx, int ny, int nz,
+                                                       T* __restrict__ buf, int to_buf) {
+  const long long n = (long long)nx * ny * nz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = i % nx;
+    const int y = (i / nx) % ny;
+    const int z = i / ((long long)nx * ny);
+    const long long o = (long long)(lz + z) * sz + (long long)(ly + y) * sy + (lx + x);
+    if (to_buf) buf[i] = base[o];
+    else base[o] = buf[i];
+  }
+}
 
 }  // namespace
 
@@ -588,9 +607,21 @@ void launch_pyramid(const T* ff, int nfx, int nfy, int nfz, T* fc, cudaStream_t 
 }
 
 template <class T>
-void launch_gather(const Lvl& L, const T* useg, T* out, cudaStream_t st) {
+void launch_gather(const Lvl& L, const T* useg, T* out, const int bo[3], long long sy,
+                   long long sz, cudaStream_t st) {
   const ColCfg c = col_cfg(L.S[0], L.S[1], L.S[2], L.nsegs);
-  k_gather<T><<<c.grid, c.block, 0, st>>>(L, useg, out, c.ntx, c.zchunk);
+  k_gather<T><<<c.grid, c.block, 0, st>>>(L, useg, out, bo[0], bo[1], bo[2], sy, sz, c.ntx,
+                                          c.zchunk);
+}
+
+template <class T>
+void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const int n[3], T* buf,
+                     int to_buf, cudaStream_t st) {
+  const long long cnt = (long long)n[0] * n[1] * n[2];
+  if (cnt <= 0) return;
+  const unsigned g = (unsigned)std::min<long long>(148LL * 8, (cnt + kThreads - 1) / kThreads);
+  k_box_copy<T><<<std::max(g, 1u), kThreads, 0, st>>>(base, sy, sz, lo[0], lo[1], lo[2], n[0],
+                                                      n[1], n[2], buf, to_buf);
 }
 
 #define SRFMG_INST(T)                                                                          \
@@ -603,7 +634,10 @@ void launch_gather(const Lvl& L, const T* useg, T* out, cudaStream_t st) {
                                   cudaStream_t);                                               \
   template void launch_coarsest<T>(const Lvl&, T*, View<T>, const T*, cudaStream_t);            \
   template void launch_pyramid<T>(const T*, int, int, int, T*, cudaStream_t);                   \
-  template void launch_gather<T>(const Lvl&, const T*, T*, cudaStream_t);
+  template void launch_gather<T>(const Lvl&, const T*, T*, const int*, long long, long long,      \
+                                 cudaStream_t);                                                  \
+  template void launch_box_copy<T>(T*, long long, long long, const int*, const int*, T*, int,    \
+                                   cudaStream_t);
 SRFMG_INST(double)
 SRFMG_INST(float)
 

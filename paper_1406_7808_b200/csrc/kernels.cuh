@@ -15,7 +15,8 @@ struct Lvl {
   int N[3];          // cells of Omega_l per dimension
   int S[3];          // genuine segment edge per dimension (N on conventional levels)
   int J;             // buffer width (0 on conventional levels)
-  int ns[3];         // segments per dimension
+  int ns[3];         // segments per dimension (of this rank's block)
+  int so[3];         // global segment coordinates of this rank's first segment (0 on 1 GPU)
   int E[3];          // storage extent per dimension: S + 2J + 2
   int py;            // row pitch in elements
   long long pz;      // plane pitch in elements
@@ -26,12 +27,18 @@ struct Lvl {
 
 // Read-only right-hand-side view: either a dense global array over Omega_l without ghosts
 // (user f or an f-pyramid level) or a level's segment storage (tau right-hand sides).
+// Dense arrays may be a rank's haloed local block: `p` then points at the (virtual)
+// global origin, so that p[g.z*sz + g.y*sy + g.x] is valid for the block's global cells.
 template <class T>
 struct View {
   const T* p;
   int global;        // 1: dense global array, index g.z*sz + g.y*sy + g.x
   long long sy, sz;  // strides (row, plane)
   long long ss;      // segment stride (segment storage only)
+  // dense arrays only (host side, for TMA tensor maps): the real array
+  const T* base;     // element 0
+  int dims[3];       // array dims
+  int off[3];        // global index of element 0
 };
 
 // Launchers (kernels.cu).  All asynchronous on `st`.
@@ -50,8 +57,15 @@ template <class T>
 void launch_coarsest(const Lvl& L0, T* u, View<T> b, const T* ainv, cudaStream_t st);
 template <class T>
 void launch_pyramid(const T* ff, int nfx, int nfy, int nfz, T* fc, cudaStream_t st);
+// out: this rank's dense output block; (bo, sy, sz): its global origin and strides
 template <class T>
-void launch_gather(const Lvl& L, const T* useg, T* out, cudaStream_t st);
+void launch_gather(const Lvl& L, const T* useg, T* out, const int bo[3], long long sy,
+                   long long sz, cudaStream_t st);
+// copy the box [lo, lo+n) of a strided array (element (x,y,z) at base[z*sz + y*sy + x]) to
+// (to_buf = 1) or from (0) a contiguous buffer -- packing for the multi-GPU all-gathers
+template <class T>
+void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const int n[3], T* buf,
+                     int to_buf, cudaStream_t st);
 
 extern const char* const kKernelNames[];
 extern const int kNumKernelNames;

@@ -42,13 +42,14 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
   const int Ey = Lf.E[1], Ez = Lf.E[2], Ex = Lf.E[0];
   const int r0 = blockIdx.x * a.BH, r1 = min(Ey, r0 + a.BH);
   // fine segment geometry
-  const int px = s % Lf.ns[0], py_ = (s / Lf.ns[0]) % Lf.ns[1], pz_ = s / (Lf.ns[0] * Lf.ns[1]);
+  const int px = s % Lf.ns[0] + Lf.so[0], py_ = (s / Lf.ns[0]) % Lf.ns[1] + Lf.so[1],
+            pz_ = s / (Lf.ns[0] * Lf.ns[1]) + Lf.so[2];
   const int ox = px * Lf.S[0] - (Lf.J + 1), oy = py_ * Lf.S[1] - (Lf.J + 1),
             oz = pz_ * Lf.S[2] - (Lf.J + 1);
   // coarse segment: the fine segment's own coarse storage, or the single global array
   const int cs = (Lc.nsegs == 1) ? 0 : s;
-  const int cpx = cs % Lc.ns[0], cpy = (cs / Lc.ns[0]) % Lc.ns[1],
-            cpz = cs / (Lc.ns[0] * Lc.ns[1]);
+  const int cpx = cs % Lc.ns[0] + Lc.so[0], cpy = (cs / Lc.ns[0]) % Lc.ns[1] + Lc.so[1],
+            cpz = cs / (Lc.ns[0] * Lc.ns[1]) + Lc.so[2];
   const int ocx = cpx * Lc.S[0] - (Lc.J + 1), ocy = cpy * Lc.S[1] - (Lc.J + 1),
             ocz = cpz * Lc.S[2] - (Lc.J + 1);
   // fine rows / planes inside Omega

@@ -3,11 +3,15 @@
 // CUDA-graph capture, and the C ABI of include/sr_fmg.h.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -31,7 +35,15 @@ struct LevelBufs {
   int cur = 0;                      // which one holds the current iterate
   void* rhs = nullptr;              // tau right-hand side (levels < M)
   void* t = nullptr;                // t snapshot (levels < M)
-  void* fpyr = nullptr;             // dense f_l (levels < M)
+  void* fpyr = nullptr;             // dense f_l over Omega_l (levels <= T, and < M on 1 GPU)
+  void* floc = nullptr;             // multi-GPU: this rank's haloed block of f_l, T <= l < M
+};
+
+// collectives of the multi-GPU path: all-gather of equal per-rank blocks
+struct Comm {
+  virtual ~Comm() {}
+  virtual sr_status_t allgather(sr_fmg* h, const void* send, void* recv, size_t bytes,
+                                cudaStream_t st) = 0;
 };
 
 struct ProfRec {
@@ -77,6 +89,19 @@ struct sr_fmg {
   size_t prof_used = 0;
   long long workspace = 0;
   std::vector<long long> visits;
+  // ---- partition (multi-GPU); world = 1: one block = the whole grid, halo 0
+  int world = 1, rank = 0, coord[3] = {0, 0, 0};
+  int nsr[3] = {0, 0, 0};                   // SR segments per rank per dimension
+  int blk_lo[3] = {0, 0, 0}, blk_n[3] = {0, 0, 0};  // fine genuine block
+  std::vector<int> H;                       // f halo per level (levels >= T)
+  std::vector<std::array<int, 3>> flo, fdim;  // local f array: global origin, dims (levels >= T)
+  int blkT_lo[3] = {0, 0, 0}, blkT_n[3] = {0, 0, 0};  // this rank's block of level T
+  Comm* comm = nullptr;
+  void* xsend = nullptr;                    // exchange buffers (device)
+  void* xrecv = nullptr;
+  size_t xbytes = 0;                        // bytes per rank of the largest exchange
+  long long exch = 0;                       // exchanges in the current solve
+  long long exch_per_solve = 0;
 };
 
 namespace {
@@ -125,9 +150,14 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
   if (d->world < 1) return bad("world must be >= 1");
   if (d->world != d->pgrid[0] * d->pgrid[1] * d->pgrid[2]) return bad("world != prod(pgrid)");
   if (d->rank < 0 || d->rank >= d->world) return bad("rank out of range");
+  if (d->world > 1) {
+    for (int i = 0; i < 3; ++i)
+      if (d->sr_levels == 0 || (d->n[i] / d->seg) % d->pgrid[i])
+        return bad("world > 1 needs sr_levels >= 1 and pgrid dividing the segment grid");
+  }
   // supported-config checks
-  if (d->world != 1) {
-    msg = "multi-GPU descriptors are not supported by this build (world must be 1)";
+  if (d->world > 1 && d->comm != 0 && d->comm != 1) {
+    msg = "comm must be 0 (NCCL) or 1 (replay store)";
     return SR_ERR_UNSUPPORTED_CONFIG;
   }
   long long n0 = 1;
@@ -160,6 +190,45 @@ void make_plan(sr_fmg* h) {
   h->theta.assign(h->M + 1, 0);
   h->delta.assign(h->M + 1, 0);
   h->sigma.assign(h->M + 1, 0);
+  // partition: rank r owns a pgrid block of the SR segment grid
+  h->world = d->world;
+  h->rank = d->rank;
+  h->coord[0] = d->rank % d->pgrid[0];
+  h->coord[1] = (d->rank / d->pgrid[0]) % d->pgrid[1];
+  h->coord[2] = d->rank / (d->pgrid[0] * d->pgrid[1]);
+  for (int i = 0; i < 3; ++i) {
+    if (h->K > 0) {
+      h->nsr[i] = (int)(d->n[i] / d->seg) / d->pgrid[i];
+      h->blk_n[i] = h->nsr[i] * d->seg;
+    } else {
+      h->nsr[i] = 0;
+      h->blk_n[i] = (int)d->n[i];
+    }
+    h->blk_lo[i] = h->coord[i] * h->blk_n[i];
+    h->blkT_n[i] = h->blk_n[i] >> h->K;
+    h->blkT_lo[i] = h->blk_lo[i] >> h->K;
+  }
+  // f halos: SR level l reads f_l on C = V grown by J_l; a halo H_l >= J_l, halved per
+  // coarsening (the pyramid is local), kept a multiple of 4 cells above level T
+  h->H.assign(h->M + 1, 0);
+  h->flo.assign(h->M + 1, {0, 0, 0});
+  h->fdim.assign(h->M + 1, {0, 0, 0});
+  if (h->world > 1) {
+    int h1 = 0;
+    for (int l = h->T + 1; l <= h->M; ++l) {
+      const int j = buffer_of(d, l - h->T);
+      const int need = (j + (1 << (l - h->T - 1)) - 1) >> (l - h->T - 1);  // ceil(j/2^(l-T-1))
+      h1 = std::max(h1, need);
+    }
+    h1 = (int)round_up(std::max(h1, 1), 4);
+    for (int l = h->T; l <= h->M; ++l)
+      h->H[l] = l == h->T ? h1 / 2 : h1 << (l - h->T - 1);
+  }
+  for (int l = h->T; l <= h->M; ++l)
+    for (int i = 0; i < 3; ++i) {
+      h->flo[l][i] = (h->blk_lo[i] >> (h->M - l)) - h->H[l];
+      h->fdim[l][i] = (h->blk_n[i] >> (h->M - l)) + 2 * h->H[l];
+    }
   for (int l = 0; l <= h->M; ++l) {
     Lvl& L = h->L[l];
     const bool sr = l > h->T;
@@ -167,7 +236,8 @@ void make_plan(sr_fmg* h) {
     L.J = sr ? buffer_of(d, l - h->T) : 0;
     for (int i = 0; i < 3; ++i) {
       L.S[i] = sr ? (d->seg >> (h->M - l)) : L.N[i];
-      L.ns[i] = L.N[i] / L.S[i];
+      L.ns[i] = sr ? h->nsr[i] : 1;
+      L.so[i] = sr ? h->coord[i] * h->nsr[i] : 0;
       L.E[i] = L.S[i] + 2 * L.J + 2;
     }
     L.nsegs = L.ns[0] * L.ns[1] * L.ns[2];
@@ -184,7 +254,8 @@ void make_plan(sr_fmg* h) {
     // cell counts (region arithmetic of PAPER.md:187-210 on boxes)
     CellCounts& c = h->cells[l];
     for (int s = 0; s < L.nsegs; ++s) {
-      const int p[3] = {s % L.ns[0], (s / L.ns[0]) % L.ns[1], s / (L.ns[0] * L.ns[1])};
+      const int p[3] = {s % L.ns[0] + L.so[0], (s / L.ns[0]) % L.ns[1] + L.so[1],
+                        s / (L.ns[0] * L.ns[1]) + L.so[2]};
       long long vc = 1, vcg = 1;
       for (int i = 0; i < 3; ++i) {
         const int lo = p[i] * L.S[i], hi = lo + L.S[i];
@@ -299,19 +370,48 @@ struct Schedule {
 
   T* U(int l) { return (T*)h->B[l].u[h->B[l].cur]; }
 
+  // f_l as a dense view: the user's (haloed) block at l = M, the rank's haloed local
+  // pyramid block on SR levels (multi-GPU), the global f_l otherwise
   View<T> fview(int l) {
-    const Lvl& L = h->L[l];
-    View<T> v;
-    v.p = (l == h->M) ? f : (const T*)h->B[l].fpyr;
+    View<T> v{};
     v.global = 1;
-    v.sy = L.N[0];
-    v.sz = (long long)L.N[0] * L.N[1];
+    const bool local = l > h->T || (l == h->M);
+    if (local) {
+      v.base = (l == h->M) ? f : (const T*)(h->world > 1 ? h->B[l].floc : h->B[l].fpyr);
+      for (int i = 0; i < 3; ++i) {
+        v.dims[i] = h->fdim[l][i];
+        v.off[i] = h->flo[l][i];
+      }
+    } else {
+      v.base = (const T*)h->B[l].fpyr;
+      for (int i = 0; i < 3; ++i) {
+        v.dims[i] = h->L[l].N[i];
+        v.off[i] = 0;
+      }
+    }
+    v.sy = v.dims[0];
+    v.sz = (long long)v.dims[0] * v.dims[1];
+    v.p = v.base - (v.off[0] + v.off[1] * v.sy + v.off[2] * v.sz);  // virtual global origin
     v.ss = 0;
     return v;
   }
+  static srfmg::FusedRhs<T> frhs(const View<T>& v) {
+    srfmg::FusedRhs<T> r{};
+    r.p = v.p;
+    r.global = v.global;
+    r.base = v.base;
+    for (int i = 0; i < 3; ++i) {
+      r.dims[i] = v.dims[i];
+      r.off[i] = v.off[i];
+    }
+    return r;
+  }
+  static bool tma_rhs_ok(const View<T>& v) {  // tensor-map strides must be 16-byte multiples
+    return !v.global || ((long long)v.dims[0] * sizeof(T)) % 16 == 0;
+  }
   View<T> sview(int l) {
     const Lvl& L = h->L[l];
-    View<T> v;
+    View<T> v{};
     v.p = (const T*)h->B[l].rhs;
     v.global = 0;
     v.sy = L.py;
@@ -332,7 +432,7 @@ struct Schedule {
     // the fused pass marches z inside a CTA: use it only when segments x bands fill the
     // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
     if (deg == 2 && h->fused && (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
-        srfmg::cheb2_fused_ok<T>(L)) {
+        tma_rhs_ok(b) && srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
       const double rho0 = 1.0 / h->sigma[l];
       const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
@@ -341,19 +441,25 @@ struct Schedule {
       Launch g(h, st, KC_CHEB_FUSED, l,
                fin ? w * (2.0 * c.compute + nv)
                    : w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
-      srfmg::launch_cheb2_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
-                                   srfmg::FusedRhs<T>{b.p, b.global}, 1.0 / h->theta[l],
-                                   rho1 * rho0, 2.0 * rho1 / h->delta[l], st,
-                                   fin ? final_out : nullptr);
+      srfmg::FinalOut<T> fo{};
+      if (fin) {
+        fo.p = final_out;
+        for (int i = 0; i < 3; ++i) fo.bo[i] = h->blk_lo[i];
+        fo.sy = h->blk_n[0];
+        fo.sz = (long long)h->blk_n[0] * h->blk_n[1];
+      }
+      srfmg::launch_cheb2_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b),
+                                   1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st,
+                                   fo);
       bb.cur = 1 - bb.cur;
       if (fin) final_done = true;
       return;
     }
     if (deg == 1 && h->fused && (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
-        srfmg::cheb_spec_ok<T>(L)) {
+        tma_rhs_ok(b) && srfmg::cheb_spec_ok<T>(L)) {
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
-      srfmg::launch_cheb1_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
-                                   srfmg::FusedRhs<T>{b.p, b.global}, 1.0 / h->theta[l], st);
+      srfmg::launch_cheb1_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b),
+                                   1.0 / h->theta[l], st);
       bb.cur = 1 - bb.cur;
       return;
     }
@@ -400,6 +506,63 @@ struct Schedule {
                                st);
   }
 
+  // ---- multi-GPU exchanges: every rank owns a block of level T; an
+  // all-gather assembles the full level-T arrays on every rank
+  void rank_blockT(int r, int lo[3]) const {
+    const int c[3] = {r % h->d.pgrid[0], (r / h->d.pgrid[0]) % h->d.pgrid[1],
+                      r / (h->d.pgrid[0] * h->d.pgrid[1])};
+    for (int i = 0; i < 3; ++i) lo[i] = c[i] * h->blkT_n[i];
+  }
+  // fields: (base, sy, sz) strided arrays holding level T (index = global cell)
+  void exchange(int nf, T* const* base, const long long* sy, const long long* sz,
+                const int* own_lo) {
+    const long long nb = (long long)h->blkT_n[0] * h->blkT_n[1] * h->blkT_n[2];
+    T* snd = (T*)h->xsend;
+    T* rcv = (T*)h->xrecv;
+    for (int k = 0; k < nf; ++k)
+      srfmg::launch_box_copy<T>(base[k], sy[k], sz[k], own_lo, h->blkT_n, snd + k * nb, 1, st);
+    h->launches += nf;
+    const sr_status_t r = h->comm->allgather(h, snd, rcv, (size_t)nf * nb * sizeof(T), st);
+    if (r != SR_OK) h->sticky = r;
+    h->exch++;
+    for (int q = 0; q < h->world; ++q) {
+      if (q == h->rank) continue;
+      int lo[3];
+      rank_blockT(q, lo);
+      for (int k = 0; k < nf; ++k)
+        srfmg::launch_box_copy<T>(base[k], sy[k], sz[k], lo, h->blkT_n, rcv + (q * nf + k) * nb, 0,
+                                  st);
+      h->launches += nf;
+    }
+  }
+  void exchange_fT() {  // the rank's block of f_T (interior of its haloed local f_T)
+    const int HT = h->H[h->T];
+    const auto& d = h->fdim[h->T];
+    const int own[3] = {HT, HT, HT};
+    const long long nb = (long long)h->blkT_n[0] * h->blkT_n[1] * h->blkT_n[2];
+    T* snd = (T*)h->xsend;
+    T* rcv = (T*)h->xrecv;
+    srfmg::launch_box_copy<T>((T*)h->B[h->T].floc, d[0], (long long)d[0] * d[1], own, h->blkT_n,
+                              snd, 1, st);
+    const sr_status_t r = h->comm->allgather(h, snd, rcv, (size_t)nb * sizeof(T), st);
+    if (r != SR_OK) h->sticky = r;
+    h->exch++;
+    const Lvl& LT = h->L[h->T];
+    for (int q = 0; q < h->world; ++q) {
+      int lo[3];
+      rank_blockT(q, lo);
+      srfmg::launch_box_copy<T>((T*)h->B[h->T].fpyr, LT.N[0], (long long)LT.N[0] * LT.N[1], lo,
+                                h->blkT_n, rcv + q * nb, 0, st);
+    }
+    h->launches += 1 + h->world;
+  }
+  void exchange_uT() {  // u_T and R_T blocks written by this rank's k = 1 restriction
+    const Lvl& LT = h->L[h->T];
+    T* base[2] = {U(h->T) + LT.pz + LT.py + 1, (T*)h->B[h->T].rhs + LT.pz + LT.py + 1};
+    const long long sy[2] = {LT.py, LT.py}, sz[2] = {LT.pz, LT.pz};
+    exchange(2, base, sy, sz, h->blkT_lo);
+  }
+
   // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors
   void vcycle(int l, View<T> b) {
     if (l == 0) {  // L120-121: exact solve
@@ -416,6 +579,7 @@ struct Schedule {
       srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
                                 st);  // L113-115 / L233, L235
     }
+    if (h->world > 1 && l - 1 == h->T) exchange_uT();  // a8: level-T hand-off (R16)
     {
       const CellCounts& c = h->cells[l - 1];
       Launch g(h, st, KC_TAU, l - 1, w * (2.0 * c.storage + 2.0 * c.compute));
@@ -431,7 +595,17 @@ struct Schedule {
     const int M = h->M;
     final_out = uout;
     final_done = false;
-    for (int l = M; l >= 1; --l) {  // R6: f pyramid
+    // R6: f pyramid -- the rank's haloed blocks down to level T (multi-GPU), then the
+    // global levels below (after assembling f_T)
+    for (int l = M; l > h->T; --l) {
+      const auto& d = h->fdim[l];
+      const T* src = (l == M) ? f : (const T*)(h->world > 1 ? h->B[l].floc : h->B[l].fpyr);
+      T* dst = (T*)(h->world > 1 ? h->B[l - 1].floc : h->B[l - 1].fpyr);
+      Launch g(h, st, KC_PYRAMID, l, w * (double)d[0] * d[1] * d[2] * (1.0 + 1.0 / 8));
+      srfmg::launch_pyramid<T>(src, d[0], d[1], d[2], dst, st);
+    }
+    if (h->world > 1) exchange_fT();
+    for (int l = h->T; l >= 1; --l) {
       const Lvl& L = h->L[l];
       Launch g(h, st, KC_PYRAMID, l, w * (double)L.N[0] * L.N[1] * L.N[2] * (1.0 + 1.0 / 8));
       srfmg::launch_pyramid<T>(l == M ? f : (const T*)h->B[l].fpyr, L.N[0], L.N[1], L.N[2],
@@ -445,14 +619,16 @@ struct Schedule {
     }
     if (!final_done) {
       const Lvl& L = h->L[M];
-      Launch g(h, st, KC_GATHER, M, w * 2.0 * L.N[0] * (double)L.N[1] * L.N[2]);
-      srfmg::launch_gather<T>(L, U(M), uout, st);  // R19
+      Launch g(h, st, KC_GATHER, M, w * 2.0 * h->blk_n[0] * (double)h->blk_n[1] * h->blk_n[2]);
+      srfmg::launch_gather<T>(L, U(M), uout, h->blk_lo, h->blk_n[0],
+                              (long long)h->blk_n[0] * h->blk_n[1], st);  // R19
     }
   }
 };
 
 sr_status_t enqueue_solve(sr_fmg* h, const void* f, void* u, cudaStream_t st) {
   h->launches = 0;
+  h->exch = 0;
   h->prof_used = 0;
   for (int l = 0; l <= h->M; ++l) h->B[l].cur = 0;
   if (h->esize == 8) {
@@ -462,6 +638,7 @@ sr_status_t enqueue_solve(sr_fmg* h, const void* f, void* u, cudaStream_t st) {
     Schedule<float> s{h, st, (const float*)f, 4.0};
     s.run((float*)u);
   }
+  h->exch_per_solve = h->exch;
   if (h->sticky != SR_OK) return h->sticky;
   CU(h, cudaGetLastError());
   return SR_OK;
@@ -478,6 +655,86 @@ double alg_bytes(const sr_fmg* h) {
   return words * h->esize;
 }
 
+// ---- NCCL, loaded at run time from the libnccl.so.2 the process already uses (torch's)
+struct NcclApi {
+  typedef struct { char internal[128]; } UniqueId;
+  typedef void* CommT;
+  int (*getUniqueId)(UniqueId*) = nullptr;
+  int (*commInitRank)(CommT*, int, UniqueId, int) = nullptr;
+  int (*allGather)(const void*, void*, size_t, int, CommT, cudaStream_t) = nullptr;
+  int (*commDestroy)(CommT) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+      api.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return api;
+    }
+    api.getUniqueId = (int (*)(NcclApi::UniqueId*))dlsym(lib, "ncclGetUniqueId");
+    api.commInitRank =
+        (int (*)(NcclApi::CommT*, int, NcclApi::UniqueId, int))dlsym(lib, "ncclCommInitRank");
+    api.allGather = (int (*)(const void*, void*, size_t, int, NcclApi::CommT, cudaStream_t))dlsym(
+        lib, "ncclAllGather");
+    api.commDestroy = (int (*)(NcclApi::CommT))dlsym(lib, "ncclCommDestroy");
+    api.getErrorString = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
+    api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy;
+    if (!api.ok) api.why = "libnccl.so.2 lacks the expected symbols";
+  }
+  return api;
+}
+
+struct NcclComm : Comm {
+  NcclApi::CommT comm = nullptr;
+  ~NcclComm() override {
+    if (comm) nccl().commDestroy(comm);
+  }
+  sr_status_t allgather(sr_fmg* h, const void* send, void* recv, size_t bytes,
+                        cudaStream_t st) override {
+    const int r = nccl().allGather(send, recv, bytes, /*ncclInt8*/ 0, comm, st);
+    if (r != 0) return fail(h, SR_ERR_NCCL, std::string("ncclAllGather: ") +
+                                                (nccl().getErrorString ? nccl().getErrorString(r) : "error"));
+    return SR_OK;
+  }
+};
+
+// ---- test replay store: the blocks of every rank, per exchange, shared in one process
+struct ReplayStore {
+  int world;
+  std::map<long long, std::vector<std::vector<char>>> blocks;  // exchange -> rank -> bytes
+};
+
+struct ReplayComm : Comm {
+  ReplayStore* store = nullptr;
+  sr_status_t allgather(sr_fmg* h, const void* send, void* recv, size_t bytes,
+                        cudaStream_t st) override {
+    if (!store) return fail(h, SR_ERR_INVALID_ARGUMENT, "replay comm without a store");
+    auto& row = store->blocks[h->exch];
+    if ((int)row.size() != store->world) row.assign(store->world, std::vector<char>());
+    std::vector<char> mine(bytes);
+    CU(h, cudaMemcpyAsync(mine.data(), send, bytes, cudaMemcpyDeviceToHost, st));
+    CU(h, cudaStreamSynchronize(st));
+    row[h->rank] = mine;
+    for (int q = 0; q < store->world; ++q) {
+      char* dst = (char*)recv + (size_t)q * bytes;
+      if (row[q].size() == bytes)
+        CU(h, cudaMemcpyAsync(dst, row[q].data(), bytes, cudaMemcpyHostToDevice, st));
+      else
+        CU(h, cudaMemsetAsync(dst, 0, bytes, st));
+    }
+    CU(h, cudaStreamSynchronize(st));
+    return SR_OK;
+  }
+};
+
 void free_all(sr_fmg* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto& b : h->B) {
@@ -486,7 +743,12 @@ void free_all(sr_fmg* h) {
     cudaFree(b.rhs);
     cudaFree(b.t);
     cudaFree(b.fpyr);
+    cudaFree(b.floc);
   }
+  cudaFree(h->xsend);
+  cudaFree(h->xrecv);
+  delete h->comm;
+  h->comm = nullptr;
   cudaFree(h->ainv);
   cudaFree(h->host_f);
   cudaFree(h->host_u);
@@ -595,8 +857,17 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
     ok = ok && alloc(&h->B[l].u[0], bytes) && alloc(&h->B[l].u[1], bytes);
     if (l < h->M) {
       ok = ok && alloc(&h->B[l].rhs, bytes) && alloc(&h->B[l].t, bytes);
-      ok = ok && alloc(&h->B[l].fpyr, (size_t)L.N[0] * L.N[1] * L.N[2] * h->esize);
+      if (h->world == 1 || l <= h->T)
+        ok = ok && alloc(&h->B[l].fpyr, (size_t)L.N[0] * L.N[1] * L.N[2] * h->esize);
+      if (h->world > 1 && l >= h->T) {
+        const auto& fd = h->fdim[l];
+        ok = ok && alloc(&h->B[l].floc, (size_t)fd[0] * fd[1] * fd[2] * h->esize);
+      }
     }
+  }
+  if (h->world > 1) {
+    h->xbytes = (size_t)2 * h->blkT_n[0] * h->blkT_n[1] * h->blkT_n[2] * h->esize;
+    ok = ok && alloc(&h->xsend, h->xbytes) && alloc(&h->xrecv, h->xbytes * h->world);
   }
   std::vector<double> inv = coarsest_inverse(h->L[0]);
   const size_t n0sq = inv.size();
@@ -615,6 +886,32 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
     free_all(h);
     delete h;
     return fail(nullptr, SR_ERR_OUT_OF_MEMORY, "device allocation failed");
+  }
+  if (h->world > 1) {
+    if (d->comm == 1) {
+      h->comm = new ReplayComm();
+      h->d.use_graph = 0;  // host round trips inside the solve
+    } else {
+      NcclApi& api = nccl();
+      if (!api.ok || !d->nccl_id) {
+        const std::string why = !api.ok ? api.why : "world > 1 needs desc.nccl_id";
+        free_all(h);
+        delete h;
+        return fail(nullptr, api.ok ? SR_ERR_INVALID_ARGUMENT : SR_ERR_NCCL, why);
+      }
+      NcclComm* c = new NcclComm();
+      NcclApi::UniqueId id;
+      std::memcpy(&id, d->nccl_id, sizeof(id));
+      const int r = api.commInitRank(&c->comm, d->world, id, d->rank);
+      h->comm = c;
+      if (r != 0) {
+        const std::string why = std::string("ncclCommInitRank: ") +
+                                (api.getErrorString ? api.getErrorString(r) : "error");
+        free_all(h);
+        delete h;
+        return fail(nullptr, SR_ERR_NCCL, why);
+      }
+    }
   }
   *out = h;
   return SR_OK;
@@ -659,16 +956,17 @@ sr_status_t sr_fmg_solve_host(sr_fmg_t* h, const void* f_host, void* u_host) {
   if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
   if (h->sticky != SR_OK) return h->sticky;
   if (!f_host || !u_host) return fail(h, SR_ERR_INVALID_ARGUMENT, "f or u is NULL");
-  const Lvl& L = h->L[h->M];
-  const size_t bytes = (size_t)L.N[0] * L.N[1] * L.N[2] * h->esize;
+  const auto& fd = h->fdim[h->M];
+  const size_t fbytes = (size_t)fd[0] * fd[1] * fd[2] * h->esize;
+  const size_t ubytes = (size_t)h->blk_n[0] * h->blk_n[1] * h->blk_n[2] * h->esize;
   if (!h->host_f) {
-    CU(h, cudaMalloc(&h->host_f, bytes));
-    CU(h, cudaMalloc(&h->host_u, bytes));
+    CU(h, cudaMalloc(&h->host_f, fbytes));
+    CU(h, cudaMalloc(&h->host_u, ubytes));
   }
-  CU(h, cudaMemcpyAsync(h->host_f, f_host, bytes, cudaMemcpyHostToDevice, h->stream));
+  CU(h, cudaMemcpyAsync(h->host_f, f_host, fbytes, cudaMemcpyHostToDevice, h->stream));
   sr_status_t st = sr_fmg_solve(h, h->host_f, h->host_u);
   if (st != SR_OK) return st;
-  CU(h, cudaMemcpyAsync(u_host, h->host_u, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaMemcpyAsync(u_host, h->host_u, ubytes, cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
   return SR_OK;
 }
@@ -678,6 +976,57 @@ void sr_fmg_destroy(sr_fmg_t* h) {
   cudaStreamSynchronize(h->stream);
   free_all(h);
   delete h;
+}
+
+sr_status_t sr_fmg_partition(const sr_fmg_desc_t* d, sr_fmg_partition_t* out) {
+  if (!d || !out) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "NULL argument");
+  std::string msg;
+  const sr_status_t st = validate(d, msg);
+  if (st != SR_OK) return fail(nullptr, st, msg);
+  sr_fmg tmp;
+  tmp.d = *d;
+  make_plan(&tmp);
+  std::memset(out, 0, sizeof(*out));
+  out->world = tmp.world;
+  out->rank = tmp.rank;
+  for (int i = 0; i < 3; ++i) {
+    out->coord[i] = tmp.coord[i];
+    out->segs_per_rank[i] = tmp.nsr[i];
+    out->block_lo[i] = tmp.blk_lo[i];
+    out->block_n[i] = tmp.blk_n[i];
+    out->f_dims[i] = tmp.fdim[tmp.M][i];
+    out->level_T_lo[i] = tmp.blkT_lo[i];
+    out->level_T_n[i] = tmp.blkT_n[i];
+  }
+  out->f_halo = tmp.H[tmp.M];
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "NULL argument");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(nullptr, SR_ERR_NCCL, api.why);
+  NcclApi::UniqueId id;
+  const int r = api.getUniqueId(&id);
+  if (r != 0) return fail(nullptr, SR_ERR_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(out128, &id, sizeof(id));
+  return SR_OK;
+}
+
+void* sr_fmg_replay_store_create(int32_t world) {
+  ReplayStore* s = new ReplayStore();
+  s->world = world;
+  return s;
+}
+
+void sr_fmg_replay_store_destroy(void* store) { delete (ReplayStore*)store; }
+
+sr_status_t sr_fmg_set_replay(sr_fmg_t* h, void* store) {
+  if (!h || !store) return fail(h, SR_ERR_INVALID_ARGUMENT, "NULL argument");
+  ReplayComm* c = dynamic_cast<ReplayComm*>(h->comm);
+  if (!c) return fail(h, SR_ERR_INVALID_ARGUMENT, "handle was not created with comm = 1");
+  c->store = (ReplayStore*)store;
+  return SR_OK;
 }
 
 sr_status_t sr_fmg_get_info(const sr_fmg_t* h, sr_fmg_info_t* info) {
@@ -718,6 +1067,15 @@ sr_status_t sr_fmg_get_info(const sr_fmg_t* h, sr_fmg_info_t* info) {
   }
   // launches of the last enqueued solve (exact), else the unfused schedule's count
   info->launches_per_solve = h->launches > 0 ? h->launches : n;
+  info->world = h->world;
+  info->rank = h->rank;
+  for (int i = 0; i < 3; ++i) {
+    info->block_lo[i] = h->blk_lo[i];
+    info->block_n[i] = h->blk_n[i];
+    info->f_dims[i] = h->fdim[h->M][i];
+  }
+  info->f_halo = h->H[h->M];
+  info->exchanges_per_solve = h->world > 1 ? 1 + h->K : 0;
   info->alg_bytes_per_solve = alg_bytes(h);
   return SR_OK;
 }

@@ -1,0 +1,113 @@
+"""Multi-rank path on CPU (gloo, world size 2): the product's partition arithmetic drives a
+decomposed oracle solve -- each rank runs only its own segments and the ranks all-gather
+their level-T blocks at the k = 1 hand-off (the library's exchange points).
+The result must equal the single-process solve BITWISE (R25): SR segments are independent
+ and the coarse levels are solved redundantly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import workloads as W
+from oracle import Field
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+CASES = {
+    "x-split": dict(n=(32, 16, 16), M=3, seg=8, buffer=2, K=2, pgrid=(2, 1, 1)),
+    "y-split": dict(n=(16, 32, 16), M=3, seg=8, buffer=1, K=1, pgrid=(1, 2, 1)),
+}
+
+
+def _worker(rank, world, port, case, outq):
+    from paper_1406_7808_b200 import partition
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = CASES[case]
+    part = partition(c["n"], c["M"], c["seg"], c["buffer"], c["K"], world, rank, c["pgrid"])
+    f = W.make_rhs("manufactured+noise", c["n"])
+    o = O.Oracle(O.Config(n=c["n"], M=c["M"], seg=c["seg"], buffer=c["buffer"], K=c["K"]))
+    # own segments (array order (z, y, x) vs the partition's (x, y, z))
+    lo = [part["coord"][d] * part["segs_per_rank"][d] for d in range(3)]
+    hi = [lo[d] + part["segs_per_rank"][d] for d in range(3)]
+    o.segs = [p for p in o.segs if all(lo[d] <= p[2 - d] < hi[d] for d in range(3))]
+    Tn = part["level_T_n"]
+    Tlo_all = [None] * world
+    dist.all_gather_object(Tlo_all, part["level_T_lo"])
+
+    def exchange(uT, RT):
+        for fld in (uT, RT):
+            mine = torch.from_numpy(np.ascontiguousarray(
+                fld[_box(part["level_T_lo"], Tn)]))
+            got = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(got, mine)
+            for q in range(world):
+                fld[_box(Tlo_all[q], Tn)] = got[q].numpy()
+
+    o.exchange_T = exchange
+    u = o.solve(f)
+    bl, bn = part["block_lo"], part["block_n"]
+    outq.put((rank, u[bl[2]:bl[2] + bn[2], bl[1]:bl[1] + bn[1], bl[0]:bl[0] + bn[0]].copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _box(lo_xyz, n_xyz):
+    from oracle import Box
+    return Box((lo_xyz[2], lo_xyz[1], lo_xyz[0]),
+               (lo_xyz[2] + n_xyz[2], lo_xyz[1] + n_xyz[1], lo_xyz[0] + n_xyz[0]))
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_decomposed_solve_equals_single_process(case):
+    c = CASES[case]
+    world = int(np.prod(c["pgrid"]))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    f = W.make_rhs("manufactured+noise", c["n"])
+    ref = O.solve(f, O.Config(n=c["n"], M=c["M"], seg=c["seg"], buffer=c["buffer"], K=c["K"]))
+    from paper_1406_7808_b200 import partition
+    for r in range(world):
+        part = partition(c["n"], c["M"], c["seg"], c["buffer"], c["K"], world, r, c["pgrid"])
+        bl, bn = part["block_lo"], part["block_n"]
+        blk = ref[bl[2]:bl[2] + bn[2], bl[1]:bl[1] + bn[1], bl[0]:bl[0] + bn[0]]
+        assert np.array_equal(res[r], blk), (case, r)
+
+
+def test_partition_blocks_tile_the_grid():
+    from paper_1406_7808_b200 import partition
+    for n, seg, K, pg in [((1024, 1024, 1024), 64, 4, (2, 2, 2)), ((64, 32, 32), 8, 2, (2, 2, 1)),
+                          ((128, 128, 64), 16, 3, (4, 2, 1))]:
+        world = int(np.prod(pg))
+        M = int(np.log2(min(n))) - 1
+        cover = np.zeros((n[2] // seg, n[1] // seg, n[0] // seg), int)
+        for r in range(world):
+            p = partition(n, M, seg, 2, K, world, r, pg)
+            assert p["f_halo"] >= 2 << (K - 1) and p["f_halo"] % 4 == 0
+            assert all(p["f_dims"][d] == p["block_n"][d] + 2 * p["f_halo"] for d in range(3))
+            assert all(p["level_T_n"][d] * (1 << K) == p["block_n"][d] for d in range(3))
+            lo = [p["block_lo"][d] // seg for d in range(3)]
+            sl = tuple(slice(lo[2 - d], lo[2 - d] + p["segs_per_rank"][2 - d]) for d in range(3))
+            cover[sl] += 1
+        assert np.all(cover == 1)

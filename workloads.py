@@ -72,6 +72,19 @@ def manufactured_f(n, h, R=None) -> np.ndarray:
     return -f
 
 
+def manufactured_f_block(h, R, lo, dims) -> np.ndarray:
+    """f = -Lap u of the manufactured solution on the block of cells [lo, lo + dims)
+    (paper order), shape (dims3, dims2, dims1) -- a multi-GPU rank's (haloed) local block;
+    cells outside the domain are evaluated by the same formula (they are never used)."""
+    g = [(np.arange(lo[d], lo[d] + dims[d], dtype=np.float64) + 0.5) * h for d in range(3)]
+    p = [g[d] ** 4 - R[d] ** 2 * g[d] ** 2 for d in range(3)]
+    q = [12.0 * g[d] ** 2 - 2.0 * R[d] ** 2 for d in range(3)]
+    f = q[2][:, None, None] * p[1][None, :, None] * p[0][None, None, :]
+    f = f + p[2][:, None, None] * q[1][None, :, None] * p[0][None, None, :]
+    f = f + p[2][:, None, None] * p[1][None, :, None] * q[0][None, None, :]
+    return -f
+
+
 def noise(n, sigma=1e-3, seed=SEED) -> np.ndarray:
     """i.i.d. N(0, sigma^2), PCG64(seed), filled in x-fastest order (reading R21)."""
     rng = np.random.Generator(np.random.PCG64(seed))
