@@ -39,6 +39,7 @@ WORKLOADS = {
 # bounded CPU sample of C3 for the oracle: the same 8^3 segment grid, K = 4, J = 2, at
 # 128^3 (1/64 of the cells); about 7 s of numpy per solve on one core
 ORACLE_SAMPLE = dict(n=(128, 128, 128), M=6, seg=16, buffer=2, K=4, rhs="manufactured+noise")
+PGRID = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 KC_CHEB_FUSED = 7  # kernel class index of the fused TMA Chebyshev pass (sr_fmg_kernel_name)
 
 
@@ -48,7 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default=None, choices=sorted(WORKLOADS) + ["C4"],
+                    help="default: C3 on 1 GPU, C4 (weak scaling, 512^3 per GPU) on N > 1")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -146,7 +148,8 @@ def run_reference(args):
         "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} (bounded CPU sample)", "sample": sample_desc()},
+        "config": {"workload": f"{args.config or 'C3'} (bounded CPU sample)",
+                   "sample": sample_desc()},
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle",
                          "sample": sample_desc()},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
@@ -169,15 +172,37 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1406_7808_b200 import Solver
+    from paper_1406_7808_b200 import Solver, nccl_unique_id
 
-    n, M, seg, buf, K, rhs = WORKLOADS[args.config]
-    tdt = torch.float64 if args.dtype == "f64" else torch.float32
-    solver = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=args.dtype)
-    f_host = W.make_rhs(rhs, n).astype(np.float64 if args.dtype == "f64" else np.float32)
+    config = args.config or ("C3" if world == 1 else "C4")
+    npd = np.float64 if args.dtype == "f64" else np.float32
+    if config == "C4":
+        # weak scaling (BASELINE configs[3]): 512^3 cells per GPU on the global grid
+        # (512 P1, 512 P2, 512 P3), h = 1/512, R = pgrid, manufactured f, M = 8 (coarsest 2R)
+        P = PGRID.get(world, (world, 1, 1))
+        n = (512 * P[0], 512 * P[1], 512 * P[2])
+        M, seg, buf, K, rhs, h = 8, 64, 2, 4, "manufactured", 1.0 / 512
+    else:
+        P = (1, 1, 1)
+        n, M, seg, buf, K, rhs = WORKLOADS[config]
+        h = 1.0 / n[0]
+    nccl_id = None
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    solver = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=args.dtype, h=h, world=world,
+                    rank=rank, pgrid=P, nccl_id=nccl_id)
+    if world == 1 and config != "C4":
+        f_host = W.make_rhs(rhs, n).astype(npd)
+    else:
+        # this rank's haloed block, evaluated directly (no global array on any rank)
+        lo = [solver.block_lo[d] - solver.f_halo for d in range(3)]
+        dims = [solver.block_n[d] + 2 * solver.f_halo for d in range(3)]
+        f_host = W.manufactured_f_block(h, W.extents(n, h), lo, dims).astype(npd)
     f = torch.from_numpy(f_host).cuda()
-    u = torch.empty_like(f)
-    cells = float(np.prod(n))
+    u = torch.empty(solver.shape, dtype=f.dtype, device=f.device)
+    cells = float(np.prod(solver.block_n))  # this rank's fine cells
     stream = torch.cuda.current_stream()
 
     for _ in range(max(args.warmup, 3)):
@@ -216,7 +241,7 @@ def main():
     # ---- end-to-end through the public API from pinned host buffers
     solver.profile_select(-1, -1)
     fh = torch.from_numpy(f_host).pin_memory()
-    uh = torch.empty_like(fh).pin_memory()
+    uh = torch.empty(solver.shape, dtype=fh.dtype).pin_memory()
     solver.solve_host(fh, uh)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -230,7 +255,8 @@ def main():
         t = torch.tensor([ems], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
-    nbytes = f_host.nbytes
+    nbytes_in = f_host.nbytes
+    nbytes_out = int(np.prod(solver.shape)) * f_host.itemsize
 
     peak, peak_src = measured_peak()
     achieved = (kbytes / (kms / 1e3)) / 1e9 if kms > 0 else None
@@ -238,7 +264,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"{args.config}_{args.dtype}")
+            traffic = json.load(open(tp)).get(f"{config}_{args.dtype}")
         except Exception:
             traffic = None
     line = {
@@ -247,13 +273,17 @@ def main():
         "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
-        "data": f"synthetic ({rhs}, seed {W.SEED})",
-        "config": {"workload": f"{args.config}: {n[0]}x{n[1]}x{n[2]} cells per GPU, M={M}, "
-                               f"seg={seg}, buffer={buf}, K={K} SR levels, F(1,2,2)",
-                   "global_cells": cells * world,
-                   "parallelism": "independent replicas per GPU" if world > 1 else "1 GPU",
+        "data": f"synthetic ({rhs}" + (f", seed {W.SEED})" if "noise" in rhs else ")"),
+        "config": {"workload": f"{config}: global {n[0]}x{n[1]}x{n[2]} cells "
+                               f"({int(cells)} per GPU), M={M}, seg={seg}, buffer={buf}, "
+                               f"K={K} SR levels, F(1,2,2), rhs {rhs}",
+                   "global_cells": cells * world, "pgrid": list(P),
+                   "parallelism": (f"segment blocks pgrid {P}: SR levels without communication, "
+                                   f"{solver.exchanges_per_solve} NCCL all-gathers per solve "
+                                   "(level-T blocks), coarse levels redundant")
+                   if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (f %.2f GB, workspace %.2f GB)"
-                         % (nbytes / 1e9, solver.workspace_bytes / 1e9)},
+                         % (nbytes_in / 1e9, solver.workspace_bytes / 1e9)},
         "roofline": {"bound": "hbm", "kernel": "k_cheb2/k_cheb2s (fused TMA Chebyshev pass) @ finest level",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
@@ -263,7 +293,7 @@ def main():
                      "avg_launch_ms": kms / max(klaunch, 1),
                      "share_of_step": (kms / args.steps) / ms if ms > 0 else None},
         "e2e": {"value": cells * world / (ems / 1e3), "unit": "cells/s",
-                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "h2d_bytes_per_step": nbytes_in, "d2h_bytes_per_step": nbytes_out,
                 "ms_per_step": ems},
         "gpu_launches": int(solver.launches_per_solve * args.steps),
         "solve_alg_bytes": solver.alg_bytes_per_solve,
