@@ -88,10 +88,29 @@ def test_invalid_descriptors_rejected_before_allocation(kw):
 def test_unsupported_configs():
     from paper_1406_7808_b200._lib import SR_ERR_UNSUPPORTED_CONFIG, lib
     for kw in (dict(n=(64, 64, 64), M=1, sr_levels=0),           # 32^3 coarsest grid
-               dict(world=2, pgrid=(2, 1, 1))):                 # multi-GPU descriptor
+               dict(world=2, pgrid=(2, 1, 1), comm=5)):         # unknown comm backend
         d = _desc(**kw)
         h = ctypes.c_void_p()
         assert lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(h)) == SR_ERR_UNSUPPORTED_CONFIG
+
+
+def test_multi_gpu_descriptor_validation():
+    from paper_1406_7808_b200._lib import SR_ERR_INVALID_ARGUMENT, lib
+    for kw in (dict(world=2, pgrid=(2, 1, 1), sr_levels=0),     # multi-GPU needs SR levels
+               dict(world=3, pgrid=(3, 1, 1)),                   # 2 segments per dim
+               dict(world=2, pgrid=(1, 1, 1)),                   # world != prod(pgrid)
+               dict(world=2, pgrid=(2, 1, 1), rank=2)):          # rank out of range
+        d = _desc(**kw)
+        h = ctypes.c_void_p()
+        assert lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(h)) == SR_ERR_INVALID_ARGUMENT
+
+
+def test_partition_and_nccl_id_need_no_gpu():
+    from paper_1406_7808_b200 import nccl_unique_id, partition
+    p = partition((64, 64, 64), 5, 8, 2, 2, 2, 1, (2, 1, 1))
+    assert p["block_lo"] == (32, 0, 0) and p["block_n"] == (32, 64, 64)
+    assert p["level_T_n"] == (8, 16, 16) and p["f_halo"] == 8   # 4 at level T+1, doubled
+    assert len(nccl_unique_id()) == 128
 
 
 def test_null_arguments():
