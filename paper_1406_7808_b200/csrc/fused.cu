@@ -267,10 +267,12 @@ struct SpecGeom {
   static constexpr int U1S = ((BH + 2) * PY + A - 1) / A * A;
   static constexpr int RU = 3, RF = 4;
   static constexpr size_t SMEM = (size_t)(RU * U0S + RF * FS + 3 * U1S) * sizeof(T) + 8 * (RU + RF);
+  static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the smem allows
 };
 
 template <class T, int PY, int BH, int MAXS, int RG, int NST>
-__global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT, 1)
+__global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
+                                  SpecGeom<T, PY, BH, MAXS, RG>::MINB)
     k_cheb2s(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
   using G = SpecGeom<T, PY, BH, MAXS, RG>;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -597,6 +599,16 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
 template <class T>
 bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
   if (!spec_enabled()) return false;
+  static int alt = -1;
+  if (alt < 0) {
+    const char* e = std::getenv("SR_FMG_CHEB2_ALT");
+    alt = e ? std::atoi(e) : 0;
+  }
+  if constexpr (sizeof(T) == 8) {
+    if (alt == 1 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
+    if (alt == 2 && try_spec<T, 72, 18, 4>(L, a, b, nst, st)) return true;
+    if (alt == 3 && try_spec<T, 72, 24, 4>(L, a, b, nst, st)) return true;
+  }
   if constexpr (sizeof(T) == 8)
     return try_spec<T, 72, 35, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
            try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);
