@@ -270,7 +270,7 @@ struct SpecGeom {
   static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the smem allows
 };
 
-template <class T, int PY, int BH, int MAXS, int RG, int NST>
+template <class T, int PY, int BH, int MAXS, int RG, int NST, int FIN = 0>
 __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
                                   SpecGeom<T, PY, BH, MAXS, RG>::MINB)
     k_cheb2s(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
             const T r = fp[k * G::FP] - (d * c1 - sum) * ih2;
             v2 = c1 + cm * (c1 - u0v) + cr * r;
           }
-          if (a.fin.p == nullptr) {
+          if constexpr (FIN == 0) {
             orow[k * PY] = v2;
           } else {
             // last pass of the solve (R19): genuine cells straight to the user's u
@@ -583,14 +583,17 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, nt, smem, st>>>(map, a);
   };
+  const bool fin = a.fin.p != nullptr;
   if (b.global) {
     using G = SpecGeom<T, PY, BH, MAXS, 1>;
     if (!encode_rhs_map<T>(&map, b, G::FP, BH + 2)) return false;
-    if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 1, 2>, G::SMEM, G::NT);
+    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 1, 2, 1>, G::SMEM, G::NT);
+    else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 1, 2>, G::SMEM, G::NT);
     else go(k_cheb2s<T, PY, BH, MAXS, 1, 1>, G::SMEM, G::NT);
   } else {
     using G = SpecGeom<T, PY, BH, MAXS, 0>;
-    if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 0, 2>, G::SMEM, G::NT);
+    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 1>, G::SMEM, G::NT);
+    else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 0, 2>, G::SMEM, G::NT);
     else go(k_cheb2s<T, PY, BH, MAXS, 0, 1>, G::SMEM, G::NT);
   }
   return true;
