@@ -1,7 +1,7 @@
 """Build the SR-FMG shared library in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_1406_7808_b200.build          # incremental
-    python -m paper_1406_7808_b200.build --force
+    python paper_1406_7808_b200/build.py          # incremental
+    python paper_1406_7808_b200/build.py --force
 
 Produces paper_1406_7808_b200/libsrfmg.so (C ABI of include/sr_fmg.h).  No GPU needed:
 nvcc cross-compiles.  Static CUDA runtime; no torch headers or symbols.
