@@ -625,6 +625,13 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
 }  // namespace
 
 template <class T>
+bool encode_dense_tmap(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows) {
+  return get_encode() && encode_rhs_map<T>(map, rb, bw, rows);
+}
+template bool encode_dense_tmap<double>(CUtensorMap*, const FusedRhs<double>&, int, int);
+template bool encode_dense_tmap<float>(CUtensorMap*, const FusedRhs<float>&, int, int);
+
+template <class T>
 bool cheb2_final_ok(const Lvl& L) {
   return cheb_spec_ok<T>(L);
 }

@@ -1,5 +1,7 @@
 // Fused, TMA-fed multi-sweep kernels of the SR-FMG schedule (see fused.cu).
 #pragma once
+#include <cuda.h>
+
 #include "kernels.cuh"
 
 namespace srfmg {
@@ -39,6 +41,10 @@ bool cheb2_final_ok(const Lvl& L);
 template <class T>
 bool launch_cheb1_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, double c0,
                         cudaStream_t st);
+
+// 3-D tensor map of a dense rhs array, box (bw, rows, 1), element type T (fused.cu).
+template <class T>
+bool encode_dense_tmap(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows);
 
 // A geometry-specialised instantiation exists for this level's row pitch.
 template <class T>

@@ -17,6 +17,7 @@
 
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "pass.cuh"
 #include "sr_fmg.h"
 
 using srfmg::Lvl;
@@ -28,7 +29,7 @@ thread_local std::string g_tls_err = "no error";
 
 // indices into srfmg::kKernelNames (sr_fmg_kernel_name)
 enum KernelClass { KC_CHEB = 0, KC_RESTRICT, KC_TAU, KC_PROLONG, KC_COARSEST, KC_PYRAMID,
-                   KC_GATHER, KC_CHEB_FUSED, KC_COUNT };
+                   KC_GATHER, KC_CHEB_FUSED, KC_PASS_ENTRY, KC_PASS_DOWN, KC_PASS_UP, KC_COUNT };
 
 struct LevelBufs {
   void* u[2] = {nullptr, nullptr};  // two solution buffers (Chebyshev ping-pong)
@@ -84,6 +85,10 @@ struct sr_fmg {
   bool sync_debug = false;
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
   bool force = false; // SR_FMG_FORCE_FUSED=1: use them even on levels too small to fill the GPU
+  // fused multi-stage SR passes (pass.cu); SR_FMG_PASS=0 disables them.  pass_entry picks
+  // the FMG-entry chain: 4 = Pi+S1+S2+restrict, 3 = Pi+S1+S2 then restrict, 1 = Pi+S1
+  bool pass = true;
+  int pass_entry = 4;
   int prof_cls = -1, prof_level = -1;
   std::vector<ProfRec> prof;
   size_t prof_used = 0;
@@ -563,22 +568,118 @@ struct Schedule {
     exchange(2, base, sy, sz, h->blkT_lo);
   }
 
-  // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors
-  void vcycle(int l, View<T> b) {
+  // ---- fused multi-stage passes (pass.cu) on SR levels
+  bool pass_on(int l, int src, int nstep, int sink, const View<T>& b) {
+    if (!h->pass || l <= h->T || l < 1) return false;
+    if (h->d.alpha != 1 || h->d.nu1 != 2 || h->d.nu2 != 2) return false;
+    const Lvl& L = h->L[l];
+    if (!h->force && (long long)L.nsegs * ((L.E[1] + 13) / 14) < 148) return false;
+    if (!tma_rhs_ok(b)) return false;
+    return srfmg::pass_ok<T>(src, nstep, sink, L, h->L[l - 1], b.global);
+  }
+  // run one pass: steps = the Chebyshev steps of the chain (R8), u ping-pongs on level l
+  void run_pass(int l, int src, int nstep, int sink, const View<T>& b) {
+    const Lvl& L = h->L[l];
+    LevelBufs& bb = h->B[l];
+    srfmg::PassSpec<T> ps{};
+    ps.src = src;
+    ps.nstep = nstep;
+    ps.sink = sink;
+    ps.L = L;
+    ps.Lc = h->L[l - 1];
+    ps.uin = (const T*)bb.u[bb.cur];
+    ps.uout = (T*)bb.u[1 - bb.cur];
+    ps.rhs = frhs(b);
+    ps.w = U(l - 1);
+    ps.t = (const T*)h->B[l - 1].t;
+    // PSET + RESTRICT reads the coarse u (Pi) while restricting: restrict into t and
+    // merge afterwards (the coarse t is rewritten by the tau step that follows anyway)
+    const bool merge = src == srfmg::kSrcPset && sink == srfmg::kSinkRestrict;
+    ps.uc = merge ? (T*)h->B[l - 1].t : U(l - 1);
+    ps.rc = (T*)h->B[l - 1].rhs;
+    ps.jr = jr_for(l);
+    const double c0 = 1.0 / h->theta[l];
+    const double rho0 = 1.0 / h->sigma[l];
+    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
+    for (int i = 0; i < nstep; ++i) ps.cr[i] = c0;  // degree-1 steps / first step of degree 2
+    if (nstep >= 2) {                               // second step of the degree-2 polynomial
+      ps.cr[nstep - 1] = 2.0 * rho1 / h->delta[l];
+      ps.cm[nstep - 1] = rho1 * rho0;
+    }
+    const CellCounts& c = h->cells[l];
+    const double cgc = (double)c.cg / 8.0;  // coarse footprint (about 1/8 of C ∪ GSR)
+    double words = 0;
+    int cls = KC_PASS_ENTRY;
+    if (src == srfmg::kSrcPset) words = cgc + c.compute + c.cg;
+    if (src == srfmg::kSrcLoad) { words = 2.0 * c.cg + c.compute; cls = KC_PASS_DOWN; }
+    if (src == srfmg::kSrcPadd) { words = 2.0 * cgc + c.cg + c.compute; cls = KC_PASS_UP; }
+    if (sink == srfmg::kSinkRestrict) words += c.compute / 4.0;
+    if (sink == srfmg::kSinkFinal) {
+      ps.fin.p = final_out;
+      for (int i = 0; i < 3; ++i) ps.fin.bo[i] = h->blk_lo[i];
+      ps.fin.sy = h->blk_n[0];
+      ps.fin.sz = (long long)h->blk_n[0] * h->blk_n[1];
+      words += (double)h->blk_n[0] * h->blk_n[1] * h->blk_n[2];
+    } else {
+      words += c.cg;
+    }
+    {
+      Launch g(h, st, cls, l, w * words);
+      srfmg::launch_pass<T>(ps, st);
+    }
+    if (merge) {
+      Launch g(h, st, KC_TAU, l - 1, w * 2.0 * c.compute / 8.0);
+      srfmg::launch_merge_f<T>(L, h->L[l - 1], (const T*)h->B[l - 1].t, U(l - 1), ps.jr, st);
+    }
+    if (sink == srfmg::kSinkFinal) final_done = true;
+    else bb.cur = 1 - bb.cur;
+  }
+
+  void restrict_std(int l, View<T> b) {
+    const int jr = jr_for(l);
+    const Lvl& Lf = h->L[l];
+    double tgt = h->L[l].nsegs;
+    for (int i = 0; i < 3; ++i) tgt *= (Lf.S[i] / 2 + 2 * jr);
+    Launch g(h, st, KC_RESTRICT, l, w * (16.0 + 2.0) * tgt);
+    srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
+                              st);  // L113-115 / L233, L235
+  }
+
+  // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors.
+  // entry = the FMG visit of level l (fig:fmg L139-141 / fig:fmgsr L221-223): Pi and S^alpha
+  // run first, fused with the V-cycle's first half where a pass exists.
+  void vcycle(int l, View<T> b, bool entry = false) {
     if (l == 0) {  // L120-121: exact solve
       coarsest(b);
       return;
     }
-    cheb(l, h->d.nu1, b);  // L112 / L232
-    const int jr = jr_for(l);
-    {
-      const Lvl& Lf = h->L[l];
-      double tgt = h->L[l].nsegs;
-      for (int i = 0; i < 3; ++i) tgt *= (Lf.S[i] / 2 + 2 * jr);
-      Launch g(h, st, KC_RESTRICT, l, w * (16.0 + 2.0) * tgt);
-      srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
-                                st);  // L113-115 / L233, L235
+    using namespace srfmg;
+    bool restricted = false;
+    if (entry) {
+      if (h->pass_entry == 4 && pass_on(l, kSrcPset, 3, kSinkRestrict, b)) {
+        // (the merge into u_{l-1} precedes the level-T exchange below)
+        run_pass(l, kSrcPset, 3, kSinkRestrict, b);  // Pi, S^1, S^2, r, restrict
+        restricted = true;
+      } else if (h->pass_entry == 3 && pass_on(l, kSrcPset, 3, kSinkStore, b)) {
+        run_pass(l, kSrcPset, 3, kSinkStore, b);  // Pi, S^1, S^2
+        restrict_std(l, b);
+        restricted = true;
+      } else if (h->pass_entry == 1 && pass_on(l, kSrcPset, 1, kSinkStore, b)) {
+        run_pass(l, kSrcPset, 1, kSinkStore, b);  // Pi, S^1
+      } else {
+        prolong(l, 0);               // Pi onto C ∪ GSR
+        cheb(l, h->d.alpha, b);      // S^alpha
+      }
     }
+    if (!restricted) {
+      if (pass_on(l, kSrcLoad, 2, kSinkRestrict, b)) {
+        run_pass(l, kSrcLoad, 2, kSinkRestrict, b);  // L112-115 / L232-235 in one pass
+      } else {
+        cheb(l, h->d.nu1, b);  // L112 / L232
+        restrict_std(l, b);
+      }
+    }
+    const int jr = jr_for(l);
     if (h->world > 1 && l - 1 == h->T) exchange_uT();  // a8: level-T hand-off (R16)
     {
       const CellCounts& c = h->cells[l - 1];
@@ -587,8 +688,15 @@ struct Schedule {
                            st);  // L116-117 / L234-236
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
-    prolong(l, 1);                // L118 / L241
-    cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
+    const bool last = l == h->M && final_out != nullptr;
+    if (last && pass_on(l, kSrcPadd, 2, kSinkFinal, b)) {
+      run_pass(l, kSrcPadd, 2, kSinkFinal, b);  // L241-242, genuine cells -> user u (R19)
+    } else if (!last && pass_on(l, kSrcPadd, 2, kSinkStore, b)) {
+      run_pass(l, kSrcPadd, 2, kSinkStore, b);  // L241-242 in one pass
+    } else {
+      prolong(l, 1);                    // L118 / L241
+      cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
+    }
   }
 
   void run(T* uout) {
@@ -612,11 +720,8 @@ struct Schedule {
                                (T*)h->B[l - 1].fpyr, st);
     }
     coarsest(fview(0));  // fig:fmg L137-138
-    for (int l = 1; l <= M; ++l) {  // fig:fmg L139-142 (l <= T), fig:fmgsr L220-223 (l > T)
-      prolong(l, 0);                // Pi onto C ∪ GSR
-      cheb(l, h->d.alpha, fview(l));
-      vcycle(l, fview(l));
-    }
+    for (int l = 1; l <= M; ++l)  // fig:fmg L139-142 (l <= T), fig:fmgsr L220-223 (l > T)
+      vcycle(l, fview(l), /*entry=*/true);
     if (!final_done) {
       const Lvl& L = h->L[M];
       Launch g(h, st, KC_GATHER, M, w * 2.0 * h->blk_n[0] * (double)h->blk_n[1] * h->blk_n[2]);
@@ -835,6 +940,9 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->fused = !(fu && fu[0] == '0');
   const char* ff = std::getenv("SR_FMG_FORCE_FUSED");
   h->force = ff && ff[0] == '1';
+  const char* fp = std::getenv("SR_FMG_PASS");
+  h->pass = h->fused && !(fp && fp[0] == '0');
+  if (fp && (fp[0] == '1' || fp[0] == '3' || fp[0] == '4')) h->pass_entry = fp[0] - '0';
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {

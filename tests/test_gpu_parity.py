@@ -349,3 +349,57 @@ def test_fused_and_step_kernels_agree(dtype, force, monkeypatch):
     with Solver(n, 5, seg=16, buffer=2, K=3, dtype=dtype) as s:
         b = s.solve(ft).double().cpu().numpy()
     assert rel_l2(a, b) <= (1e-13 if dtype == "f64" else 1e-5)
+
+
+# ---- fused multi-stage SR passes (pass.cu): every FMG-entry variant, forced onto levels
+# that are too small to fill the GPU, against the oracle and against the unfused schedule
+PASS_CASES = [
+    # (name, n, M, seg, J, K, rhs): E = S_l + 2J + 2 in {70, 38} on the SR levels
+    ("K2-S64", (128, 128, 128), 6, 64, 2, 2, "manufactured+noise"),
+    ("K1-S64", (128, 128, 128), 6, 64, 2, 1, "bumps"),
+    ("K3-S64", (128, 128, 128), 6, 64, 2, 3, "manufactured+noise"),
+    ("noncubic-S64", (128, 64, 64), 5, 64, 2, 2, "random"),
+]
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "3", "4"])
+@pytest.mark.parametrize("case", PASS_CASES, ids=[c[0] for c in PASS_CASES])
+def test_fused_passes_match_oracle(case, mode, monkeypatch):
+    name, n, M, seg, J, K, rhs = case
+    f = W.make_rhs(rhs, n)
+    ref = _oracle(rhs, f, n, M, seg, J, K)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_PASS", mode)
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
+    assert rel_l2(u, ref) <= TOL64, (name, mode, rel_l2(u, ref))
+    monkeypatch.setenv("SR_FMG_PASS", "0")
+    monkeypatch.setenv("SR_FMG_FUSED", "0")
+    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
+    assert rel_l2(u, b) <= 1e-13, (name, mode, rel_l2(u, b))
+
+
+@pytest.mark.parametrize("mode", ["1", "4"])
+def test_fused_passes_fp32(mode, monkeypatch):
+    n, M, seg, J, K, rhs = (128, 128, 128), 6, 64, 2, 2, "manufactured+noise"
+    f = W.make_rhs(rhs, n)
+    ref = _oracle(rhs, f, n, M, seg, J, K)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_PASS", mode)
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype="f32")
+    assert rel_l2(u, ref) <= TOL32, rel_l2(u, ref)
+
+
+def test_fused_pass_launch_count(monkeypatch):
+    # C2-like level plan with passes on both SR levels: per SR level the FMG entry is one
+    # launch and every later visit two (down, up) instead of 2 + 2 + 2 (+prolong)
+    n = (128, 128, 128)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_PASS", "4")
+    with Solver(n, 6, seg=64, buffer=2, K=2) as s:
+        s.solve(torch.from_numpy(W.make_rhs("manufactured", n)).cuda())
+        fused = s.launches_per_solve
+    monkeypatch.setenv("SR_FMG_PASS", "0")
+    with Solver(n, 6, seg=64, buffer=2, K=2) as s:
+        s.solve(torch.from_numpy(W.make_rhs("manufactured", n)).cuda())
+        unfused = s.launches_per_solve
+    assert fused < unfused, (fused, unfused)
