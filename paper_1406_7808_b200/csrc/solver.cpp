@@ -85,9 +85,9 @@ struct sr_fmg {
   bool sync_debug = false;
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
   bool force = false; // SR_FMG_FORCE_FUSED=1: use them even on levels too small to fill the GPU
-  // fused multi-stage SR passes (pass.cu); SR_FMG_PASS=0 disables them.  pass_entry picks
-  // the FMG-entry chain: 4 = Pi+S1+S2+restrict, 3 = Pi+S1+S2 then restrict, 1 = Pi+S1
-  bool pass = true;
+  // fused multi-stage SR passes (pass.cu), SR_FMG_PASS=1|3|4.  pass_entry picks the
+  // FMG-entry chain: 4 = Pi+S1+S2+restrict, 3 = Pi+S1+S2 then restrict, 1 = Pi+S1
+  bool pass = false;
   int pass_entry = 4;
   int prof_cls = -1, prof_level = -1;
   std::vector<ProfRec> prof;
@@ -940,9 +940,10 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->fused = !(fu && fu[0] == '0');
   const char* ff = std::getenv("SR_FMG_FORCE_FUSED");
   h->force = ff && ff[0] == '1';
+  // fused passes: opt-in until they beat the separate kernels (SR_FMG_PASS=1|3|4)
   const char* fp = std::getenv("SR_FMG_PASS");
-  h->pass = h->fused && !(fp && fp[0] == '0');
-  if (fp && (fp[0] == '1' || fp[0] == '3' || fp[0] == '4')) h->pass_entry = fp[0] - '0';
+  h->pass = h->fused && fp && (fp[0] == '1' || fp[0] == '3' || fp[0] == '4');
+  if (h->pass) h->pass_entry = fp[0] - '0';
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {
