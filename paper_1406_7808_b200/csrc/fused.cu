@@ -262,9 +262,12 @@ struct SpecGeom {
   static constexpr int NG = (BH + 2 + MAXS - 1) / MAXS;
   static constexpr int NT = PY * NG;
   static constexpr int A = 128 / (int)sizeof(T);
-  static constexpr int U0S = ((BH + 4) * PY + A - 1) / A * A;
-  static constexpr int FS = ((BH + 2) * FP + A - 1) / A * A;
-  static constexpr int U1S = ((BH + 2) * PY + A - 1) / A * A;
+  // thread rows (NG * MAXS >= BH + 2): the branch-free plane steps read and write every
+  // thread row, so the buffers cover them all (+1 row above and below for u0)
+  static constexpr int TR = NG * MAXS;
+  static constexpr int U0S = ((TR + 2) * PY + A - 1) / A * A;
+  static constexpr int FS = (TR * FP + A - 1) / A * A;
+  static constexpr int U1S = ((TR + 2) * PY + A - 1) / A * A;
   static constexpr int RU = 3, RF = 4;
   static constexpr size_t SMEM = (size_t)(RU * U0S + RF * FS + 3 * U1S) * sizeof(T) + 8 * (RU + RF);
   static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the smem allows
@@ -311,7 +314,8 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
   auto issue_u0 = [=](int z) {
     const int sl = z % 3;
     mbar_expect_tx(&bars[sl], u0_bytes);
-    bulk_g2s(u0s + sl * G::U0S, useg + (long long)z * pz + (long long)q0 * PY, u0_bytes,
+    bulk_g2s(u0s + sl * G::U0S + (q0 - s0 + 1) * PY, useg + (long long)z * pz + (long long)q0 * PY,
+             u0_bytes,
              &bars[sl]);
   };
   auto issue_f = [=, &fmap](int z) {
@@ -349,9 +353,14 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
     if (in && y >= r0 && y < r1) w_mask |= 1u << k;
     yb_mask |= (unsigned)((gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0)) << (2 * k);
   }
-  const T* const u0b = u0s + (y0 - q0) * PY + tx;
+  // diagonal of A per slot (6 + reflected x/y neighbours, R3); the z part is per plane
+  T dk[MAXS];
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) dk[k] = T(6 + dxo) + T((yb_mask >> (2 * k)) & 3u);
+  // smem row = storage row - s0 + 1 (one margin row above every thread row, for u0 and u1)
+  const T* const u0b = u0s + (y0 - s0 + 1) * PY + tx;
   const T* const fb = fs + (y0 - s0) * G::FP + tx + fsh;
-  T* const u1b = u1s + (y0 - s0) * PY + tx;
+  T* const u1b = u1s + (y0 - s0 + 1) * PY + tx;
   T* const ob = oseg + (long long)y0 * PY + tx;
   T u0q[MAXS][3], u1q[MAXS][3];
   mbar_wait(&bars[0], 0);
@@ -377,30 +386,23 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
       T* u1w = u1b + R * G::U1S;
       const int gz = oz + z;
       const bool zc = gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2;
-      const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
-      if (z + 1 < Ez) {
+      const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+      // rows outside the loaded range hold stale smem: they only feed dead slots
 #pragma unroll
-        for (int k = 0; k < MAXS; ++k)
-          if ((ld_mask >> k) & 1u) u0q[k][IP] = pn[k * PY];
-      } else {
-#pragma unroll
-        for (int k = 0; k < MAXS; ++k) u0q[k][IP] = T(0);
-      }
+      for (int k = 0; k < MAXS; ++k) u0q[k][IP] = (z + 1 < Ez) ? pn[k * PY] : T(0);
+      const unsigned act = zc ? c_mask : 0u;
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
+        // branch-free: every slot computes, the C-cell predicate selects
         const T v0 = u0q[k][I0];
-        T v1 = v0;
-        if (zc && ((c_mask >> k) & 1u)) {
-          const T ym = (k == 0) ? pl[-PY] : u0q[k > 0 ? k - 1 : 0][I0];
-          const T yp = (k == MAXS - 1) ? pl[MAXS * PY] : u0q[k + 1 < MAXS ? k + 1 : k][I0];
-          const T sum = ((u0q[k][IM] + u0q[k][IP]) + (ym + yp)) + (pl[k * PY - 1] + pl[k * PY + 1]);
-          const T d = dg + T((yb_mask >> (2 * k)) & 3u);
-          const T r = fp[k * G::FP] - (d * v0 - sum) * ih2;
-          v1 = v0 + c0 * r;
-        }
+        const T ym = (k == 0) ? pl[-PY] : u0q[k > 0 ? k - 1 : 0][I0];
+        const T yp = (k == MAXS - 1) ? pl[MAXS * PY] : u0q[k + 1 < MAXS ? k + 1 : k][I0];
+        const T sum = ((u0q[k][IM] + u0q[k][IP]) + (ym + yp)) + (pl[k * PY - 1] + pl[k * PY + 1]);
+        const T r = fp[k * G::FP] - ((dk[k] + dz) * v0 - sum) * ih2;
+        const T v1 = ((act >> k) & 1u) ? v0 + c0 * r : v0;
         if constexpr (NST == 2) {
           u1q[k][I0] = v1;
-          if ((ex_mask >> k) & 1u) u1w[k * PY] = v1;
+          u1w[k * PY] = v1;
         } else {
           // degree 1: the first step is the result (C updated, GSR copied)
           if (((w_mask >> k) & 1u) && gz >= 0 && gz < L.N[2])
@@ -418,25 +420,22 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
       const int gz = oz + zz;
       if (gz >= 0 && gz < L.N[2]) {
         const bool zc = zz >= 1 && zz <= Ez - 2;
-        const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+        const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
         constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
         const T* u1r = u1b + J1 * G::U1S;
         const T* fp = fb + (zz & 3) * G::FS;
         T* orow = ob + (long long)zz * pz;
+        const unsigned act = zc ? c_mask : 0u;
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) {
-          if (!((w_mask >> k) & 1u)) continue;
           const T u0v = u0q[k][J1];
-          T v2 = u0v;
-          if (zc && ((c_mask >> k) & 1u)) {
-            const T c1 = u1q[k][J1];
-            const T ym = (k == 0) ? u1r[-PY] : u1q[k > 0 ? k - 1 : 0][J1];
-            const T yp = (k == MAXS - 1) ? u1r[MAXS * PY] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
-            const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
-            const T d = dg + T((yb_mask >> (2 * k)) & 3u);
-            const T r = fp[k * G::FP] - (d * c1 - sum) * ih2;
-            v2 = c1 + cm * (c1 - u0v) + cr * r;
-          }
+          const T c1 = u1q[k][J1];
+          const T ym = (k == 0) ? u1r[-PY] : u1q[k > 0 ? k - 1 : 0][J1];
+          const T yp = (k == MAXS - 1) ? u1r[MAXS * PY] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
+          const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
+          const T r = fp[k * G::FP] - ((dk[k] + dz) * c1 - sum) * ih2;
+          const T v2 = ((act >> k) & 1u) ? c1 + cm * (c1 - u0v) + cr * r : u0v;
+          if (!((w_mask >> k) & 1u)) continue;
           if constexpr (FIN == 0) {
             orow[k * PY] = v2;
           } else {
@@ -576,6 +575,7 @@ bool encode_rhs_map(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows) {
 template <class T, int PY, int BH, int MAXS>
 bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
   if (L.py != PY || L.E[0] > PY) return false;
+  if (SpecGeom<T, PY, BH, MAXS, 1>::SMEM > 227 * 1024) return false;
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   dim3 grid((L.E[1] + BH - 1) / BH, L.nsegs);
@@ -610,7 +610,7 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
   if constexpr (sizeof(T) == 8) {
     // default for the two-sweep pass at E = 70: 5 bands of 14 rows, 2 CTAs per SM
     // (measured 0.82 vs 0.845 ms for 2 bands of 35 at C3's finest level)
-    if (alt == 1 && nst == 2 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
+    if (alt == 1 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
     if (alt == 2 && try_spec<T, 72, 18, 4>(L, a, b, nst, st)) return true;
     if (alt == 3 && try_spec<T, 72, 24, 4>(L, a, b, nst, st)) return true;
   }

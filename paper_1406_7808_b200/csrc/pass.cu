@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
   const bool xin = colok && gx >= 0 && gx < L.N[0];
   const bool xc = tx >= 1 && tx <= Ex - 2;
   const T six = T(6 + (gx == 0 ? 1 : 0) + (gx == L.N[0] - 1 ? 1 : 0));
-  unsigned ldm = 0, inm = 0, cmk = 0, wmk = 0, ydg = 0;
+  unsigned inm = 0, cmk = 0, wmk = 0, ydg = 0;
   unsigned vm[NS + 1];
 #pragma unroll
   for (int j = 0; j <= NS; ++j) vm[j] = 0;
@@ -228,7 +228,6 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
     const int y = y0 + k, gy = oy + y;
     const bool rowin = y >= 0 && y < Ey;
     const bool in = xin && rowin && gy >= 0 && gy < L.N[1];
-    if (colok && rowin) ldm |= 1u << k;
     if (in) inm |= 1u << k;
     if (in && xc && y >= 1 && y <= Ey - 2) cmk |= 1u << k;
     if (in && y >= r0 && y < r1) wmk |= 1u << k;
@@ -237,6 +236,11 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
     for (int j = 0; j <= NS; ++j)
       if (y >= r0 - (NS - j) && y < r1 + (NS - j)) vm[j] |= 1u << k;
   }
+  // diagonal of A per slot: 6 + one per reflected (out-of-domain) x/y neighbour (R3);
+  // the z part is added per plane
+  T dk[MAXS];
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) dk[k] = six + T((ydg >> (2 * k)) & 3u);
   const int po = (g * MAXS + 1) * PY + tx;  // own row 0 in a stage plane
   const int fo = g * MAXS * G::FPI + tx + fsh;
   const T ih2 = T(L.inv_h2);
@@ -289,6 +293,20 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
     for (int k = 0; k < MAXS; ++k) I[k] = W0 * xi[k / 2 + 1] + W1 * xi[(k & 1) ? k / 2 + 2 : k / 2];
   };
 
+  // I(c) with the reflected coarse ghost planes I(-1) = -I(0), I(Nc) = -I(Nc-1) (R3)
+  auto get_c = [&](int c, T (&I)[MAXS]) {
+    const int cc = min(max(c, 0), Lc.N[2] - 1);
+    wait_c(cc);
+    interp(cc, I);
+    if (cc != c) {
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) I[k] = -I[k];
+    }
+  };
+  T Iprev[MAXS], Icur[MAXS];
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) Iprev[k] = Icur[k] = T(0);
+
   // restriction target box (coarse global indices): F of half-width jr around V_{l-1}^p
   bool rx = false;
   unsigned ryk = 0;
@@ -334,33 +352,40 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) pv[k] = T(0);
       if constexpr (COARSE) {
+        // the xy-interpolant of every coarse plane is formed once and kept in registers:
+        // fine plane 2P uses I(P), I(P-1); fine plane 2P+1 uses I(P), I(P+1)
         if (zin) {
           const int P = gz >> 1;
-          int Q = P + ((gz & 1) ? 1 : -1);
-          T wq = W1;
-          if (Q < 0) { Q = 0; wq = -W1; }
-          if (Q >= Lc.N[2]) { Q = Lc.N[2] - 1; wq = -W1; }
-          wait_c(P);
-          wait_c(Q);
-          T IP[MAXS], IQ[MAXS];
-          interp(P, IP);
-          interp(Q, IQ);
+          if (gz == max(oz, 0)) {  // first in-domain plane of the segment
+            get_c(P, Icur);
+            if (!(gz & 1)) get_c(P - 1, Iprev);
+          }
+          if (gz & 1) {
+            T In[MAXS];
+            get_c(P + 1, In);
 #pragma unroll
-          for (int k = 0; k < MAXS; ++k) pv[k] = W0 * IP[k] + wq * IQ[k];
+            for (int k = 0; k < MAXS; ++k) {
+              pv[k] = W0 * Icur[k] + W1 * In[k];
+              Iprev[k] = Icur[k];
+              Icur[k] = In[k];
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < MAXS; ++k) pv[k] = W0 * Icur[k] + W1 * Iprev[k];
+          }
         }
       }
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
         T v = T(0);
-        if constexpr (RING) v = ((ldm >> k) & 1u) ? up[k * PY] : T(0);
+        if constexpr (RING) v = up[k * PY];
         if constexpr (COARSE) {
-          if (zin && ((inm >> k) & 1u)) v = (SRC == kSrcPadd) ? v + pv[k] : pv[k];
+          const bool in = zin && ((inm >> k) & 1u);
+          const T pw = (SRC == kSrcPadd) ? v + pv[k] : pv[k];
+          v = in ? pw : v;
         }
         q[0][k][R] = v;
-        if constexpr (SRC == kSrcPadd) {
-          if (zin && ((inm >> k) & 1u)) up[k * PY] = v;
-        }
-        if constexpr (SRC == kSrcPset) up[k * PY] = v;
+        if constexpr (SRC != kSrcLoad) up[k * PY] = v;
       }
     }
     // ------------------------------------------------------------ steps j = 1..NSTEP
@@ -372,7 +397,7 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
       if (j == 1) mbar_wait(&barF[zj % G::RF], (zj / G::RF) & 1);
       const int gz = oz + zj;
       const bool zc = zj >= 1 && zj <= Ez - 2 && gz >= 0 && gz < L.N[2];
-      const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+      const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
       const T* src;
       if constexpr (j == 1)
         src = bufU + (RING ? (zj % G::RU) : (zj & 1)) * G::PL + po;
@@ -384,20 +409,20 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
       const unsigned act = zc ? (cmk & vm[j]) : 0u;
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
+        // branch-free: every slot computes, the C-cell predicate selects (GSR, dead rows
+        // and out-of-domain cells carry their value through)
         const T v = q[j - 1][k][I0];
-        T o = v;
-        if ((act >> k) & 1u) {
-          const T ym = (k == 0) ? src[-PY] : q[j - 1][k > 0 ? k - 1 : 0][I0];
-          const T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[j - 1][k + 1 < MAXS ? k + 1 : k][I0];
-          const T sum = ((q[j - 1][k][IM] + q[j - 1][k][IP]) + (ym + yp)) +
-                        (src[k * PY - 1] + src[k * PY + 1]);
-          const T d = dg + T((ydg >> (2 * k)) & 3u);
-          const T r = fp[k * G::FPI] - (d * v - sum) * ih2;
-          if constexpr (j == NSTEP && NSTEP >= 2)
-            o = v + a.cm * (v - q[j - 2][k][I0]) + a.cr[j - 1] * r;
-          else
-            o = v + a.cr[j - 1] * r;
-        }
+        const T ym = (k == 0) ? src[-PY] : q[j - 1][k > 0 ? k - 1 : 0][I0];
+        const T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[j - 1][k + 1 < MAXS ? k + 1 : k][I0];
+        const T sum = ((q[j - 1][k][IM] + q[j - 1][k][IP]) + (ym + yp)) +
+                      (src[k * PY - 1] + src[k * PY + 1]);
+        const T r = fp[k * G::FPI] - ((dk[k] + dz) * v - sum) * ih2;
+        T o;
+        if constexpr (j == NSTEP && NSTEP >= 2)
+          o = v + a.cm * (v - q[j - 2][k][I0]) + a.cr[j - 1] * r;
+        else
+          o = v + a.cr[j - 1] * r;
+        o = ((act >> k) & 1u) ? o : v;
         q[j][k][I0] = o;
         if constexpr (STAGED) dst[k * PY] = o;
       }
@@ -433,23 +458,20 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
         constexpr int I0 = ((R - NS) % 3 + 3) % 3, IM = (I0 + 2) % 3, IP = (I0 + 1) % 3;
         const int gz = oz + zr;
         const bool zc = zr >= 1 && zr <= Ez - 2 && gz >= 0 && gz < L.N[2];
-        const T dg = six + T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
+        const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
         const T* src = bufS + (2 * (NSTEP - 1) + (zr & 1)) * G::PL + po;
         const T* fp = bufF + (zr % G::RF) * G::FPL + fo;
         const unsigned act = zc ? (cmk & vm[NS]) : 0u;
         T rv[MAXS];
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) {
-          rv[k] = T(0);
-          if ((act >> k) & 1u) {
-            const T v = q[NSTEP][k][I0];
-            const T ym = (k == 0) ? src[-PY] : q[NSTEP][k > 0 ? k - 1 : 0][I0];
-            const T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[NSTEP][k + 1 < MAXS ? k + 1 : k][I0];
-            const T sum = ((q[NSTEP][k][IM] + q[NSTEP][k][IP]) + (ym + yp)) +
-                          (src[k * PY - 1] + src[k * PY + 1]);
-            const T d = dg + T((ydg >> (2 * k)) & 3u);
-            rv[k] = fp[k * G::FPI] - (d * v - sum) * ih2;
-          }
+          const T v = q[NSTEP][k][I0];
+          const T ym = (k == 0) ? src[-PY] : q[NSTEP][k > 0 ? k - 1 : 0][I0];
+          const T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[NSTEP][k + 1 < MAXS ? k + 1 : k][I0];
+          const T sum = ((q[NSTEP][k][IM] + q[NSTEP][k][IP]) + (ym + yp)) +
+                        (src[k * PY - 1] + src[k * PY + 1]);
+          const T r = fp[k * G::FPI] - ((dk[k] + dz) * v - sum) * ih2;
+          rv[k] = ((act >> k) & 1u) ? r : T(0);
         }
         const bool zodd = (gz & 1) != 0;
         const int Z = gz >> 1;
@@ -588,8 +610,9 @@ int max_py() {
 template <class T, int SRC, int NSTEP, int SINK, int RG>
 bool by_geom(const PassSpec<T>& ps, cudaStream_t st, bool launch) {
   if (ps.L.py > max_py()) return false;
-  return inst<T, 72, 14, 4, SRC, NSTEP, SINK, RG>(ps, st, launch) ||
-         inst<T, 40, 12, 4, SRC, NSTEP, SINK, RG>(ps, st, launch);
+  // only the E = 70 geometry (64^3 segments, J = 2): on smaller boxes the band halos and
+  // the low occupancy make the fused pass slower than the separate kernels (measured)
+  return inst<T, 72, 14, 4, SRC, NSTEP, SINK, RG>(ps, st, launch);
 }
 
 template <class T>

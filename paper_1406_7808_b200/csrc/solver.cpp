@@ -88,7 +88,9 @@ struct sr_fmg {
   // fused multi-stage SR passes (pass.cu), SR_FMG_PASS=1|3|4.  pass_entry picks the
   // FMG-entry chain: 4 = Pi+S1+S2+restrict, 3 = Pi+S1+S2 then restrict, 1 = Pi+S1
   bool pass = false;
-  int pass_entry = 4;
+  int pass_entry = 0;      // 0: unfused entry
+  bool pass_down = false;  // (LOAD, 2, RESTRICT)
+  bool pass_up = false;    // (PADD, 2, STORE|FINAL)
   int prof_cls = -1, prof_level = -1;
   std::vector<ProfRec> prof;
   size_t prof_used = 0;
@@ -672,7 +674,7 @@ struct Schedule {
       }
     }
     if (!restricted) {
-      if (pass_on(l, kSrcLoad, 2, kSinkRestrict, b)) {
+      if (h->pass_down && pass_on(l, kSrcLoad, 2, kSinkRestrict, b)) {
         run_pass(l, kSrcLoad, 2, kSinkRestrict, b);  // L112-115 / L232-235 in one pass
       } else {
         cheb(l, h->d.nu1, b);  // L112 / L232
@@ -689,9 +691,9 @@ struct Schedule {
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
     const bool last = l == h->M && final_out != nullptr;
-    if (last && pass_on(l, kSrcPadd, 2, kSinkFinal, b)) {
+    if (h->pass_up && last && pass_on(l, kSrcPadd, 2, kSinkFinal, b)) {
       run_pass(l, kSrcPadd, 2, kSinkFinal, b);  // L241-242, genuine cells -> user u (R19)
-    } else if (!last && pass_on(l, kSrcPadd, 2, kSinkStore, b)) {
+    } else if (h->pass_up && !last && pass_on(l, kSrcPadd, 2, kSinkStore, b)) {
       run_pass(l, kSrcPadd, 2, kSinkStore, b);  // L241-242 in one pass
     } else {
       prolong(l, 1);                    // L118 / L241
@@ -940,10 +942,17 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->fused = !(fu && fu[0] == '0');
   const char* ff = std::getenv("SR_FMG_FORCE_FUSED");
   h->force = ff && ff[0] == '1';
-  // fused passes: opt-in until they beat the separate kernels (SR_FMG_PASS=1|3|4)
+  // fused passes: opt-in until they beat the separate kernels.  SR_FMG_PASS=1|3|4 turns on
+  // all three kinds with that entry chain; SR_FMG_PASS_{ENTRY,DOWN,UP} override per kind
   const char* fp = std::getenv("SR_FMG_PASS");
-  h->pass = h->fused && fp && (fp[0] == '1' || fp[0] == '3' || fp[0] == '4');
-  if (h->pass) h->pass_entry = fp[0] - '0';
+  const bool all = fp && (fp[0] == '1' || fp[0] == '3' || fp[0] == '4');
+  h->pass_entry = all ? fp[0] - '0' : 0;
+  h->pass_down = all;
+  h->pass_up = all;
+  if (const char* e = std::getenv("SR_FMG_PASS_ENTRY")) h->pass_entry = std::atoi(e);
+  if (const char* e = std::getenv("SR_FMG_PASS_DOWN")) h->pass_down = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_PASS_UP")) h->pass_up = std::atoi(e) != 0;
+  h->pass = h->fused && (h->pass_entry || h->pass_down || h->pass_up);
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {
