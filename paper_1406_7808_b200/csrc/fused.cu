@@ -270,7 +270,8 @@ struct SpecGeom {
   static constexpr int U1S = ((TR + 2) * PY + A - 1) / A * A;
   static constexpr int RU = 3, RF = 4;
   static constexpr size_t SMEM = (size_t)(RU * U0S + RF * FS + 3 * U1S) * sizeof(T) + 8 * (RU + RF);
-  static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the smem allows
+  // CTAs per SM the smem allows (capped at 3: registers)
+  static constexpr int MINB = SMEM <= 75 * 1024 ? 3 : SMEM <= 113 * 1024 ? 2 : 1;
 };
 
 template <class T, int PY, int BH, int MAXS, int RG, int NST, int FIN = 0>
@@ -607,13 +608,11 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
     const char* e = std::getenv("SR_FMG_CHEB2_ALT");
     alt = e ? std::atoi(e) : 1;
   }
-  if constexpr (sizeof(T) == 8) {
-    // default for the two-sweep pass at E = 70: 5 bands of 14 rows, 2 CTAs per SM
-    // (measured 0.82 vs 0.845 ms for 2 bands of 35 at C3's finest level)
-    if (alt == 1 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
-    if (alt == 2 && try_spec<T, 72, 18, 4>(L, a, b, nst, st)) return true;
-    if (alt == 3 && try_spec<T, 72, 24, 4>(L, a, b, nst, st)) return true;
-  }
+  // E = 70 (64^3 segments, J = 2): 5 bands of 14 rows, 2+ CTAs per SM by default (fp64:
+  // 0.77 vs 0.85 ms for 2 bands of 35 at C3's finest level); SR_FMG_CHEB2_ALT picks others
+  if (alt == 1 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
+  if (alt == 2 && try_spec<T, 72, 18, 4>(L, a, b, nst, st)) return true;
+  if (alt == 3 && try_spec<T, 72, 24, 4>(L, a, b, nst, st)) return true;
   if constexpr (sizeof(T) == 8)
     return try_spec<T, 72, 35, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
            try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);
