@@ -12,8 +12,8 @@ namespace srfmg {
 
 const char* const kKernelNames[] = {"k_cheb_step", "k_restrict", "k_tau",     "k_prolong",
                                     "k_coarsest",  "k_pyramid",  "k_gather",  "k_cheb2",
-                                    "k_pass_entry", "k_pass_down", "k_pass_up"};
-const int kNumKernelNames = 11;
+                                    "k_pass_entry", "k_pass_down", "k_pass_up", "k_coarse"};
+const int kNumKernelNames = 12;
 
 namespace {
 

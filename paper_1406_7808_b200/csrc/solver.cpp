@@ -17,6 +17,7 @@
 
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "coarse.cuh"
 #include "pass.cuh"
 #include "sr_fmg.h"
 
@@ -29,7 +30,8 @@ thread_local std::string g_tls_err = "no error";
 
 // indices into srfmg::kKernelNames (sr_fmg_kernel_name)
 enum KernelClass { KC_CHEB = 0, KC_RESTRICT, KC_TAU, KC_PROLONG, KC_COARSEST, KC_PYRAMID,
-                   KC_GATHER, KC_CHEB_FUSED, KC_PASS_ENTRY, KC_PASS_DOWN, KC_PASS_UP, KC_COUNT };
+                   KC_GATHER, KC_CHEB_FUSED, KC_PASS_ENTRY, KC_PASS_DOWN, KC_PASS_UP, KC_COARSE,
+                   KC_COUNT };
 
 struct LevelBufs {
   void* u[2] = {nullptr, nullptr};  // two solution buffers (Chebyshev ping-pong)
@@ -91,6 +93,11 @@ struct sr_fmg {
   int pass_entry = 0;      // 0: unfused entry
   bool pass_down = false;  // (LOAD, 2, RESTRICT)
   bool pass_up = false;    // (PADD, 2, STORE|FINAL)
+  // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
+  // disables it.  flush_fn: enqueue the recorded operations (called before every launch)
+  bool cexec = true;
+  void (*flush_fn)(void*) = nullptr;
+  void* flush_ctx = nullptr;
   int prof_cls = -1, prof_level = -1;
   std::vector<ProfRec> prof;
   size_t prof_used = 0;
@@ -338,6 +345,7 @@ struct Launch {
   cudaStream_t st;
   ProfRec* rec = nullptr;
   Launch(sr_fmg* h_, cudaStream_t st_, int cls, int level, double bytes) : h(h_), st(st_) {
+    if (h->flush_fn) h->flush_fn(h->flush_ctx);  // recorded coarse-level operations first
     h->launches++;
     if (cls == h->prof_cls && level == h->prof_level) {
       if (h->prof_used == h->prof.size()) {
@@ -427,6 +435,52 @@ struct Schedule {
     return v;
   }
 
+  // ---- coarse-level executor: operations on small conventional levels are recorded and
+  // enqueued as one cluster launch right before the next ordinary launch (Launch ctor)
+  srfmg::COpList<T> cops{};
+  bool flushing = false;
+  int cops_top = 0;
+  double cops_bytes = 0;
+  bool cx(int l) const { return h->cexec && srfmg::coarse_level_ok(h->L[l]); }
+  void emit(const srfmg::COp<T>& o, double bytes) {
+    if (cops.n == srfmg::kCoarseMaxOps) flush();
+    if (cops.n == 0) {
+      for (int i = 0; i <= std::min(h->M, srfmg::kCoarseMaxLevels - 1); ++i) cops.L[i] = h->L[i];
+      cops_top = 0;
+      cops_bytes = 0;
+    }
+    cops.op[cops.n++] = o;
+    cops_top = std::max(cops_top, o.lf);
+    cops_bytes += bytes;
+  }
+  void flush() {
+    if (cops.n == 0 || flushing) return;
+    flushing = true;
+    {
+      Launch g(h, st, KC_COARSE, cops_top, cops_bytes);
+      srfmg::launch_coarse_exec<T>(cops, st);
+    }
+    cops.n = 0;
+    flushing = false;
+  }
+  static void flush_cb(void* p) { static_cast<Schedule*>(p)->flush(); }
+  void bind() {
+    h->flush_fn = &Schedule::flush_cb;
+    h->flush_ctx = this;
+  }
+  void unbind() {
+    flush();
+    h->flush_fn = nullptr;
+    h->flush_ctx = nullptr;
+  }
+  static srfmg::COp<T> cop(int code, int lf, int lc) {
+    srfmg::COp<T> o{};
+    o.code = code;
+    o.lf = lf;
+    o.lc = lc;
+    return o;
+  }
+
   // S^deg(L_l, u_l, b) on C_l of every segment (R8): ping-pong between the two buffers
   T* final_out = nullptr;  // user u: the last level-M smoothing writes it directly (R19)
   bool final_done = false;
@@ -471,6 +525,29 @@ struct Schedule {
       return;
     }
     int lat = bb.cur, oth = 1 - bb.cur;
+    if (cx(l)) {  // recorded for the coarse-level executor (same steps, same ping-pong)
+      double rho_prev = 1.0 / h->sigma[l];
+      for (int k = 0; k < deg; ++k) {
+        srfmg::COp<T> o = cop(srfmg::kCopCheb, l, l);
+        o.a = (const T*)bb.u[lat];
+        o.b = k == 0 ? nullptr : (const T*)bb.u[oth];
+        o.c = (T*)bb.u[oth];
+        o.v = b;
+        if (k == 0) {
+          o.c0 = 0.0;
+          o.c1 = 1.0 / h->theta[l];
+        } else {
+          const double rho = 1.0 / (2.0 * h->sigma[l] - rho_prev);
+          o.c0 = rho * rho_prev;
+          o.c1 = 2.0 * rho / h->delta[l];
+          rho_prev = rho;
+        }
+        emit(o, w * (k == 0 ? 3.0 : 4.0) * c.compute);
+        std::swap(lat, oth);
+      }
+      bb.cur = lat;
+      return;
+    }
     {
       Launch g(h, st, KC_CHEB, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb_step<T>(L, (const T*)bb.u[lat], nullptr, b, (T*)bb.u[oth], 0.0,
@@ -497,12 +574,29 @@ struct Schedule {
   }
 
   void coarsest(View<T> b) {
+    if (cx(0)) {
+      srfmg::COp<T> o = cop(srfmg::kCopCoarsest, 0, 0);
+      o.a = (const T*)h->ainv;
+      o.c = U(0);
+      o.v = b;
+      emit(o, 0.0);
+      return;
+    }
     Launch g(h, st, KC_COARSEST, 0, 0.0);
     srfmg::launch_coarsest<T>(h->L[0], U(0), b, (const T*)h->ainv, st);
   }
 
   void prolong(int l, int add) {
     const CellCounts& c = h->cells[l];
+    if (cx(l) && cx(l - 1)) {
+      srfmg::COp<T> o = cop(srfmg::kCopProlong, l, l - 1);
+      o.flag = add;
+      o.a = U(l - 1);
+      o.b = (const T*)h->B[l - 1].t;
+      o.c = U(l);
+      emit(o, w * (add ? 2.0 : 1.0) * c.cg);
+      return;
+    }
     Launch g(h, st, KC_PROLONG, l,
              w * (add ? 2.0 : 1.0) * c.cg + w * (add ? 2.0 : 1.0) * h->cells[l - 1].cg / 8.0);
     if (h->fused && (h->force || srfmg::prolong_tma_ok<T>(h->L[l], h->L[l - 1])))
@@ -523,6 +617,7 @@ struct Schedule {
   // fields: (base, sy, sz) strided arrays holding level T (index = global cell)
   void exchange(int nf, T* const* base, const long long* sy, const long long* sz,
                 const int* own_lo) {
+    flush();
     const long long nb = (long long)h->blkT_n[0] * h->blkT_n[1] * h->blkT_n[2];
     T* snd = (T*)h->xsend;
     T* rcv = (T*)h->xrecv;
@@ -543,6 +638,7 @@ struct Schedule {
     }
   }
   void exchange_fT() {  // the rank's block of f_T (interior of its haloed local f_T)
+    flush();
     const int HT = h->H[h->T];
     const auto& d = h->fdim[h->T];
     const int own[3] = {HT, HT, HT};
@@ -639,6 +735,15 @@ struct Schedule {
 
   void restrict_std(int l, View<T> b) {
     const int jr = jr_for(l);
+    if (cx(l) && cx(l - 1)) {
+      srfmg::COp<T> o = cop(srfmg::kCopRestrict, l, l - 1);
+      o.a = U(l);
+      o.c = U(l - 1);
+      o.d = (T*)h->B[l - 1].rhs;
+      o.v = b;
+      emit(o, w * 2.25 * h->cells[l].compute);
+      return;
+    }
     const Lvl& Lf = h->L[l];
     double tgt = h->L[l].nsegs;
     for (int i = 0; i < 3; ++i) tgt *= (Lf.S[i] / 2 + 2 * jr);
@@ -683,7 +788,13 @@ struct Schedule {
     }
     const int jr = jr_for(l);
     if (h->world > 1 && l - 1 == h->T) exchange_uT();  // a8: level-T hand-off (R16)
-    {
+    if (cx(l - 1)) {  // conventional level: F = V = Omega (jr = 0)
+      srfmg::COp<T> o = cop(srfmg::kCopTau, l - 1, l - 1);
+      o.a = U(l - 1);
+      o.c = (T*)h->B[l - 1].rhs;
+      o.d = (T*)h->B[l - 1].t;
+      emit(o, w * 4.0 * h->cells[l - 1].compute);
+    } else {
       const CellCounts& c = h->cells[l - 1];
       Launch g(h, st, KC_TAU, l - 1, w * (2.0 * c.storage + 2.0 * c.compute));
       srfmg::launch_tau<T>(h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, (T*)h->B[l - 1].t, jr,
@@ -702,6 +813,11 @@ struct Schedule {
   }
 
   void run(T* uout) {
+    bind();
+    run_body(uout);
+    unbind();
+  }
+  void run_body(T* uout) {
     const int M = h->M;
     final_out = uout;
     final_done = false;
@@ -717,6 +833,13 @@ struct Schedule {
     if (h->world > 1) exchange_fT();
     for (int l = h->T; l >= 1; --l) {
       const Lvl& L = h->L[l];
+      if (l < M && cx(l)) {
+        srfmg::COp<T> o = cop(srfmg::kCopPyramid, l, l - 1);
+        o.a = (const T*)h->B[l].fpyr;
+        o.c = (T*)h->B[l - 1].fpyr;
+        emit(o, w * (double)L.N[0] * L.N[1] * L.N[2] * (1.0 + 1.0 / 8));
+        continue;
+      }
       Launch g(h, st, KC_PYRAMID, l, w * (double)L.N[0] * L.N[1] * L.N[2] * (1.0 + 1.0 / 8));
       srfmg::launch_pyramid<T>(l == M ? f : (const T*)h->B[l].fpyr, L.N[0], L.N[1], L.N[2],
                                (T*)h->B[l - 1].fpyr, st);
@@ -944,6 +1067,8 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->force = ff && ff[0] == '1';
   // fused passes: opt-in until they beat the separate kernels.  SR_FMG_PASS=1|3|4 turns on
   // all three kinds with that entry chain; SR_FMG_PASS_{ENTRY,DOWN,UP} override per kind
+  const char* ce = std::getenv("SR_FMG_CEXEC");
+  h->cexec = !(ce && ce[0] == '0');
   const char* fp = std::getenv("SR_FMG_PASS");
   const bool all = fp && (fp[0] == '1' || fp[0] == '3' || fp[0] == '4');
   h->pass_entry = all ? fp[0] - '0' : 0;
@@ -1270,6 +1395,7 @@ sr_status_t sr_fmg_debug_op(sr_fmg_t* h, int32_t op, int32_t level, int32_t deg,
     using T = decltype(tag);
     Schedule<T> s{h, st, (const T*)f_dev, (double)sizeof(T)};
     auto rhs = [&](int l) { return (l == h->M) ? s.fview(l) : s.sview(l); };
+    s.bind();
     switch (op) {
       case 0: s.cheb(level, deg, rhs(level)); break;
       case 1:
@@ -1283,8 +1409,9 @@ sr_status_t sr_fmg_debug_op(sr_fmg_t* h, int32_t op, int32_t level, int32_t deg,
       case 3: s.prolong(level, 0); break;
       case 4: s.prolong(level, 1); break;
       case 5: s.coarsest(s.sview(0)); break;
-      default: return fail(h, SR_ERR_INVALID_ARGUMENT, "unknown op");
+      default: s.unbind(); return fail(h, SR_ERR_INVALID_ARGUMENT, "unknown op");
     }
+    s.unbind();
     return SR_OK;
   };
   if (op == 0 && level == h->M && !f_dev)
