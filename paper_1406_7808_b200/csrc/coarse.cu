@@ -21,8 +21,8 @@ namespace srfmg {
 
 namespace {
 
-constexpr int kCluster = 8;
-constexpr int kThreadsC = 1024;
+constexpr int kCluster = 16;  // non-portable cluster size (B200 allows 16)
+constexpr int kThreadsC = 512;
 
 template <class T>
 __device__ __forceinline__ long long soff(const Lvl& L, int x, int y, int z) {
@@ -50,102 +50,148 @@ __device__ __forceinline__ T apply_A(const Lvl& L, const T* __restrict__ u, long
   return (T(6) * c - s) * T(L.inv_h2);
 }
 
-__device__ __forceinline__ void cell_of(long long i, const int n[3], int& x, int& y, int& z) {
-  x = (int)(i % n[0]);
-  const long long r = i / n[0];
-  y = (int)(r % n[1]);
-  z = (int)(r / n[1]);
+__device__ __forceinline__ void cell_of(int i, const int n[3], int& x, int& y, int& z) {
+  x = i % n[0];
+  const int r = i / n[0];
+  y = r % n[1];
+  z = r / n[1];
 }
 
-template <class T>
-__device__ void op_cheb(const Lvl& L, const COp<T>& o, int tid, int nth) {
-  const long long n = (long long)L.N[0] * L.N[1] * L.N[2];
+// Thread layout of every operation: thread t owns the (x, y) column t % ncol and the z
+// chunk t / ncol of ceil(nz / nchunk) planes (nchunk = max(1, nth / ncol)); the column's
+// z-neighbours stay in registers and all loads of a chunk are issued before the arithmetic.
+struct ColMap {
+  int x, y, z0, z1;
+  bool ok;
+};
+__device__ __forceinline__ ColMap col_map(int nx, int ny, int nz, int tid, int nth) {
+  ColMap m;
+  const int ncol = nx * ny;
+  const int nch = max(1, min(nz, nth / ncol));
+  const int per = (nz + nch - 1) / nch;
+  const int col = tid % ncol, ch = tid / ncol;
+  m.x = col % nx;
+  m.y = col / nx;
+  m.z0 = ch * per;
+  m.z1 = min(nz, m.z0 + per);
+  m.ok = tid < ncol * nch && m.z0 < m.z1;
+  return m;
+}
+constexpr int kZC = 4;  // planes per register batch (longer chunks loop; 64 registers)
+
+// CHEB (c_mom == 0 and prev == null: first step) and TAU share the column sweep:
+// storage ghosts are zero, so the reflected ghost -u_i is +1 on the diagonal (R3)
+template <class T, bool TAU>
+__device__ void op_column(const Lvl& L, const COp<T>& o, int tid, int nth) {
+  const ColMap m = col_map(L.N[0], L.N[1], L.N[2], tid, nth);
+  if (!m.ok) return;
   const T cm = T(o.c0), cr = T(o.c1);
-  for (long long i = tid; i < n; i += nth) {
-    int x, y, z;
-    cell_of(i, L.N, x, y, z);
-    const long long off = soff<T>(L, x, y, z);
-    const T c = o.a[off];
-    const T r = rhs_at(o.v, x, y, z) - apply_A(L, o.a, off, x, y, z);
-    T v = c + cr * r;
-    if (o.b) v = c + cm * (c - o.b[off]) + cr * r;
-    o.c[off] = v;
+  const bool xm = m.x > 0, xp = m.x < L.N[0] - 1, ym = m.y > 0, yp = m.y < L.N[1] - 1;
+  const T dxy = T(6 + !xm + !xp + !ym + !yp);
+  for (int zb = m.z0; zb < m.z1; zb += kZC) {
+    const int ze = min(m.z1, zb + kZC);
+    T q[kZC + 2], nb[kZC], bv[kZC], pv[kZC];
+    const long long c0 = soff<T>(L, m.x, m.y, zb);
+#pragma unroll
+    for (int k = 0; k < kZC + 2; ++k)  // planes zb-1 .. zb+kZC (ghost planes are zero)
+      q[k] = (zb - 1 + k <= ze) ? o.a[c0 + (long long)(k - 1) * L.pz] : T(0);
+#pragma unroll
+    for (int k = 0; k < kZC; ++k) {
+      if (zb + k >= ze) break;
+      const long long off = c0 + (long long)k * L.pz;
+      nb[k] = ((ym ? o.a[off - L.py] : T(0)) + (yp ? o.a[off + L.py] : T(0))) +
+              ((xm ? o.a[off - 1] : T(0)) + (xp ? o.a[off + 1] : T(0)));
+      if constexpr (TAU) {
+        bv[k] = o.c[off];
+      } else {
+        bv[k] = rhs_at(o.v, m.x, m.y, zb + k);
+        pv[k] = o.b ? o.b[off] : T(0);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kZC; ++k) {
+      const int z = zb + k;
+      if (z >= ze) break;
+      const T d = dxy + T((z == 0 ? 1 : 0) + (z == L.N[2] - 1 ? 1 : 0));
+      const T c = q[k + 1];
+      const T Au = (d * c - ((q[k] + q[k + 2]) + nb[k])) * T(L.inv_h2);
+      const long long off = c0 + (long long)k * L.pz;
+      if constexpr (TAU) {
+        o.d[off] = c;           // t = u
+        o.c[off] = bv[k] + Au;  // rhs = R + A u
+      } else {
+        const T r = bv[k] - Au;
+        o.c[off] = o.b ? c + cm * (c - pv[k]) + cr * r : c + cr * r;
+      }
+    }
   }
 }
 
+// RESTRICT: eight lanes per coarse cell, one fine child each (residual of the child with all
+// its loads in flight at once), reduced with three butterfly shuffles
 template <class T>
 __device__ void op_restrict(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int tid, int nth) {
-  const long long n = (long long)Lc.N[0] * Lc.N[1] * Lc.N[2];
-  for (long long i = tid; i < n; i += nth) {
+  const int n = Lc.N[0] * Lc.N[1] * Lc.N[2];
+  const int ch = tid & 7;
+  const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
+  for (int base = tid - ch; base < 8 * n; base += nth) {  // warp-uniform trip count
+    const int c = base >> 3;
+    const bool ok = c < n;
     int X, Y, Z;
-    cell_of(i, Lc.N, X, Y, Z);
-    T su = T(0), sr = T(0);
+    cell_of(ok ? c : n - 1, Lc.N, X, Y, Z);
+    const int x = 2 * X + dx, y = 2 * Y + dy, z = 2 * Z + dz;
+    const long long off = soff<T>(Lf, x, y, z);
+    T su = o.a[off];
+    T sr = rhs_at(o.v, x, y, z) - apply_A(Lf, o.a, off, x, y, z);
 #pragma unroll
-    for (int dz = 0; dz < 2; ++dz)
-#pragma unroll
-      for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 2; ++dx) {
-          const int x = 2 * X + dx, y = 2 * Y + dy, z = 2 * Z + dz;
-          const long long off = soff<T>(Lf, x, y, z);
-          su += o.a[off];
-          sr += rhs_at(o.v, x, y, z) - apply_A(Lf, o.a, off, x, y, z);
-        }
-    const long long co = soff<T>(Lc, X, Y, Z);
-    o.c[co] = su * T(0.125);
-    o.d[co] = sr * T(0.125);
-  }
-}
-
-template <class T>
-__device__ void op_tau(const Lvl& L, const COp<T>& o, int tid, int nth) {
-  const long long n = (long long)L.N[0] * L.N[1] * L.N[2];
-  for (long long i = tid; i < n; i += nth) {
-    int x, y, z;
-    cell_of(i, L.N, x, y, z);
-    const long long off = soff<T>(L, x, y, z);
-    o.d[off] = o.a[off];
-    o.c[off] = o.c[off] + apply_A(L, o.a, off, x, y, z);
+    for (int m = 1; m < 8; m <<= 1) {
+      su += __shfl_xor_sync(0xffffffffu, su, m);
+      sr += __shfl_xor_sync(0xffffffffu, sr, m);
+    }
+    if (ok && ch == 0) {
+      const long long co = soff<T>(Lc, X, Y, Z);
+      o.c[co] = su * T(0.125);
+      o.d[co] = sr * T(0.125);
+    }
   }
 }
 
 template <class T>
 __device__ void op_prolong(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int tid, int nth) {
-  const long long n = (long long)Lf.N[0] * Lf.N[1] * Lf.N[2];
+  const ColMap m = col_map(Lf.N[0], Lf.N[1], Lf.N[2], tid, nth);
+  if (!m.ok) return;
   const T W0 = T(0.75), W1 = T(0.25);
-  for (long long i = tid; i < n; i += nth) {
-    int x, y, z;
-    cell_of(i, Lf.N, x, y, z);
-    const int g[3] = {x, y, z};
-    int P[3], Q[3];
-    T sg[3];
+  const int g[2] = {m.x, m.y};
+  int P[2], Q[2];
+  T sg[2];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      P[d] = g[d] >> 1;
-      Q[d] = P[d] + ((g[d] & 1) ? 1 : -1);
-      sg[d] = T(1);
-      if (Q[d] < 0) { Q[d] = 0; sg[d] = T(-1); }
-      if (Q[d] >= Lc.N[d]) { Q[d] = Lc.N[d] - 1; sg[d] = T(-1); }
+  for (int d = 0; d < 2; ++d) {
+    P[d] = g[d] >> 1;
+    Q[d] = P[d] + ((g[d] & 1) ? 1 : -1);
+    sg[d] = T(1);
+    if (Q[d] < 0) { Q[d] = 0; sg[d] = T(-1); }
+    if (Q[d] >= Lc.N[d]) { Q[d] = Lc.N[d] - 1; sg[d] = T(-1); }
+  }
+  // xy-interpolant of coarse plane cz (weights 3/4 parent, 1/4 neighbour, signed ghosts)
+  auto ixy = [&](int cz) {
+    T sgz = T(1);
+    if (cz < 0) { cz = 0; sgz = T(-1); }
+    if (cz >= Lc.N[2]) { cz = Lc.N[2] - 1; sgz = T(-1); }
+    T py[2];
+#pragma unroll
+    for (int ky = 0; ky < 2; ++ky) {
+      const int cy = ky ? Q[1] : P[1];
+      const long long a0 = soff<T>(Lc, P[0], cy, cz), a1 = soff<T>(Lc, Q[0], cy, cz);
+      const T v0 = o.flag ? o.a[a0] - o.b[a0] : o.a[a0];
+      const T v1 = o.flag ? o.a[a1] - o.b[a1] : o.a[a1];
+      py[ky] = W0 * v0 + (W1 * sg[0]) * v1;
     }
-    auto cv = [&](int cx, int cy, int cz) {
-      const long long co = soff<T>(Lc, cx, cy, cz);
-      return o.flag ? o.a[co] - o.b[co] : o.a[co];
-    };
-    // separable: x, then y, then z (weights 3/4 parent, 1/4 neighbour, signed ghosts)
-    T pz[2];
-#pragma unroll
-    for (int kz = 0; kz < 2; ++kz) {
-      const int cz = kz ? Q[2] : P[2];
-      T py[2];
-#pragma unroll
-      for (int ky = 0; ky < 2; ++ky) {
-        const int cy = ky ? Q[1] : P[1];
-        py[ky] = W0 * cv(P[0], cy, cz) + (W1 * sg[0]) * cv(Q[0], cy, cz);
-      }
-      pz[kz] = W0 * py[0] + (W1 * sg[1]) * py[1];
-    }
-    const T acc = W0 * pz[0] + (W1 * sg[2]) * pz[1];
-    const long long off = soff<T>(Lf, x, y, z);
+    return sgz * (W0 * py[0] + (W1 * sg[1]) * py[1]);
+  };
+  for (int z = m.z0; z < m.z1; ++z) {
+    const int Pz = z >> 1, Qz = Pz + ((z & 1) ? 1 : -1);
+    const T acc = W0 * ixy(Pz) + W1 * ixy(Qz);
+    const long long off = soff<T>(Lf, m.x, m.y, z);
     o.c[off] = o.flag ? o.c[off] + acc : acc;
   }
 }
@@ -154,10 +200,9 @@ template <class T>
 __device__ void op_pyramid(const Lvl& Lf, const COp<T>& o, int tid, int nth) {
   const int nfx = Lf.N[0], nfy = Lf.N[1];
   const int nc[3] = {Lf.N[0] / 2, Lf.N[1] / 2, Lf.N[2] / 2};
-  const long long n = (long long)nc[0] * nc[1] * nc[2];
-  for (long long i = tid; i < n; i += nth) {
-    int x, y, z;
-    cell_of(i, nc, x, y, z);
+  const ColMap m = col_map(nc[0], nc[1], nc[2], tid, nth);
+  if (!m.ok) return;
+  for (int z = m.z0; z < m.z1; ++z) {
     T s = T(0);
 #pragma unroll
     for (int dz = 0; dz < 2; ++dz)
@@ -165,31 +210,58 @@ __device__ void op_pyramid(const Lvl& Lf, const COp<T>& o, int tid, int nth) {
       for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx)
-          s += o.a[((long long)(2 * z + dz) * nfy + (2 * y + dy)) * nfx + (2 * x + dx)];
-    o.c[i] = s * T(0.125);
+          s += o.a[((long long)(2 * z + dz) * nfy + (2 * m.y + dy)) * nfx + (2 * m.x + dx)];
+    o.c[((long long)z * nc[1] + m.y) * nc[0] + m.x] = s * T(0.125);
   }
 }
 
 template <class T>
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreadsC, 1)
+__global__ void __launch_bounds__(kThreadsC, 1)
     k_coarse_exec(const __grid_constant__ COpList<T> ol) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   __shared__ T bs[1024];
+  // the operation list and the level table are read from shared memory: dynamically
+  // indexed kernel-parameter reads go through the constant cache and miss (~1 us per op)
+  __shared__ COp<T> sop[kCoarseMaxOps];
+  __shared__ Lvl sL[kCoarseMaxLevels];
+  {
+    const int* src = reinterpret_cast<const int*>(ol.op);
+    int* dst = reinterpret_cast<int*>(sop);
+    const int nw = (int)(ol.n * sizeof(COp<T>) / sizeof(int));
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) dst[k] = src[k];
+    const int* ls = reinterpret_cast<const int*>(ol.L);
+    int* ld = reinterpret_cast<int*>(sL);
+    for (int k = threadIdx.x; k < (int)(sizeof(sL) / sizeof(int)); k += blockDim.x) ld[k] = ls[k];
+  }
+  __syncthreads();
   const int rank = (int)cl.block_rank();
-  const int tid = rank * kThreadsC + (int)threadIdx.x;
-  const int nth = kCluster * kThreadsC;
+  if (ol.prof && rank == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ol.prof[0] = t;
+  }
   for (int i = 0; i < ol.n; ++i) {
-    const COp<T>& o = ol.op[i];
+    const COp<T>& o = sop[i];
+    // an operation on a tiny level runs on CTA 0 alone, and a run of them needs only CTA
+    // barriers; the cluster barrier follows the last of the run
+    const bool tiny = o.tiny != 0;
+    if (tiny && rank != 0) {
+      while (i + 1 < ol.n && sop[i + 1].tiny) ++i;
+      cl.sync();
+      continue;
+    }
+    const int tid = tiny ? (int)threadIdx.x : rank * kThreadsC + (int)threadIdx.x;
+    const int nth = tiny ? kThreadsC : kCluster * kThreadsC;
     switch (o.code) {
-      case kCopCheb: op_cheb(ol.L[o.lf], o, tid, nth); break;
-      case kCopRestrict: op_restrict(ol.L[o.lf], ol.L[o.lc], o, tid, nth); break;
-      case kCopTau: op_tau(ol.L[o.lf], o, tid, nth); break;
-      case kCopProlong: op_prolong(ol.L[o.lf], ol.L[o.lc], o, tid, nth); break;
-      case kCopPyramid: op_pyramid(ol.L[o.lf], o, tid, nth); break;
+      case kCopCheb: op_column<T, false>(sL[o.lf], o, tid, nth); break;
+      case kCopRestrict: op_restrict(sL[o.lf], sL[o.lc], o, tid, nth); break;
+      case kCopTau: op_column<T, true>(sL[o.lf], o, tid, nth); break;
+      case kCopProlong: op_prolong(sL[o.lf], sL[o.lc], o, tid, nth); break;
+      case kCopPyramid: op_pyramid(sL[o.lf], o, tid, nth); break;
       case kCopCoarsest:
         if (rank == 0) {  // one CTA: n0 <= 1024 (create-time check)
-          const Lvl& L = ol.L[o.lf];
+          const Lvl& L = sL[o.lf];
           const int n0 = L.N[0] * L.N[1] * L.N[2];
           for (int j = threadIdx.x; j < n0; j += kThreadsC) {
             int x, y, z;
@@ -208,7 +280,15 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreadsC, 1)
         break;
       default: break;
     }
-    cl.sync();  // the operation's results are visible to every CTA of the cluster
+    if (tiny && i + 1 < ol.n && sop[i + 1].tiny)
+      __syncthreads();  // CTA 0 alone: block-scope visibility suffices
+    else
+      cl.sync();  // the operation's results are visible to every CTA of the cluster
+    if (ol.prof && rank == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ol.prof[i + 1] = t;
+    }
   }
 }
 
@@ -218,10 +298,30 @@ bool coarse_level_ok(const Lvl& L) {
   return L.nsegs == 1 && L.J == 0 && (long long)L.N[0] * L.N[1] * L.N[2] <= kCoarseMaxCells;
 }
 
+bool coarse_level_tiny(const Lvl& L) {
+  return coarse_level_ok(L) && (long long)L.N[0] * L.N[1] * L.N[2] <= 512;
+}
+
 template <class T>
 void launch_coarse_exec(const COpList<T>& ops, cudaStream_t st) {
   if (ops.n <= 0) return;
-  k_coarse_exec<T><<<kCluster, kThreadsC, 0, st>>>(ops);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_coarse_exec<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kCluster);
+  cfg.blockDim = dim3(kThreadsC);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_coarse_exec<T>, ops);
 }
 
 template void launch_coarse_exec<double>(const COpList<double>&, cudaStream_t);

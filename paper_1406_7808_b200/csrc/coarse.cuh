@@ -19,6 +19,7 @@ struct COp {
   int code;
   int lf, lc;      // level indices into COpList::L (fine, coarse)
   int flag;        // PROLONG: add
+  int tiny;        // level small enough for one CTA (set by the recorder)
   const T* a;      // CHEB cur | RESTRICT u_f | TAU u | PROLONG w | COARSEST A0^-1 | PYRAMID f_f
   const T* b;      // CHEB prev (may alias c, or null) | PROLONG t
   T* c;            // CHEB out | RESTRICT u_c | TAU rhs | PROLONG u_f | COARSEST u | PYRAMID f_c
@@ -30,12 +31,15 @@ struct COp {
 template <class T>
 struct COpList {
   int n;
+  unsigned long long* prof;  // optional: %globaltimer after every operation (debug)
   Lvl L[kCoarseMaxLevels];
   COp<T> op[kCoarseMaxOps];
 };
 
 // Conventional single-segment level small enough for the executor.
 bool coarse_level_ok(const Lvl& L);
+// ... and small enough for one CTA of it (no cluster barrier needed around its operations)
+bool coarse_level_tiny(const Lvl& L);
 
 template <class T>
 void launch_coarse_exec(const COpList<T>& ops, cudaStream_t st);

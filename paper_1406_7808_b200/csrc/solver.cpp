@@ -449,7 +449,10 @@ struct Schedule {
       cops_top = 0;
       cops_bytes = 0;
     }
-    cops.op[cops.n++] = o;
+    cops.op[cops.n] = o;
+    // tiny: every level the operation touches fits one CTA
+    cops.op[cops.n].tiny = srfmg::coarse_level_tiny(h->L[o.lf]) && srfmg::coarse_level_tiny(h->L[o.lc]);
+    cops.n++;
     cops_top = std::max(cops_top, o.lf);
     cops_bytes += bytes;
   }
@@ -458,7 +461,22 @@ struct Schedule {
     flushing = true;
     {
       Launch g(h, st, KC_COARSE, cops_top, cops_bytes);
-      srfmg::launch_coarse_exec<T>(cops, st);
+      static const char* pe = std::getenv("SR_FMG_CEXEC_PROF");
+      cops.prof = nullptr;
+      if (pe && pe[0] == '1') {  // debug: per-operation timestamps, printed after the launch
+        static unsigned long long* buf = nullptr;
+        if (!buf) cudaMallocManaged(&buf, sizeof(unsigned long long) * (srfmg::kCoarseMaxOps + 1));
+        cops.prof = buf;
+        srfmg::launch_coarse_exec<T>(cops, st);
+        cudaStreamSynchronize(st);
+        for (int i = 0; i < cops.n; ++i) {
+          const srfmg::COp<T>& o = cops.op[i];
+          fprintf(stderr, "cexec op %2d code %d lf %d lc %d tiny %d  %8.2f us\n", i, o.code, o.lf,
+                  o.lc, o.tiny, (buf[i + 1] - buf[i]) * 1e-3);
+        }
+      } else {
+        srfmg::launch_coarse_exec<T>(cops, st);
+      }
     }
     cops.n = 0;
     flushing = false;
