@@ -87,10 +87,12 @@ struct PassGeom {
   static constexpr int OFF_C = OFF_F + RF * FPL;
   static size_t smem(int cpl) { return (size_t)(OFF_C + RC * NF * cpl) * sizeof(T) + 8 * NBAR; }
   static int crows() { return RW / 2 + 2; }
+  static constexpr int MINB = 1;  // (2 for Pi + S^1 spills and measured no faster)
 };
 
 template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG>
-__global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>::NT, 1)
+__global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>::NT,
+                                  PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>::MINB)
     k_pass(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ PassArgs<T> a) {
   using G = PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>;
   constexpr int NS = G::NS;

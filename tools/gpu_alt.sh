@@ -1,2 +1,3 @@
-for a in 0 1 2 3; do SR_FMG_CHEB2_ALT=$a timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --dtype f32 > gpurun_out/bench_alt32_$a.log 2>&1; done
-for a in 1 2; do SR_FMG_CHEB2_ALT=$a timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_alt64_$a.log 2>&1; done
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_e0.log 2>&1
+SR_FMG_PASS_ENTRY=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_e1.log 2>&1
+SR_FMG_PASS_ENTRY=1 timeout 300 python tools/breakdown.py > gpurun_out/breakdown_e1.log 2>&1
