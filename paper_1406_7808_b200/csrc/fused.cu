@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(NTMAX, 1)
 // (tensor TMA, smem pitch PY + 16 B so the 16-byte aligned box start fits); RG = 0: rhs
 // is segment storage (1-D bulk copies, pitch PY).  Same arithmetic as k_cheb2.
 // =====================================================================================
-template <class T, int PY, int BH, int MAXS, int RG>
+template <class T, int PY, int BH, int MAXS, int RG, int NST = 2>
 struct SpecGeom {
   static constexpr int kAl = 16 / (int)sizeof(T);
   static constexpr int FP = RG ? PY + kAl : PY;
@@ -268,17 +268,20 @@ struct SpecGeom {
   static constexpr int U0S = ((TR + 2) * PY + A - 1) / A * A;
   static constexpr int FS = (TR * FP + A - 1) / A * A;
   static constexpr int U1S = ((TR + 2) * PY + A - 1) / A * A;
-  static constexpr int RU = 3, RF = 4;
-  static constexpr size_t SMEM = (size_t)(RU * U0S + RF * FS + 3 * U1S) * sizeof(T) + 8 * (RU + RF);
+  // rings: the degree-1 pass has half the arithmetic per plane, so it streams 4 planes
+  // ahead (in the smem the u1 planes of the degree-2 pass would take)
+  static constexpr int RU = NST == 1 ? 5 : 3, RF = NST == 1 ? 5 : 4, NU1 = NST == 1 ? 0 : 3;
+  static constexpr size_t SMEM =
+      (size_t)(RU * U0S + RF * FS + NU1 * U1S) * sizeof(T) + 8 * (RU + RF);
   // CTAs per SM the smem allows (capped at 3: registers)
   static constexpr int MINB = SMEM <= 75 * 1024 ? 3 : SMEM <= 113 * 1024 ? 2 : 1;
 };
 
 template <class T, int PY, int BH, int MAXS, int RG, int NST, int FIN = 0>
-__global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
-                                  SpecGeom<T, PY, BH, MAXS, RG>::MINB)
+__global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
+                                  SpecGeom<T, PY, BH, MAXS, RG, NST>::MINB)
     k_cheb2s(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
-  using G = SpecGeom<T, PY, BH, MAXS, RG>;
+  using G = SpecGeom<T, PY, BH, MAXS, RG, NST>;
   extern __shared__ __align__(128) unsigned char sm[];
   const Lvl& L = a.L;
   const int Ex = L.E[0], Ey = L.E[1], Ez = L.E[2];
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
   T* u0s = reinterpret_cast<T*>(sm);
   T* fs = u0s + G::RU * G::U0S;
   T* u1s = fs + G::RF * G::FS;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + 3 * G::U1S);  // [0,3) u0, [3,7) f
+  uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + G::NU1 * G::U1S);  // [0,RU) u0, then f
 
   const int px = s % L.ns[0] + L.so[0];
   const int pyy = (s / L.ns[0]) % L.ns[1] + L.so[1];
@@ -313,26 +316,25 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
   }
   __syncthreads();
   auto issue_u0 = [=](int z) {
-    const int sl = z % 3;
+    const int sl = z % G::RU;
     mbar_expect_tx(&bars[sl], u0_bytes);
     bulk_g2s(u0s + sl * G::U0S + (q0 - s0 + 1) * PY, useg + (long long)z * pz + (long long)q0 * PY,
              u0_bytes,
              &bars[sl]);
   };
   auto issue_f = [=, &fmap](int z) {
-    const int sl = z & 3;
-    mbar_expect_tx(&bars[3 + sl], f_bytes);
+    const int sl = z % G::RF;
+    mbar_expect_tx(&bars[G::RU + sl], f_bytes);
     if (RG)
-      tma_3d(fs + sl * G::FS, &fmap, oxa, oy + s0 - a.foff[1], oz + z - a.foff[2], &bars[3 + sl]);
+      tma_3d(fs + sl * G::FS, &fmap, oxa, oy + s0 - a.foff[1], oz + z - a.foff[2],
+             &bars[G::RU + sl]);
     else
       bulk_g2s(fs + sl * G::FS, rseg + (long long)z * pz + (long long)s0 * PY, f_bytes,
-               &bars[3 + sl]);
+               &bars[G::RU + sl]);
   };
   if (threadIdx.x == 0) {
-    for (int z = 0; z < min(3, Ez); ++z) {
-      issue_u0(z);
-      issue_f(z);
-    }
+    for (int z = 0; z < min(G::RU, Ez); ++z) issue_u0(z);
+    for (int z = 0; z < min(NST == 1 ? G::RF : 3, Ez); ++z) issue_f(z);
   }
 
   const int tx = threadIdx.x % PY, g = threadIdx.x / PY;
@@ -379,11 +381,11 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
     constexpr int R = decltype(RR)::value;  // z % 3: u0 ring slot, u1 buffer, queue slot
     constexpr int IM = (R + 2) % 3, I0 = R, IP = (R + 1) % 3;
     if (z < Ez) {
-      if (z + 1 < Ez) mbar_wait(&bars[IP], ((z + 1) / 3) & 1);
-      mbar_wait(&bars[3 + (z & 3)], (z >> 2) & 1);
-      const T* pl = u0b + R * G::U0S;
-      const T* pn = u0b + IP * G::U0S;
-      const T* fp = fb + (z & 3) * G::FS;
+      if (z + 1 < Ez) mbar_wait(&bars[(z + 1) % G::RU], ((z + 1) / G::RU) & 1);
+      mbar_wait(&bars[G::RU + z % G::RF], (z / G::RF) & 1);
+      const T* pl = u0b + (z % G::RU) * G::U0S;
+      const T* pn = u0b + ((z + 1) % G::RU) * G::U0S;
+      const T* fp = fb + (z % G::RF) * G::FS;
       T* u1w = u1b + R * G::U1S;
       const int gz = oz + z;
       const bool zc = gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2;
@@ -413,8 +415,12 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
     }
     __syncthreads();  // the only barrier of the plane step
     if (threadIdx.x == 0) {
-      if (z + 3 < Ez) issue_u0(z + 3);                  // u0 slot z%3 is free
-      if (z >= 1 && z + 2 < Ez) issue_f(z + 2);         // rhs slot (z-2)&3 is free
+      if (z + G::RU < Ez) issue_u0(z + G::RU);  // u0 slot of plane z is free
+      if (NST == 1) {
+        if (z + G::RF < Ez) issue_f(z + G::RF);  // rhs plane z is consumed
+      } else if (z >= 1 && z + 2 < Ez) {
+        issue_f(z + 2);  // rhs slot of plane z-2 (stage 2 finished it) is free
+      }
     }
     if (NST == 2 && z >= 1) {
       const int zz = z - 1;
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG>::NT,
         const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
         constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
         const T* u1r = u1b + J1 * G::U1S;
-        const T* fp = fb + (zz & 3) * G::FS;
+        const T* fp = fb + (zz % G::RF) * G::FS;
         T* orow = ob + (long long)zz * pz;
         const unsigned act = zc ? c_mask : 0u;
 #pragma unroll
@@ -586,16 +592,18 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
   };
   const bool fin = a.fin.p != nullptr;
   if (b.global) {
-    using G = SpecGeom<T, PY, BH, MAXS, 1>;
-    if (!encode_rhs_map<T>(&map, b, G::FP, BH + 2)) return false;
-    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 1, 2, 1>, G::SMEM, G::NT);
-    else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 1, 2>, G::SMEM, G::NT);
-    else go(k_cheb2s<T, PY, BH, MAXS, 1, 1>, G::SMEM, G::NT);
+    using G2 = SpecGeom<T, PY, BH, MAXS, 1, 2>;
+    using G1 = SpecGeom<T, PY, BH, MAXS, 1, 1>;
+    if (!encode_rhs_map<T>(&map, b, G2::FP, BH + 2)) return false;
+    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 1, 2, 1>, G2::SMEM, G2::NT);
+    else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 1, 2>, G2::SMEM, G2::NT);
+    else go(k_cheb2s<T, PY, BH, MAXS, 1, 1>, G1::SMEM, G1::NT);
   } else {
-    using G = SpecGeom<T, PY, BH, MAXS, 0>;
-    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 1>, G::SMEM, G::NT);
-    else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 0, 2>, G::SMEM, G::NT);
-    else go(k_cheb2s<T, PY, BH, MAXS, 0, 1>, G::SMEM, G::NT);
+    using G2 = SpecGeom<T, PY, BH, MAXS, 0, 2>;
+    using G1 = SpecGeom<T, PY, BH, MAXS, 0, 1>;
+    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 1>, G2::SMEM, G2::NT);
+    else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 0, 2>, G2::SMEM, G2::NT);
+    else go(k_cheb2s<T, PY, BH, MAXS, 0, 1>, G1::SMEM, G1::NT);
   }
   return true;
 }

@@ -23,6 +23,7 @@
 // every thread's MAXS rows hold whole 2x2 restriction/prolongation pairs, and lanes are
 // rotated by the parity of the segment's x origin so that x-pairs are lane pairs (2m, 2m+1)
 // of one warp (restriction sums with one shuffle).
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -59,11 +60,14 @@ struct PassArgs {
 
 constexpr long long rup(long long v, long long m) { return (v + m - 1) / m * m; }
 
-template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG>
+template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG, int CL>
 struct PassGeom {
   static constexpr int NS = NSTEP + (SINK == kSinkRestrict ? 1 : 0);  // stencil stages
-  static constexpr int NSE = NS + (NS & 1);    // thread rows start NSE rows above the band
-  static constexpr int RW = (int)rup(BH + 1 + NS + NSE, MAXS);  // thread rows of a band
+  // CL = 0: bands recompute their halo rows (thread rows start NSE rows above the band);
+  // CL = 1: the bands of a segment form a cluster and exchange halo rows through DSMEM, so
+  // thread rows cover the band only (band 0 starts one row early to keep row pairs aligned)
+  static constexpr int NSE = CL ? 0 : NS + (NS & 1);
+  static constexpr int RW = CL ? (int)rup(BH + 1, MAXS) : (int)rup(BH + 1 + NS + NSE, MAXS);
   static constexpr int NG = RW / MAXS;
   static constexpr int NT = PY * NG;
   static constexpr int A = 128 / (int)sizeof(T);
@@ -90,11 +94,11 @@ struct PassGeom {
   static constexpr int MINB = 1;  // (2 for Pi + S^1 spills and measured no faster)
 };
 
-template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG>
-__global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>::NT,
-                                  PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>::MINB)
+template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG, int CL>
+__global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG, CL>::NT,
+                                  PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG, CL>::MINB)
     k_pass(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ PassArgs<T> a) {
-  using G = PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>;
+  using G = PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG, CL>;
   constexpr int NS = G::NS;
   constexpr bool RING = G::RING;
   constexpr bool RESTRICT = SINK == kSinkRestrict;
@@ -118,8 +122,12 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
   const int yal = oy & 1;
   const int r0 = blockIdx.x == 0 ? 0 : yal + (int)blockIdx.x * BH;  // output rows [r0, r1)
   const int r1 = min(Ey, yal + ((int)blockIdx.x + 1) * BH);
-  const int yb = yal + (int)blockIdx.x * BH - G::NSE;  // first thread row
-  const int q0 = max(0, yb), q1 = min(Ey, yb + G::RW);  // rows streamed
+  const int nb = (int)gridDim.x;  // bands of a segment (= cluster size when CL)
+  // first thread row; rows streamed (CL: the band plus one halo row each side)
+  const int yb = CL ? (blockIdx.x == 0 ? -yal : r0) : yal + (int)blockIdx.x * BH - G::NSE;
+  const int q0 = CL ? max(0, r0 - 1) : max(0, yb);
+  const int q1 = CL ? min(Ey, r1 + 1) : min(Ey, yb + G::RW);
+  const int fq0 = max(0, yb), fq1 = min(Ey, yb + G::RW);  // rhs rows (segment storage rhs)
   T* const bufU = sbase + G::OFF_U;
   T* const bufS = sbase + G::OFF_S;
   T* const bufF = sbase + G::OFF_F;
@@ -135,8 +143,9 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
   const int oxt = ox - a.foff[0];
   const int oxa = oxt & ~(G::kAl - 1);
   const int fsh = RG ? oxt - oxa : 0;
-  const uint32_t fbytes = RG ? (uint32_t)(G::RW * G::FPI * sizeof(T)) : ubytes;
-  const int foffs = RG ? 0 : (q0 - yb) * PY;
+  const uint32_t fbytes = RG ? (uint32_t)(G::RW * G::FPI * sizeof(T))
+                              : (uint32_t)((fq1 - fq0) * PY * sizeof(T));
+  const int foffs = RG ? 0 : (fq0 - yb) * PY;
 
   // coarse segment (PSET/PADD source, RESTRICT target): the fine segment's own coarse
   // storage on SR levels, the single global array at the transition level
@@ -174,7 +183,10 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
     for (int i = 0; i < G::NBAR; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  if constexpr (CL)
+    cooperative_groups::this_cluster().sync();  // every band's smem exists before DSMEM use
+  else
+    __syncthreads();
   auto issue_u = [&](int z) {
     const int sl = z % G::RU;
     mbar_expect_tx(&barU[sl], ubytes);
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
     if constexpr (RG)
       tma_3d(bufF + sl * G::FPL, &fmap, oxa, oy + yb - a.foff[1], oz + z - a.foff[2], &barF[sl]);
     else
-      bulk_g2s(bufF + sl * G::FPL + foffs, rseg + (long long)z * pz + (long long)q0 * PY, fbytes,
+      bulk_g2s(bufF + sl * G::FPL + foffs, rseg + (long long)z * pz + (long long)fq0 * PY, fbytes,
                &barF[sl]);
   };
   auto issue_c = [&](int c) {
@@ -235,9 +247,43 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
     if (in && y >= r0 && y < r1) wmk |= 1u << k;
     ydg |= (unsigned)((gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0)) << (2 * k);
 #pragma unroll
-    for (int j = 0; j <= NS; ++j)
-      if (y >= r0 - (NS - j) && y < r1 + (NS - j)) vm[j] |= 1u << k;
+    for (int j = 0; j <= NS; ++j) {
+      const int hw = CL ? 0 : NS - j;  // rows recomputed beyond the band by stage j
+      if (y >= r0 - hw && y < r1 + hw) vm[j] |= 1u << k;
+    }
   }
+  // CL: the y-halo rows of every stage input (rows r0 - 1 and r1) live in the neighbouring
+  // bands' shared memory; the two slots that need them read them through DSMEM once per
+  // plane step, right after the cluster barrier that published them
+  unsigned hu = 0, hd = 0;
+  const T* nb_up = nullptr;
+  const T* nb_dn = nullptr;
+  int hoff_up = 0, hoff_dn = 0;
+  if constexpr (CL) {
+    const int b = (int)blockIdx.x;
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) {
+      const int y = y0 + k;
+      if (b > 0 && y == r0 && tx < Ex) hu |= 1u << k;
+      if (b < nb - 1 && y == r1 - 1 && tx < Ex) hd |= 1u << k;
+    }
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    if (b > 0) nb_up = cl.map_shared_rank(sbase, b - 1);
+    if (b < nb - 1) nb_dn = cl.map_shared_rank(sbase, b + 1);
+    const int yb_up = (b - 1 == 0) ? -yal : yal + (b - 1) * BH;
+    const int yb_dn = yal + (b + 1) * BH;
+    hoff_up = (r0 - 1 - yb_up + 1) * PY + tx;
+    hoff_dn = (r1 - yb_dn + 1) * PY + tx;
+  }
+  T hup[NS + 1], hdn[NS + 1];
+#pragma unroll
+  for (int j = 0; j <= NS; ++j) hup[j] = hdn[j] = T(0);
+  // element offset (from the smem base) of the input plane of stage j (1..NS) at plane zj
+  auto in_off = [&](int j, int zj) -> int {
+    if (j == 1) return G::OFF_U + (RING ? (zj % G::RU) : (zj & 1)) * G::PL;
+    return G::OFF_S + (2 * (j - 2) + (zj & 1)) * G::PL;
+  };
+
   // diagonal of A per slot: 6 + one per reflected (out-of-domain) x/y neighbour (R3);
   // the z part is added per plane
   T dk[MAXS];
@@ -344,6 +390,17 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
 
   auto iter = [&](auto RR, int z) {
     constexpr int R = decltype(RR)::value;  // z % 3
+    if constexpr (CL) {
+#pragma unroll
+      for (int j = 1; j <= NS; ++j) {
+        const int zj = z - j;
+        if (zj >= 0 && zj < Ez) {
+          const int o = in_off(j, zj);
+          if (hu) hup[j] = nb_up[o + hoff_up];
+          if (hd) hdn[j] = nb_dn[o + hoff_dn];
+        }
+      }
+    }
     // ------------------------------------------------------------ source at plane z
     if (z < Ez) {
       const int gz = oz + z;
@@ -414,8 +471,12 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
         // branch-free: every slot computes, the C-cell predicate selects (GSR, dead rows
         // and out-of-domain cells carry their value through)
         const T v = q[j - 1][k][I0];
-        const T ym = (k == 0) ? src[-PY] : q[j - 1][k > 0 ? k - 1 : 0][I0];
-        const T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[j - 1][k + 1 < MAXS ? k + 1 : k][I0];
+        T ym = (k == 0) ? src[-PY] : q[j - 1][k > 0 ? k - 1 : 0][I0];
+        T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[j - 1][k + 1 < MAXS ? k + 1 : k][I0];
+        if constexpr (CL) {
+          ym = ((hu >> k) & 1u) ? hup[j] : ym;
+          yp = ((hd >> k) & 1u) ? hdn[j] : yp;
+        }
         const T sum = ((q[j - 1][k][IM] + q[j - 1][k][IP]) + (ym + yp)) +
                       (src[k * PY - 1] + src[k * PY + 1]);
         const T r = fp[k * G::FPI] - ((dk[k] + dz) * v - sum) * ih2;
@@ -468,8 +529,12 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) {
           const T v = q[NSTEP][k][I0];
-          const T ym = (k == 0) ? src[-PY] : q[NSTEP][k > 0 ? k - 1 : 0][I0];
-          const T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[NSTEP][k + 1 < MAXS ? k + 1 : k][I0];
+          T ym = (k == 0) ? src[-PY] : q[NSTEP][k > 0 ? k - 1 : 0][I0];
+          T yp = (k == MAXS - 1) ? src[MAXS * PY] : q[NSTEP][k + 1 < MAXS ? k + 1 : k][I0];
+          if constexpr (CL) {
+            ym = ((hu >> k) & 1u) ? hup[NS] : ym;
+            yp = ((hd >> k) & 1u) ? hdn[NS] : yp;
+          }
           const T sum = ((q[NSTEP][k][IM] + q[NSTEP][k][IP]) + (ym + yp)) +
                         (src[k * PY - 1] + src[k * PY + 1]);
           const T r = fp[k * G::FPI] - ((dk[k] + dz) * v - sum) * ih2;
@@ -501,7 +566,10 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
         }
       }
     }
-    __syncthreads();  // the only barrier of the plane step
+    if constexpr (CL)
+      cooperative_groups::this_cluster().sync();  // planes (and halo rows) published
+    else
+      __syncthreads();  // the only barrier of the plane step
     if (threadIdx.x == 0) {
       if constexpr (RING)
         if (z + G::RU - 1 < Ez) issue_u(z + G::RU - 1);  // slot of plane z-1 is free
@@ -560,9 +628,9 @@ __global__ void __launch_bounds__(256) k_merge_f(Lvl L, Lvl Lc, const T* __restr
 }
 
 // ---- host side ---------------------------------------------------------------------
-template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG>
+template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG, int CL>
 bool inst(const PassSpec<T>& ps, cudaStream_t st, bool launch) {
-  using G = PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>;
+  using G = PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG, CL>;
   const Lvl& L = ps.L;
   if (L.py != PY || L.E[0] > PY) return false;
   PassArgs<T> a{};
@@ -590,13 +658,30 @@ bool inst(const PassSpec<T>& ps, cudaStream_t st, bool launch) {
   const int oy = L.so[1] * L.S[1] - (L.J + 1);  // parity of every segment's y origin
   const int yal = oy & 1;
   const int nb = (L.E[1] - yal + BH - 1) / BH;
-  auto kern = k_pass<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG>;
+  if (CL && (nb < 2 || nb > 8)) return false;  // one cluster per segment (portable size)
+  auto kern = k_pass<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG, CL>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  kern<<<dim3(nb, L.nsegs), G::NT, smem, st>>>(map, a);
+  if constexpr (CL) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nb, L.nsegs);
+    cfg.blockDim = dim3(G::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = nb;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, map, a);
+  } else {
+    kern<<<dim3(nb, L.nsegs), G::NT, smem, st>>>(map, a);
+  }
   return true;
 }
 
@@ -614,7 +699,15 @@ bool by_geom(const PassSpec<T>& ps, cudaStream_t st, bool launch) {
   if (ps.L.py > max_py()) return false;
   // only the E = 70 geometry (64^3 segments, J = 2): on smaller boxes the band halos and
   // the low occupancy make the fused pass slower than the separate kernels (measured)
-  return inst<T, 72, 14, 4, SRC, NSTEP, SINK, RG>(ps, st, launch);
+  // SR_FMG_PASS_CL=1: the cluster/DSMEM variant (no recomputed halos; one CTA of 9 warps
+  // per SM and a cluster barrier per plane: measured 1.5-1.7x slower than recomputing)
+  static int cl = -1;
+  if (cl < 0) {
+    const char* e = std::getenv("SR_FMG_PASS_CL");
+    cl = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (cl) return inst<T, 72, 14, 4, SRC, NSTEP, SINK, RG, 1>(ps, st, launch);
+  return inst<T, 72, 14, 4, SRC, NSTEP, SINK, RG, 0>(ps, st, launch);
 }
 
 template <class T>

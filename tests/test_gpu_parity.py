@@ -362,13 +362,17 @@ PASS_CASES = [
 ]
 
 
+@pytest.mark.parametrize("cl", ["1", "0"], ids=["cluster", "recompute"])
 @pytest.mark.parametrize("mode", ["0", "1", "3", "4"])
 @pytest.mark.parametrize("case", PASS_CASES, ids=[c[0] for c in PASS_CASES])
-def test_fused_passes_match_oracle(case, mode, monkeypatch):
+def test_fused_passes_match_oracle(case, mode, cl, monkeypatch):
+    # cl: bands of a segment as one thread-block cluster exchanging halo rows through DSMEM,
+    # or independent bands that recompute their halo rows
     name, n, M, seg, J, K, rhs = case
     f = W.make_rhs(rhs, n)
     ref = _oracle(rhs, f, n, M, seg, J, K)
     monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_PASS_CL", cl)
     monkeypatch.setenv("SR_FMG_PASS", mode)
     u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
     assert rel_l2(u, ref) <= TOL64, (name, mode, rel_l2(u, ref))
