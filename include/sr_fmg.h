@@ -141,6 +141,19 @@ sr_status_t sr_fmg_solve(sr_fmg_t *h, const void *f, void *u);
  * synchronises.  Pinned host memory makes the copies asynchronous DMA. */
 sr_status_t sr_fmg_solve_host(sr_fmg_t *h, const void *f_host, void *u_host);
 
+/* Asynchronous host-buffer solve for a stream of right-hand sides.  Enqueues: copy f_host
+ * (layout of sr_fmg_solve's f) into one of two internal device slots on a copy stream, the
+ * solve on the handle's stream, and the copy of u back to u_host on a second copy stream,
+ * chained with events.  Consecutive calls alternate the slots, so the host->device copy of
+ * call i+1, the solve of call i and the device->host copy of call i-1 overlap (PCIe is full
+ * duplex; the copy engines run beside the SMs).  Returns immediately: the caller must not
+ * modify f_host nor read u_host before sr_fmg_synchronize(h).  f_host/u_host should be
+ * pinned (cudaHostAlloc / cudaHostRegister); pageable memory works but serialises. */
+sr_status_t sr_fmg_solve_host_async(sr_fmg_t *h, const void *f_host, void *u_host);
+
+/* Wait for every solve and copy enqueued on the handle; returns its sticky status. */
+sr_status_t sr_fmg_synchronize(sr_fmg_t *h);
+
 /* Change the stream later solves are ordered on (a captured graph is reused). */
 sr_status_t sr_fmg_set_stream(sr_fmg_t *h, void *stream);
 

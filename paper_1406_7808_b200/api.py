@@ -237,6 +237,24 @@ class Solver:
                                     ctypes.c_void_p(out.data_ptr())), self._h)
         return out
 
+    def solve_host_async(self, f, out):
+        """Enqueue a host-buffer solve (sr_fmg_solve_host_async): returns at once; the
+        host->device copy of the next call, this solve and the device->host copy of the
+        previous call overlap.  Neither `f` nor `out` may be touched before synchronize()."""
+        import torch
+        for t, nm, shp in ((f, "f", self.f_shape), (out, "out", self.shape)):
+            if not isinstance(t, torch.Tensor) or t.is_cuda or tuple(t.shape) != tuple(shp) \
+                    or not t.is_contiguous() or t.dtype != (torch.float64 if self.dtype == "f64"
+                                                            else torch.float32):
+                raise ValueError(f"{nm} must be a contiguous host tensor of shape {shp}")
+        check(lib.sr_fmg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+              self._h)
+        check(lib.sr_fmg_solve_host_async(self._h, ctypes.c_void_p(f.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr())), self._h)
+
+    def synchronize(self):
+        check(lib.sr_fmg_synchronize(self._h), self._h)
+
     # -- test / profiling hooks ----------------------------------------------------------
     def level_storage(self, l, field=0) -> np.ndarray:
         """Internal storage of level l (field 0 = u, 1 = rhs, 2 = t) as an array of shape

@@ -78,11 +78,25 @@ struct sr_fmg {
   cudaStream_t cap = nullptr;      // private stream used for graph capture
   std::string err = "no error";
   sr_status_t sticky = SR_OK;
-  cudaGraphExec_t gexec = nullptr;
-  const void* g_f = nullptr;
-  void* g_u = nullptr;
-  void* host_f = nullptr;  // device staging buffers for sr_fmg_solve_host
-  void* host_u = nullptr;
+  // captured solves, keyed by the (f, u) device pointers (two: the host-buffer pipeline
+  // alternates two staging slots)
+  struct GraphEnt {
+    cudaGraphExec_t exec = nullptr;
+    const void* f = nullptr;
+    void* u = nullptr;
+    long long used = 0;
+  };
+  GraphEnt graphs[2];
+  long long gclock = 0;
+  // host-buffer pipeline (sr_fmg_solve_host_async): two device staging slots; H2D on one
+  // copy stream, the solve on the handle's stream, D2H on another, chained with events, so
+  // consecutive calls overlap the two PCIe directions with each other and with the solves
+  void* host_f[2] = {nullptr, nullptr};
+  void* host_u[2] = {nullptr, nullptr};
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_solve[2] = {nullptr, nullptr},
+              ev_d2h[2] = {nullptr, nullptr};
+  long long hcalls = 0;
   long long launches = 0;
   bool sync_debug = false;
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
@@ -984,7 +998,15 @@ struct ReplayComm : Comm {
 };
 
 void free_all(sr_fmg* h) {
-  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto& g : h->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
+    if (h->ev_solve[i]) cudaEventDestroy(h->ev_solve[i]);
+    if (h->ev_d2h[i]) cudaEventDestroy(h->ev_d2h[i]);
+  }
+  if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+  if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
   for (auto& b : h->B) {
     cudaFree(b.u[0]);
     cudaFree(b.u[1]);
@@ -998,8 +1020,10 @@ void free_all(sr_fmg* h) {
   delete h->comm;
   h->comm = nullptr;
   cudaFree(h->ainv);
-  cudaFree(h->host_f);
-  cudaFree(h->host_u);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(h->host_f[i]);
+    cudaFree(h->host_u[i]);
+  }
   for (auto& r : h->prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -1192,10 +1216,16 @@ sr_status_t sr_fmg_solve(sr_fmg_t* h, const void* f, void* u) {
     return fail(h, SR_ERR_INVALID_ARGUMENT, "f and u must be 16-byte aligned");
   const bool graph = h->d.use_graph && !h->sync_debug;
   if (!graph) return enqueue_solve(h, f, u, h->stream);
-  if (!h->gexec || h->g_f != f || h->g_u != u) {
-    if (h->gexec) {
-      cudaGraphExecDestroy(h->gexec);
-      h->gexec = nullptr;
+  sr_fmg::GraphEnt* ge = nullptr;
+  for (auto& g : h->graphs)
+    if (g.exec && g.f == f && g.u == u) ge = &g;
+  if (!ge) {  // capture for these pointers, replacing the least recently used graph
+    ge = &h->graphs[0];
+    for (auto& g : h->graphs)
+      if (!g.exec || g.used < ge->used) ge = &g;
+    if (ge->exec) {
+      cudaGraphExecDestroy(ge->exec);
+      ge->exec = nullptr;
     }
     CU(h, cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
     sr_status_t st = enqueue_solve(h, f, u, h->cap);
@@ -1203,33 +1233,70 @@ sr_status_t sr_fmg_solve(sr_fmg_t* h, const void* f, void* u) {
     cudaError_t e = cudaStreamEndCapture(h->cap, &g);
     if (st != SR_OK) return st;
     if (e != cudaSuccess) return fail(h, SR_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&h->gexec, g, 0);
+    e = cudaGraphInstantiate(&ge->exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, SR_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
-    h->g_f = f;
-    h->g_u = u;
+    ge->f = f;
+    ge->u = u;
   }
-  CU(h, cudaGraphLaunch(h->gexec, h->stream));
+  ge->used = ++h->gclock;
+  CU(h, cudaGraphLaunch(ge->exec, h->stream));
   return SR_OK;
 }
 
-sr_status_t sr_fmg_solve_host(sr_fmg_t* h, const void* f_host, void* u_host) {
+sr_status_t sr_fmg_solve_host_async(sr_fmg_t* h, const void* f_host, void* u_host) {
   if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
   if (h->sticky != SR_OK) return h->sticky;
   if (!f_host || !u_host) return fail(h, SR_ERR_INVALID_ARGUMENT, "f or u is NULL");
   const auto& fd = h->fdim[h->M];
   const size_t fbytes = (size_t)fd[0] * fd[1] * fd[2] * h->esize;
   const size_t ubytes = (size_t)h->blk_n[0] * h->blk_n[1] * h->blk_n[2] * h->esize;
-  if (!h->host_f) {
-    CU(h, cudaMalloc(&h->host_f, fbytes));
-    CU(h, cudaMalloc(&h->host_u, ubytes));
+  if (!h->s_h2d) {
+    CU(h, cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    CU(h, cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CU(h, cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming));
+      CU(h, cudaEventCreateWithFlags(&h->ev_solve[i], cudaEventDisableTiming));
+      CU(h, cudaEventCreateWithFlags(&h->ev_d2h[i], cudaEventDisableTiming));
+      // "already completed" initial state for the first two calls' waits
+      CU(h, cudaEventRecord(h->ev_solve[i], h->stream));
+      CU(h, cudaEventRecord(h->ev_d2h[i], h->stream));
+    }
   }
-  CU(h, cudaMemcpyAsync(h->host_f, f_host, fbytes, cudaMemcpyHostToDevice, h->stream));
-  sr_status_t st = sr_fmg_solve(h, h->host_f, h->host_u);
+  const int k = (int)(h->hcalls & 1);
+  if (!h->host_f[k]) {
+    CU(h, cudaMalloc(&h->host_f[k], fbytes));
+    CU(h, cudaMalloc(&h->host_u[k], ubytes));
+  }
+  // f -> slot k once the solve two calls back has finished reading it
+  CU(h, cudaStreamWaitEvent(h->s_h2d, h->ev_solve[k], 0));
+  CU(h, cudaMemcpyAsync(h->host_f[k], f_host, fbytes, cudaMemcpyHostToDevice, h->s_h2d));
+  CU(h, cudaEventRecord(h->ev_h2d[k], h->s_h2d));
+  // the solve once f has landed and the copy-out two calls back has drained u of slot k
+  CU(h, cudaStreamWaitEvent(h->stream, h->ev_h2d[k], 0));
+  CU(h, cudaStreamWaitEvent(h->stream, h->ev_d2h[k], 0));
+  sr_status_t st = sr_fmg_solve(h, h->host_f[k], h->host_u[k]);
   if (st != SR_OK) return st;
-  CU(h, cudaMemcpyAsync(u_host, h->host_u, ubytes, cudaMemcpyDeviceToHost, h->stream));
-  CU(h, cudaStreamSynchronize(h->stream));
+  CU(h, cudaEventRecord(h->ev_solve[k], h->stream));
+  CU(h, cudaStreamWaitEvent(h->s_d2h, h->ev_solve[k], 0));
+  CU(h, cudaMemcpyAsync(u_host, h->host_u[k], ubytes, cudaMemcpyDeviceToHost, h->s_d2h));
+  CU(h, cudaEventRecord(h->ev_d2h[k], h->s_d2h));
+  h->hcalls++;
   return SR_OK;
+}
+
+sr_status_t sr_fmg_synchronize(sr_fmg_t* h) {
+  if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->s_h2d) CU(h, cudaStreamSynchronize(h->s_h2d));
+  if (h->s_d2h) CU(h, cudaStreamSynchronize(h->s_d2h));
+  return h->sticky;
+}
+
+sr_status_t sr_fmg_solve_host(sr_fmg_t* h, const void* f_host, void* u_host) {
+  sr_status_t st = sr_fmg_solve_host_async(h, f_host, u_host);
+  if (st != SR_OK) return st;
+  return sr_fmg_synchronize(h);
 }
 
 void sr_fmg_destroy(sr_fmg_t* h) {
@@ -1358,9 +1425,9 @@ sr_status_t sr_fmg_profile_select(sr_fmg_t* h, int32_t kernel_class, int32_t lev
   if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
   h->prof_cls = kernel_class;
   h->prof_level = level;
-  if (h->gexec) {
-    cudaGraphExecDestroy(h->gexec);
-    h->gexec = nullptr;
+  for (auto& g : h->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
   }
   return SR_OK;
 }
