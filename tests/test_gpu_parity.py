@@ -428,3 +428,53 @@ def test_host_async_pipeline_matches_device_solves():
         # the synchronous wrapper still works after the pipeline
         u = s.solve_host(fs[1])
         assert np.array_equal(u.numpy(), ref[1])
+
+
+# ---- BASELINE configs[4] (C5) parameter sets at 256^3 against the oracle (the 1024^3
+# oracle does not fit this test's time budget): 16 Gaussian bumps, J = 2, S = 32 (8^3
+# segments; E = 38 boxes) and S = 128 (2^3 segments; E = 134 boxes -> generic fused path)
+C5_CASES = [
+    ("S32-K3", (256, 256, 256), 7, 32, 2, 3),
+    ("S128-K5", (256, 256, 256), 7, 128, 2, 5),
+]
+
+
+@pytest.mark.parametrize("case", C5_CASES, ids=[c[0] for c in C5_CASES])
+def test_c5_shapes_at_256_match_oracle(case):
+    name, n, M, seg, J, K = case
+    f = W.make_rhs("bumps", n)
+    ref = _oracle("bumps", f, n, M, seg, J, K)
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
+    assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
+
+
+def test_c4_two_ranks_full_size_equal_single_gpu():
+    # BASELINE configs[3] (C4) at 2 GPUs: global 1024 x 512 x 512, h = 1/512, R = (2,1,1),
+    # manufactured f, 64^3 segments, J = 2, K = 4, M = 8 (coarsest 4 x 2 x 2).  Both ranks run
+    # on this GPU through the replay backend (no rank waits on another); each rank's block
+    # must equal the single-GPU solve of the same global problem.
+    from paper_1406_7808_b200 import ReplayStore
+    n, M, seg, J, K, pgrid, h = (1024, 512, 512), 8, 64, 2, 4, (2, 1, 1), 1.0 / 512
+    R = W.extents(n, h)
+    with Solver(n, M, seg=seg, buffer=J, K=K, h=h) as s1:
+        f = torch.from_numpy(W.manufactured_f_block(h, R, (0, 0, 0), n)).cuda()
+        single = s1.solve(f)
+        del f
+    store = ReplayStore(2)
+    ranks = [Solver(n, M, seg=seg, buffer=J, K=K, h=h, world=2, rank=r, pgrid=pgrid,
+                    replay_store=store) for r in range(2)]
+    fl = []
+    for s in ranks:
+        lo = [s.block_lo[d] - s.f_halo for d in range(3)]
+        dims = [s.block_n[d] + 2 * s.f_halo for d in range(3)]
+        fl.append(torch.from_numpy(W.manufactured_f_block(h, R, lo, dims)).cuda())
+    outs = None
+    for _ in range(ranks[0].exchanges_per_solve + 1):
+        outs = [s.solve(fl[r]) for r, s in enumerate(ranks)]
+    for r, s in enumerate(ranks):
+        lo, nb = s.block_lo, s.block_n
+        blk = single[lo[2]:lo[2] + nb[2], lo[1]:lo[1] + nb[1], lo[0]:lo[0] + nb[0]]
+        d = float(torch.linalg.vector_norm(outs[r] - blk) / torch.linalg.vector_norm(blk))
+        assert d <= 1e-13, (r, d)
+    for s in ranks:
+        s.close()
