@@ -91,7 +91,9 @@ struct PassGeom {
   static constexpr int OFF_C = OFF_F + RF * FPL;
   static size_t smem(int cpl) { return (size_t)(OFF_C + RC * NF * cpl) * sizeof(T) + 8 * NBAR; }
   static int crows() { return RW / 2 + 2; }
-  static constexpr int MINB = 1;  // (2 for Pi + S^1 spills and measured no faster)
+  // 1 CTA per SM for the chains (2 for Pi + S^1 spills and measured no faster); the plain
+  // residual + restriction pass (NSTEP = 0) fits two
+  static constexpr int MINB = NSTEP == 0 ? 2 : 1;
 };
 
 template <class T, int PY, int BH, int MAXS, int SRC, int NSTEP, int SINK, int RG, int CL>
@@ -105,7 +107,9 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
   constexpr bool COARSE = SRC != kSrcLoad;
   constexpr int NCR = MAXS / 2 + 2;  // coarse rows touched by a thread's MAXS fine rows
   static_assert(MAXS % 2 == 0 && MAXS <= 8, "MAXS even");
-  static_assert(NSTEP >= 1 && NSTEP <= 3, "1..3 steps");
+  static_assert(NSTEP >= 0 && NSTEP <= 3, "0..3 steps");
+  static_assert(NSTEP >= 1 || (SRC == kSrcLoad && SINK == kSinkRestrict),
+                "a pass without Chebyshev steps is the plain residual + restriction");
   extern __shared__ __align__(128) unsigned char sm[];
   T* const sbase = reinterpret_cast<T*>(sm);
   const Lvl& L = a.L;
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
         }
       }
     };
-    stage(std::integral_constant<int, 1>{});
+    if constexpr (NSTEP >= 1) stage(std::integral_constant<int, 1>{});
     if constexpr (NSTEP >= 2) stage(std::integral_constant<int, 2>{});
     if constexpr (NSTEP >= 3) stage(std::integral_constant<int, 3>{});
     // ------------------------------------------------------------ residual + restriction
@@ -522,8 +526,9 @@ __global__ void __launch_bounds__(PassGeom<T, PY, BH, MAXS, SRC, NSTEP, SINK, RG
         const int gz = oz + zr;
         const bool zc = zr >= 1 && zr <= Ez - 2 && gz >= 0 && gz < L.N[2];
         const T dz = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0));
-        const T* src = bufS + (2 * (NSTEP - 1) + (zr & 1)) * G::PL + po;
+        const T* src = sbase + in_off(NS, zr) + po;  // input of the residual stage
         const T* fp = bufF + (zr % G::RF) * G::FPL + fo;
+        if (NSTEP == 0) mbar_wait(&barF[zr % G::RF], (zr / G::RF) & 1);
         const unsigned act = zc ? (cmk & vm[NS]) : 0u;
         T rv[MAXS];
 #pragma unroll
@@ -649,7 +654,7 @@ bool inst(const PassSpec<T>& ps, cudaStream_t st, bool launch) {
   a.rc = ps.rc;
   a.jr = ps.jr;
   for (int i = 0; i < 3; ++i) a.cr[i] = (T)ps.cr[i];
-  a.cm = (T)(NSTEP >= 2 ? ps.cm[NSTEP - 1] : 0.0);
+  a.cm = (T)(NSTEP >= 2 ? ps.cm[NSTEP >= 2 ? NSTEP - 1 : 0] : 0.0);
   a.fin = ps.fin;
   for (int d = 0; d < 3; ++d) a.foff[d] = ps.rhs.global ? ps.rhs.off[d] : 0;
   CUtensorMap map;
@@ -707,6 +712,8 @@ bool by_geom(const PassSpec<T>& ps, cudaStream_t st, bool launch) {
     cl = (e && e[0] == '1') ? 1 : 0;
   }
   if (cl) return inst<T, 72, 14, 4, SRC, NSTEP, SINK, RG, 1>(ps, st, launch);
+  if constexpr (NSTEP == 0)  // the plain residual + restriction also on E = 38 boxes
+    if (inst<T, 40, 12, 4, SRC, NSTEP, SINK, RG, 0>(ps, st, launch)) return true;
   return inst<T, 72, 14, 4, SRC, NSTEP, SINK, RG, 0>(ps, st, launch);
 }
 
@@ -720,6 +727,9 @@ bool dispatch(const PassSpec<T>& ps, cudaStream_t st, bool launch) {
                : by_geom<T, kSrcPadd, 2, kSinkStore, 0>(ps, st, launch);
     case kSrcPadd * 100 + 20 + kSinkFinal:
       return g && by_geom<T, kSrcPadd, 2, kSinkFinal, 1>(ps, st, launch);
+    case kSrcLoad * 100 + 0 + kSinkRestrict:
+      return g ? by_geom<T, kSrcLoad, 0, kSinkRestrict, 1>(ps, st, launch)
+               : by_geom<T, kSrcLoad, 0, kSinkRestrict, 0>(ps, st, launch);
     case kSrcLoad * 100 + 20 + kSinkRestrict:
       return g ? by_geom<T, kSrcLoad, 2, kSinkRestrict, 1>(ps, st, launch)
                : by_geom<T, kSrcLoad, 2, kSinkRestrict, 0>(ps, st, launch);

@@ -107,6 +107,8 @@ struct sr_fmg {
   int pass_entry = 0;      // 0: unfused entry
   bool pass_down = false;  // (LOAD, 2, RESTRICT)
   bool pass_up = false;    // (PADD, 2, STORE|FINAL)
+  bool pass_restrict = false;  // (LOAD, 0, RESTRICT) for the restriction (SR_FMG_PASS_RESTRICT=1;
+                              // measured equal to k_restrict in fp64, slower in fp32)
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
   // disables it.  flush_fn: enqueue the recorded operations (called before every launch)
   bool cexec = true;
@@ -744,13 +746,17 @@ struct Schedule {
     if (src == srfmg::kSrcLoad) { words = 2.0 * c.cg + c.compute; cls = KC_PASS_DOWN; }
     if (src == srfmg::kSrcPadd) { words = 2.0 * cgc + c.cg + c.compute; cls = KC_PASS_UP; }
     if (sink == srfmg::kSinkRestrict) words += c.compute / 4.0;
+    if (nstep == 0) {  // plain residual + restriction: reads u over C and b, writes coarse
+      words = c.compute * (2.0 + 0.25);
+      cls = KC_RESTRICT;
+    }
     if (sink == srfmg::kSinkFinal) {
       ps.fin.p = final_out;
       for (int i = 0; i < 3; ++i) ps.fin.bo[i] = h->blk_lo[i];
       ps.fin.sy = h->blk_n[0];
       ps.fin.sz = (long long)h->blk_n[0] * h->blk_n[1];
       words += (double)h->blk_n[0] * h->blk_n[1] * h->blk_n[2];
-    } else {
+    } else if (nstep > 0) {
       words += c.cg;
     }
     {
@@ -762,11 +768,18 @@ struct Schedule {
       srfmg::launch_merge_f<T>(L, h->L[l - 1], (const T*)h->B[l - 1].t, U(l - 1), ps.jr, st);
     }
     if (sink == srfmg::kSinkFinal) final_done = true;
-    else bb.cur = 1 - bb.cur;
+    else if (nstep > 0) bb.cur = 1 - bb.cur;  // (no steps: u unchanged, not written)
   }
 
   void restrict_std(int l, View<T> b) {
     const int jr = jr_for(l);
+    if (h->fused && h->pass_restrict && l > h->T && tma_rhs_ok(b) &&
+        (h->force || (long long)h->L[l].nsegs * ((h->L[l].E[1] + 13) / 14) >= 148) &&
+        srfmg::pass_ok<T>(srfmg::kSrcLoad, 0, srfmg::kSinkRestrict, h->L[l], h->L[l - 1],
+                          b.global)) {
+      run_pass(l, srfmg::kSrcLoad, 0, srfmg::kSinkRestrict, b);  // TMA-fed residual+restrict
+      return;
+    }
     if (cx(l) && cx(l - 1)) {
       srfmg::COp<T> o = cop(srfmg::kCopRestrict, l, l - 1);
       o.a = U(l);
@@ -1119,6 +1132,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_PASS_ENTRY")) h->pass_entry = std::atoi(e);
   if (const char* e = std::getenv("SR_FMG_PASS_DOWN")) h->pass_down = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PASS_UP")) h->pass_up = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_PASS_RESTRICT")) h->pass_restrict = std::atoi(e) != 0;
   h->pass = h->fused && (h->pass_entry || h->pass_down || h->pass_up);
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);

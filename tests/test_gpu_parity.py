@@ -382,6 +382,19 @@ def test_fused_passes_match_oracle(case, mode, cl, monkeypatch):
     assert rel_l2(u, b) <= 1e-13, (name, mode, rel_l2(u, b))
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_restriction_pass_matches_oracle(dtype, monkeypatch):
+    # the TMA-fed residual + restriction pass (pass.cu with no Chebyshev steps) on the E = 70
+    # and E = 38 boxes, forced onto these small levels
+    n, M, seg, J, K, rhs = (128, 128, 128), 6, 64, 2, 3, "manufactured+noise"
+    f = W.make_rhs(rhs, n)
+    ref = _oracle(rhs, f, n, M, seg, J, K)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_PASS_RESTRICT", "1")
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    assert rel_l2(u, ref) <= (TOL64 if dtype == "f64" else TOL32), rel_l2(u, ref)
+
+
 @pytest.mark.parametrize("mode", ["1", "4"])
 def test_fused_passes_fp32(mode, monkeypatch):
     n, M, seg, J, K, rhs = (128, 128, 128), 6, 64, 2, 2, "manufactured+noise"
