@@ -273,7 +273,7 @@ struct SpecGeom {
   static constexpr int RU = NST == 1 ? 5 : 3, RF = NST == 1 ? 5 : 4, NU1 = NST == 1 ? 0 : 3;
   static constexpr size_t SMEM =
       (size_t)(RU * U0S + RF * FS + NU1 * U1S) * sizeof(T) + 8 * (RU + RF);
-  // CTAs per SM the smem allows (capped at 3: registers)
+  // CTAs per SM the smem allows (capped at 3: registers; more measured no faster)
   static constexpr int MINB = SMEM <= 75 * 1024 ? 3 : SMEM <= 113 * 1024 ? 2 : 1;
 };
 
@@ -621,6 +621,18 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
   if (alt == 1 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
   if (alt == 2 && try_spec<T, 72, 18, 4>(L, a, b, nst, st)) return true;
   if (alt == 3 && try_spec<T, 72, 24, 4>(L, a, b, nst, st)) return true;
+  // E = 38 / 22 boxes (32^3 / 16^3 segments): SR_FMG_CHEB2_ALT40 / _ALT24 pick band shapes
+  static int a40 = -1, a24 = -1;
+  if (a40 < 0) {
+    const char* e = std::getenv("SR_FMG_CHEB2_ALT40");
+    a40 = e ? std::atoi(e) : 0;
+    const char* f = std::getenv("SR_FMG_CHEB2_ALT24");
+    a24 = f ? std::atoi(f) : 0;
+  }
+  if (a40 == 1 && try_spec<T, 40, 13, 4>(L, a, b, nst, st)) return true;
+  if (a40 == 2 && try_spec<T, 40, 10, 4>(L, a, b, nst, st)) return true;
+  if (a24 == 1 && try_spec<T, 24, 11, 4>(L, a, b, nst, st)) return true;
+  if (a24 == 2 && try_spec<T, 24, 8, 3>(L, a, b, nst, st)) return true;
   if constexpr (sizeof(T) == 8)
     return try_spec<T, 72, 35, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
            try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);

@@ -1,3 +1,2 @@
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_e0.log 2>&1
-SR_FMG_PASS_ENTRY=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_e1.log 2>&1
-SR_FMG_PASS_ENTRY=1 timeout 300 python tools/breakdown.py > gpurun_out/breakdown_e1.log 2>&1
+for a in 0 1 2; do SR_FMG_CHEB2_ALT40=$a timeout 300 python tools/breakdown.py > gpurun_out/bd_a40_$a.log 2>&1; done
+for a in 1 2; do SR_FMG_CHEB2_ALT24=$a timeout 300 python tools/breakdown.py > gpurun_out/bd_a24_$a.log 2>&1; done
