@@ -66,7 +66,9 @@ typedef struct {
   int32_t buffer;     /* J: buffer cells on every SR level (Eq. 5 with A = J, B = 0)     */
   int32_t sr_levels;  /* K: number of SR levels, 0 <= K <= M (0 = conventional FMG)      */
   int32_t sched_A;    /* Eq. 5 buffer schedule J_k = 2 floor((A + B (K-k))/2)            */
-  int32_t sched_B;    /*   (PAPER.md:192); (-1, -1) = constant `buffer`                  */
+  int32_t sched_B;    /*   (PAPER.md:192); (-1, -1) = constant `buffer`; sched_B = -2:    */
+                      /*   maximum buffer schedule J_k = 2^(k-1) J_1 with J_1 = sched_A  */
+                      /*   (C_k = F_k for k < K)                        */
   int32_t dtype;      /* sr_dtype_t                                                       */
   double h;           /* fine cell size; 0 = 1/n[0] (unit cube for cubic grids)          */
   int32_t alpha;      /* F(alpha, nu1, nu2) Chebyshev degrees;       */

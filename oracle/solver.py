@@ -33,7 +33,7 @@ class Config:
     buffer: int = 2                  # J (constant buffer, Eq. 5 with A = J, B = 0)
     K: int = 0                       # number of SR levels (0 = conventional FMG)
     h: Optional[float] = None        # fine cell size (default 1/n1)
-    sched: Optional[Tuple[int, int]] = None   # Eq. 5 (A, B); overrides `buffer`
+    sched: Optional[Tuple] = None    # Eq. 5 (A, B), or ("mbs", J1); overrides `buffer`
     alpha: int = 1                   # F(alpha, nu1, nu2)
     nu1: int = 2
     nu2: int = 2
@@ -56,9 +56,14 @@ class Config:
             raise ValueError("buffer must be >= 0")
 
     def J(self, k: int) -> int:
-        """Buffer width of SR level k (1..K): Eq. 5, PAPER.md:192 (R14)."""
+        """Buffer width of SR level k (1..K): Eq. 5, PAPER.md:192 (R14); or the maximum
+        buffer schedule (MBS): J_1 given and the finer buffers completely
+        support grid k = 1, i.e. C_k = F_k for k < K.  With F_k = grow(V_k, floor(J_{k+1}/2))
+        (R15) that is J_{k+1} = 2 J_k, so J_k = 2^(k-1) J_1."""
         if self.sched is None:
             return self.buffer
+        if self.sched[0] == "mbs":
+            return int(self.sched[1]) << (k - 1)
         A, B = self.sched
         return 2 * ((A + B * (self.K - k)) // 2)
 

@@ -41,7 +41,10 @@ def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha
         d.pgrid[i] = int(pgrid[i])
     d.M, d.seg, d.buffer, d.sr_levels = int(M), int(seg), int(buffer), int(K)
     if sched is not None:
-        d.sched_A, d.sched_B = int(sched[0]), int(sched[1])
+        if sched[0] == "mbs":  # maximum buffer schedule, J_k = 2^(k-1) J_1
+            d.sched_A, d.sched_B = int(sched[1]), -2
+        else:
+            d.sched_A, d.sched_B = int(sched[0]), int(sched[1])
     d.dtype = {"f64": _lib.SR_F64, "f32": _lib.SR_F32}[dtype]
     d.h = 0.0 if h is None else float(h)
     d.alpha, d.nu1, d.nu2 = int(alpha), int(nu1), int(nu2)

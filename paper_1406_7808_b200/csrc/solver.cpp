@@ -172,7 +172,11 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
     if (d->seg % (1 << d->sr_levels)) return bad("seg must be divisible by 2^sr_levels");
   }
   if (d->buffer < 0) return bad("buffer must be >= 0");
-  if ((d->sched_A < 0) != (d->sched_B < 0)) return bad("sched_A/sched_B: both or neither");
+  if (d->sched_B == -2) {
+    if (d->sched_A < 0) return bad("maximum buffer schedule (sched_B = -2) needs sched_A = J_1 >= 0");
+  } else if ((d->sched_A < 0) != (d->sched_B < 0)) {
+    return bad("sched_A/sched_B: both or neither");
+  }
   if (d->dtype != SR_F64 && d->dtype != SR_F32) return bad("dtype must be SR_F64 or SR_F32");
   if (d->h < 0 || !std::isfinite(d->h)) return bad("h must be >= 0 and finite");
   if (d->alpha < 0 || d->nu1 < 0 || d->nu2 < 0) return bad("Chebyshev degrees must be >= 0");
@@ -200,6 +204,7 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
 }
 
 int buffer_of(const sr_fmg_desc_t* d, int k) {  // Eq. 5
+  if (d->sched_B == -2) return d->sched_A << (k - 1);  // MBS: J_k = 2^(k-1) J_1
   if (d->sched_A < 0) return d->buffer;
   return 2 * ((d->sched_A + d->sched_B * (d->sr_levels - k)) / 2);
 }

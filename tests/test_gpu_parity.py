@@ -89,6 +89,18 @@ def test_eq5_schedule_matches_oracle():
     assert rel_l2(u, ref) <= TOL64
 
 
+@pytest.mark.parametrize("J1", [1, 2])
+def test_mbs_schedule_matches_oracle(J1):
+    # maximum buffer schedule: J_k = 2^(k-1) J_1, C_k = F_k for k < K
+    n = (64, 64, 64)
+    f = W.make_rhs("manufactured+noise", n)
+    ref = _oracle("mn", f, n, 5, 16, 2, 3, sched=("mbs", J1))
+    with Solver(n, 5, seg=16, buffer=2, K=3, sched=("mbs", J1)) as s:
+        assert [s.level(l).buffer for l in (3, 4, 5)] == [J1, 2 * J1, 4 * J1]
+        u = s.solve(torch.from_numpy(f).cuda()).cpu().numpy()
+    assert rel_l2(u, ref) <= TOL64
+
+
 def test_graph_and_eager_and_host_paths_bitwise_equal():
     n = (64, 64, 64)
     f = W.make_rhs("manufactured+noise", n)

@@ -191,3 +191,40 @@ def test_paper_tables_fixture_is_context_only():
             col = [r[c] for r in rows if r[c] is not None]
             assert all(x >= y for x, y in zip(col, col[1:]))
     assert g["table2"]["e_r"] == sorted(g["table2"]["e_r"])
+
+
+# ---- maximum buffer schedule (MBS) ----------------
+@pytest.mark.parametrize("J1", [1, 2, 4])
+def test_mbs_compute_regions_equal_F(J1):
+    # "the rest of the SR buffers completely support grid k=1: pOmega^C_k = pOmega^F_k for
+    # k < K", checked on cell sets: F_k from the children of C_{k+1}
+    cfg = Config(n=(64, 64, 64), M=5, seg=32, K=3, sched=("mbs", J1))
+    o = Oracle(cfg)
+    assert [cfg.J(k) for k in (1, 2, 3)] == [J1, 2 * J1, 4 * J1]
+    for l in range(o.T + 2, o.M + 1):          # coarse level l-1 = T+1 .. M-1 (k < K)
+        for p in list(o.segs)[:3]:
+            C = _cells(o.C(l, p))
+            omc = _cells(o.dom[l - 1])
+            F = {I for I in omc
+                 if all((2 * I[0] + a, 2 * I[1] + b, 2 * I[2] + c) in C
+                        for a, b, c in itertools.product((0, 1), repeat=3))}
+            assert F == _cells(o.C(l - 1, p)), (l, p)
+    # the number of buffer cells grows exponentially toward the fine grid
+    assert cfg.J(3) == 4 * cfg.J(1)
+
+
+def test_mbs_error_ratio_trend():
+    # Table 3: with MBS (K fixed, J_1 = 4) the error ratio still grows as
+    # pN0V halves, and MBS is at least as accurate as the constant buffer J = J_1
+    n = (64, 64, 64)
+    f = W.manufactured_f(n, 1 / n[0])
+    u = W.manufactured_u(n, 1 / n[0])
+    e_conv = np.abs(O.solve(f, Config(n=n, M=5)) - u).max()
+
+    def er(S, sched=None, J=4):
+        return np.abs(O.solve(f, Config(n=n, M=5, seg=S, buffer=J, K=2, sched=sched)) - u).max() / e_conv
+
+    mbs = [er(S, ("mbs", 2)) for S in (32, 16, 8)]          # pN0V = 8, 4, 2
+    assert mbs[0] < mbs[1] < mbs[2], mbs
+    for S in (16, 8):
+        assert er(S, ("mbs", 2)) <= er(S, None, 2) + 1e-12
