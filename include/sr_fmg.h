@@ -156,6 +156,16 @@ sr_status_t sr_fmg_solve_host_async(sr_fmg_t *h, const void *f_host, void *u_hos
 /* Wait for every solve and copy enqueued on the handle; returns its sticky status. */
 sr_status_t sr_fmg_synchronize(sr_fmg_t *h);
 
+/* Conventional multigrid V-cycle solver, the paper's comparison solver ("V-cycle solve
+ * with a relative residual tolerance of 10^-4"): u = 0 on the fine grid,
+ * then V(nu1, nu2)-cycles (fig:mgv) until ||f - A u||_2 <= rtol ||f||_2 or maxit cycles.
+ * f, u: device pointers as in sr_fmg_solve.  Needs a handle with sr_levels = 0 and
+ * world = 1 (SR_ERR_UNSUPPORTED_CONFIG otherwise).  Synchronous (one device->host read of
+ * the residual norm per cycle).  *cycles = cycles run, *relres = final relative residual
+ * (either may be NULL). */
+sr_status_t sr_fmg_vsolve(sr_fmg_t *h, const void *f, void *u, double rtol, int32_t maxit,
+                          int32_t *cycles, double *relres);
+
 /* Change the stream later solves are ordered on (a captured graph is reused). */
 sr_status_t sr_fmg_set_stream(sr_fmg_t *h, void *stream);
 

@@ -9,7 +9,7 @@ both.
 Plain, slow, obviously-correct numpy in fp64: every function cites the PAPER.md passage it
 transcribes.  Pins: tests/test_oracle_*.py.  Parity status per function:
   fill_bc_ghosts, apply_A, cheb, restrict_avg8, prolong, exact_solve  -> pinned
-  Oracle.vconv / fmg_conventional                                     -> pinned
+  Oracle.vconv / fmg_conventional / vsolve                            -> pinned
   Oracle.vsr / solve (SR)                                             -> pinned by
       equivalences (huge buffer, one segment), region brute force, symmetry, O(h^2) and
       GSR-freeze invariants; the paper's e_r table values are for a different stencil,
@@ -18,10 +18,10 @@ transcribes.  Pins: tests/test_oracle_*.py.  Parity status p
 from .grid import Box, Field
 from .ops import (apply_A, cheb, cheb_constants, dense_operator, exact_solve, fill_bc_ghosts,
                   prolong, residual, restrict_avg8)
-from .solver import Config, Oracle, solve, vcycle_iterate
+from .solver import Config, Oracle, solve, vcycle_iterate, vsolve
 
 __all__ = [
     "Box", "Field", "apply_A", "cheb", "cheb_constants", "dense_operator", "exact_solve",
     "fill_bc_ghosts", "prolong", "residual", "restrict_avg8", "Config", "Oracle", "solve",
-    "vcycle_iterate",
+    "vcycle_iterate", "vsolve",
 ]

@@ -297,3 +297,27 @@ def vcycle_iterate(f: np.ndarray, cfg: Config, cycles: int, u0: Optional[np.ndar
         o.vconv(M, o.f[M])
         its.append(o.u[M][o.dom[M]].copy())
     return its
+
+
+def vsolve(f: np.ndarray, cfg: Config, rtol: float = 1e-4, maxit: int = 50):
+    """Conventional V-cycle solver: "the solve times for a V-cycle
+    solve with a relative residual tolerance of 10^-4".  From u = 0 on
+    Omega_M, repeat FASMGV(M) (fig:mgv) until ||f - A u||_2 / ||f||_2 <=
+    rtol (reading R26: 2-norm over the fine grid, checked before every cycle).
+
+    Returns (u, cycles, history of the relative residual norms, one per check).
+    """
+    o = Oracle(Config(**{**cfg.__dict__, "K": 0}))
+    M, dom, h = o.M, o.dom[o.M], o.h[o.M]
+    fM = Field(dom, array=np.asarray(f, dtype=np.float64).copy())
+    o.f = {M: fM}
+    u = o.u[M]
+    u[dom] = 0.0
+    fn = float(np.linalg.norm(fM[dom]))
+    hist = []
+    for it in range(maxit + 1):
+        rel = float(np.linalg.norm(residual(u, fM, dom, h, dom))) / fn
+        hist.append(rel)
+        if rel <= rtol or it == maxit:
+            return u[dom].copy(), it, hist
+        o.vconv(M, fM)

@@ -25,7 +25,7 @@ EXPORTED = [
     "sr_fmg_debug_level_io", "sr_fmg_debug_op", "sr_fmg_profile_select", "sr_fmg_profile_read",
     "sr_fmg_partition", "sr_fmg_nccl_unique_id", "sr_fmg_replay_store_create",
     "sr_fmg_replay_store_destroy", "sr_fmg_set_replay", "sr_fmg_solve_host_async",
-    "sr_fmg_synchronize",
+    "sr_fmg_synchronize", "sr_fmg_vsolve",
 ]
 
 
@@ -90,6 +90,7 @@ def _load():
         "sr_fmg_solve_host": (I32, [P, P, P]),
         "sr_fmg_solve_host_async": (I32, [P, P, P]),
         "sr_fmg_synchronize": (I32, [P]),
+        "sr_fmg_vsolve": (I32, [P, P, P, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]),
         "sr_fmg_set_stream": (I32, [P, P]),
         "sr_fmg_destroy": (None, [P]),
         "sr_fmg_get_info": (I32, [P, ctypes.POINTER(Info)]),

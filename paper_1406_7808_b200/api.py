@@ -258,6 +258,23 @@ class Solver:
     def synchronize(self):
         check(lib.sr_fmg_synchronize(self._h), self._h)
 
+    def vsolve(self, f, out=None, rtol=1e-4, maxit=50):
+        """Conventional V-cycle solver (sr_fmg_vsolve; needs K = 0): returns
+        (u, cycles, relative residual)."""
+        import torch
+        want = torch.float64 if self.dtype == "f64" else torch.float32
+        if not f.is_cuda or f.dtype != want or not f.is_contiguous():
+            raise ValueError("f must be a contiguous CUDA tensor of the solver's dtype")
+        if out is None:
+            out = torch.empty(self.shape, dtype=want, device=f.device)
+        check(lib.sr_fmg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+              self._h)
+        cyc, rel = ctypes.c_int32(0), ctypes.c_double(0.0)
+        check(lib.sr_fmg_vsolve(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                float(rtol), int(maxit), ctypes.byref(cyc), ctypes.byref(rel)),
+              self._h)
+        return out, int(cyc.value), float(rel.value)
+
     # -- test / profiling hooks ----------------------------------------------------------
     def level_storage(self, l, field=0) -> np.ndarray:
         """Internal storage of level l (field 0 = u, 1 = rhs, 2 = t) as an array of shape

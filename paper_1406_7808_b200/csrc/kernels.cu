@@ -500,6 +500,35 @@ __global__ void __launch_bounds__(kThreads) k_pyramid(const T* __restrict__ ff, 
   }
 }
 
+// sum over Omega of (b - A u)^2 on a conventional (single-segment) level, accumulated in
+// fp64 into acc[0] (V-cycle solver stopping test, reading R26)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_resnorm(Lvl L, const T* __restrict__ u, View<T> b,
+                                                      double* acc) {
+  const long long n = (long long)L.N[0] * L.N[1] * L.N[2];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g[3] = {(int)(i % L.N[0]), (int)((i / L.N[0]) % L.N[1]),
+                      (int)(i / ((long long)L.N[0] * L.N[1]))};
+    const int a[3] = {g[0] + 1, g[1] + 1, g[2] + 1};
+    const long long off = loc_off(L, 0, a[0], a[1], a[2]);
+    const double r = (double)(view_at(b, 0, a, g) - apply_A(L, u, off, g));
+    s += r * r;
+  }
+  __shared__ double red[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) atomicAdd(acc, s);
+  }
+}
+
 // output: genuine cells of each segment -> user u (R19); one thread per
 // genuine (x, y) column of a segment, marching z.
 template <class T>
@@ -608,6 +637,13 @@ void launch_pyramid(const T* ff, int nfx, int nfy, int nfz, T* fc, cudaStream_t 
 }
 
 template <class T>
+void launch_resnorm(const Lvl& L, const T* u, View<T> b, double* acc, cudaStream_t st) {
+  const long long n = (long long)L.N[0] * L.N[1] * L.N[2];
+  const unsigned g = (unsigned)std::min<long long>(148LL * 8, (n + kThreads - 1) / kThreads);
+  k_resnorm<T><<<std::max(g, 1u), kThreads, 0, st>>>(L, u, b, acc);
+}
+
+template <class T>
 void launch_gather(const Lvl& L, const T* useg, T* out, const int bo[3], long long sy,
                    long long sz, cudaStream_t st) {
   const ColCfg c = col_cfg(L.S[0], L.S[1], L.S[2], L.nsegs);
@@ -635,6 +671,7 @@ void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const
                                   cudaStream_t);                                               \
   template void launch_coarsest<T>(const Lvl&, T*, View<T>, const T*, cudaStream_t);            \
   template void launch_pyramid<T>(const T*, int, int, int, T*, cudaStream_t);                   \
+  template void launch_resnorm<T>(const Lvl&, const T*, View<T>, double*, cudaStream_t);        \
   template void launch_gather<T>(const Lvl&, const T*, T*, const int*, long long, long long,      \
                                  cudaStream_t);                                                  \
   template void launch_box_copy<T>(T*, long long, long long, const int*, const int*, T*, int,    \

@@ -57,6 +57,9 @@ template <class T>
 void launch_coarsest(const Lvl& L0, T* u, View<T> b, const T* ainv, cudaStream_t st);
 template <class T>
 void launch_pyramid(const T* ff, int nfx, int nfy, int nfz, T* fc, cudaStream_t st);
+// acc[0] += sum over Omega of (b - A u)^2 (single-segment level, fp64 accumulation)
+template <class T>
+void launch_resnorm(const Lvl& L, const T* u, View<T> b, double* acc, cudaStream_t st);
 // out: this rank's dense output block; (bo, sy, sz): its global origin and strides
 template <class T>
 void launch_gather(const Lvl& L, const T* useg, T* out, const int bo[3], long long sy,

@@ -1263,6 +1263,73 @@ sr_status_t sr_fmg_solve(sr_fmg_t* h, const void* f, void* u) {
   return SR_OK;
 }
 
+// Conventional V-cycle solver: u = 0, then FASMGV(M) until
+// ||f - A u||_2 / ||f||_2 <= rtol (reading R26), at most maxit cycles.  Eager launches; one
+// host synchronisation per cycle for the stopping test.
+sr_status_t sr_fmg_vsolve(sr_fmg_t* h, const void* f, void* u, double rtol, int32_t maxit,
+                          int32_t* cycles, double* relres) {
+  if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->sticky != SR_OK) return h->sticky;
+  if (!f || !u) return fail(h, SR_ERR_INVALID_ARGUMENT, "f or u is NULL");
+  if (!(rtol >= 0) || maxit < 0) return fail(h, SR_ERR_INVALID_ARGUMENT, "need rtol >= 0, maxit >= 0");
+  if (h->K != 0 || h->world != 1)
+    return fail(h, SR_ERR_UNSUPPORTED_CONFIG,
+                "the V-cycle solver runs on a conventional (sr_levels = 0) single-GPU handle");
+  cudaStream_t st = h->stream;
+  double* acc = nullptr;
+  CU(h, cudaMalloc(&acc, 2 * sizeof(double)));
+  auto body = [&](auto tag) -> sr_status_t {
+    using T = decltype(tag);
+    Schedule<T> s{h, st, (const T*)f, (double)sizeof(T)};
+    s.bind();
+    const int M = h->M;
+    const Lvl& L = h->L[M];
+    LevelBufs& bb = h->B[M];
+    for (int l = 0; l <= M; ++l) h->B[l].cur = 0;
+    CU(h, cudaMemsetAsync(bb.u[0], 0, (size_t)L.ss * L.nsegs * sizeof(T), st));
+    CU(h, cudaMemsetAsync(bb.u[1], 0, (size_t)L.ss * L.nsegs * sizeof(T), st));
+    // the R6 pyramid is not used: the coarse rhs are the tau right-hand sides
+    auto norm2 = [&](double& out) -> sr_status_t {
+      s.flush();
+      CU(h, cudaMemsetAsync(acc, 0, sizeof(double), st));
+      srfmg::launch_resnorm<T>(L, s.U(M), s.fview(M), acc, st);
+      h->launches++;
+      double hv = 0;
+      CU(h, cudaMemcpyAsync(&hv, acc, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CU(h, cudaStreamSynchronize(st));
+      out = std::sqrt(hv);
+      return SR_OK;
+    };
+    double fn = 0, rn = 0;
+    sr_status_t r = norm2(fn);  // u = 0: the residual is f
+    if (r != SR_OK) return r;
+    int it = 0;
+    double rel = fn > 0 ? 1.0 : 0.0;
+    for (;; ++it) {
+      if (it > 0) {
+        r = norm2(rn);
+        if (r != SR_OK) return r;
+        rel = fn > 0 ? rn / fn : 0.0;
+      }
+      if (rel <= rtol || it == maxit) break;
+      s.vcycle(M, s.fview(M));  // fig:mgv from level M
+    }
+    s.flush();
+    srfmg::launch_gather<T>(L, s.U(M), (T*)u, h->blk_lo, h->blk_n[0],
+                            (long long)h->blk_n[0] * h->blk_n[1], st);
+    h->launches++;
+    s.unbind();
+    if (cycles) *cycles = it;
+    if (relres) *relres = rel;
+    return SR_OK;
+  };
+  sr_status_t r = h->esize == 8 ? body(double{}) : body(float{});
+  cudaFree(acc);
+  if (r != SR_OK) return r;
+  CU(h, cudaGetLastError());
+  return SR_OK;
+}
+
 sr_status_t sr_fmg_solve_host_async(sr_fmg_t* h, const void* f_host, void* u_host) {
   if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
   if (h->sticky != SR_OK) return h->sticky;

@@ -503,3 +503,31 @@ def test_c4_two_ranks_full_size_equal_single_gpu():
         assert d <= 1e-13, (r, d)
     for s in ranks:
         s.close()
+
+
+# ---- conventional V-cycle solver ----------------------------
+@pytest.mark.parametrize("rhs", ["manufactured+noise", "bumps"])
+@pytest.mark.parametrize("rtol", [1e-4, 1e-8])
+def test_vsolve_matches_oracle(rhs, rtol):
+    n, M = (64, 64, 64), 5
+    f = W.make_rhs(rhs, n)
+    ref, cyc, hist = O.vsolve(f, O.Config(n=n, M=M), rtol=rtol, maxit=40)
+    with Solver(n, M, K=0) as s:
+        u, gcyc, grel = s.vsolve(torch.from_numpy(f).cuda(), rtol=rtol, maxit=40)
+        u = u.cpu().numpy()
+    assert gcyc == cyc, (gcyc, cyc)
+    assert grel == pytest.approx(hist[-1], rel=1e-6)
+    assert rel_l2(u, ref) <= TOL64
+
+
+def test_vsolve_fp32_and_unsupported_sr_handle():
+    n, M = (64, 64, 64), 5
+    f = W.make_rhs("manufactured+noise", n)
+    ref, cyc, _ = O.vsolve(f, O.Config(n=n, M=M), rtol=1e-4)
+    with Solver(n, M, K=0, dtype="f32") as s:
+        u, gcyc, _ = s.vsolve(torch.from_numpy(f.astype(np.float32)).cuda(), rtol=1e-4)
+    assert gcyc == cyc and rel_l2(u.double().cpu().numpy(), ref) <= TOL32
+    from paper_1406_7808_b200 import SrError
+    with Solver(n, M, seg=16, buffer=2, K=2) as s:
+        with pytest.raises(SrError):
+            s.vsolve(torch.from_numpy(f).cuda())

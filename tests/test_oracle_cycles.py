@@ -129,3 +129,29 @@ def test_fmg_non_cubic_domain():
         assert np.abs(ufmg - ustar).max() < 3.0 * np.abs(ustar - u).max()
         errs.append(np.abs(ufmg - u).max())
     assert 2.5 < errs[0] / errs[1] < 4.6
+
+
+# ---- conventional V-cycle solver to a relative residual tolerance
+def test_vsolve_converges_to_the_exact_discrete_solution():
+    # against the exact discrete solution (DST, tests/pins.py): independent of the cycle
+    from tests.pins import dst_solve
+    n = (32, 32, 32)
+    f = W.make_rhs("manufactured+noise", n)
+    ustar = dst_solve(f, 1.0 / n[0])
+    u, it, hist = O.vsolve(f, Config(n=n, M=4), rtol=1e-10, maxit=40)
+    assert hist[-1] <= 1e-10 and it < 40
+    assert np.linalg.norm(u - ustar) / np.linalg.norm(ustar) < 1e-8
+    # geometric reduction by about the measured V(2,2) contraction (Gamma < 0.25, L151)
+    ratios = [b / a for a, b in zip(hist[1:], hist[2:])]
+    assert max(ratios) < 0.3, ratios
+
+
+def test_vsolve_tolerance_semantics():
+    n = (32, 32, 32)
+    f = W.make_rhs("bumps", n)
+    u, it, hist = O.vsolve(f, Config(n=n, M=4), rtol=1e-4)
+    assert hist[0] == pytest.approx(1.0) and hist[-1] <= 1e-4 < hist[-2]
+    assert len(hist) == it + 1
+    # a tolerance the zero guess already meets needs no cycle
+    u0, it0, _ = O.vsolve(f, Config(n=n, M=4), rtol=1.0)
+    assert it0 == 0 and np.all(u0 == 0)
