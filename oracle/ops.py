@@ -8,9 +8,12 @@ listed in DESIGN.md §3).  Plain numpy slicing; no blocking, fusion or reorderin
                   operator application": u_ghost = -u_mirror (linear through 0 at the face),
                   per dimension sequentially => (-1)^m u_mirror at edges/corners.
   apply_A         R1/R2: A = -Lap_h, 7-point cell-centred FD on h_l (PAPER.md:51-70, Eq. 2;
-                  re-discretised coarse operators PAPER.md:91).
+                  re-discretised coarse operators PAPER.md:91); or the
+                  paper's "27-point stencil, second order" (PAPER.md:259) with SPEC's
+                  trilinear FE/FV weights: centre 8/3, faces 0, edges -1/6, corners -1/12.
   cheb            R8: PAPER.md:133, 257 (§5.1) Chebyshev smoother of degree d on
-                  [lo_frac, hi_frac] * lambda_max, lambda_max = 12/h^2.
+                  [lo_frac, hi_frac] * lambda_max, lambda_max = 12/h^2 (7-point) or 4/h^2
+                  (27-point: the supremum of its symbol, R28).
   restrict_avg8   R9: "simple averaging"/"piecewise constant restriction".
   prolong         R10: "linear prolongation": cell-centred trilinear,
                   1D weights 3/4 (parent) and 1/4 (neighbour on the child's side).
@@ -52,32 +55,57 @@ def fill_bc_ghosts(u: Field, domain: Box) -> None:
             a[tuple(gi)] = -a[tuple(mi)]
 
 
-def apply_A(u: Field, X: Box, h: float) -> np.ndarray:
-    """(A u)_i = (6 u_i - sum_{+-e_d} u_{i+-e_d}) / h^2 on X (R1, R2).
+def _shift(u: Field, X: Box, o) -> np.ndarray:
+    return u[Box([a + d for a, d in zip(X.lo, o)], [b + d for b, d in zip(X.hi, o)])]
 
-    Reads u on grow(X,1) as stored (ghosts must have been filled by the caller).
+
+def apply_A(u: Field, X: Box, h: float, stencil: str = "7pt") -> np.ndarray:
+    """(A u)_i on X, A = -L_h (R1, R2).
+
+    7pt:  (6 u_i - sum_{+-e_d} u_{i+-e_d}) / h^2.
+    27pt: (8/3 u_i - 1/6 sum_{12 edge neighbours} - 1/12 sum_{8 corner neighbours}) / h^2,
+          face neighbours weight 0 (SPEC "Stencil weights"; R28).
+    Reads u on grow(X,1) as stored (ghosts, incl. edges/corners, filled by the caller).
     """
     c = u[X]
     s = np.zeros(X.shape)
-    for d in range(3):
-        for o in (-1, 1):
-            lo = list(X.lo)
-            hi = list(X.hi)
-            lo[d] += o
-            hi[d] += o
-            s = s + u[Box(lo, hi)]
-    return (6.0 * c - s) / (h * h)
+    if stencil == "7pt":
+        for d in range(3):
+            for o in (-1, 1):
+                off = [0, 0, 0]
+                off[d] = o
+                s = s + _shift(u, X, off)
+        return (6.0 * c - s) / (h * h)
+    if stencil != "27pt":
+        raise ValueError(f"unknown stencil {stencil!r}")
+    e = np.zeros(X.shape)
+    k = np.zeros(X.shape)
+    for o in itertools.product((-1, 0, 1), repeat=3):
+        nz = sum(1 for v in o if v)
+        if nz == 2:
+            e = e + _shift(u, X, o)
+        elif nz == 3:
+            k = k + _shift(u, X, o)
+    return ((8.0 / 3.0) * c - e / 6.0 - k / 12.0) / (h * h)
 
 
-def residual(u: Field, b: Field, X: Box, h: float, domain: Box) -> np.ndarray:
+def residual(u: Field, b: Field, X: Box, h: float, domain: Box, stencil: str = "7pt") -> np.ndarray:
     """r = b - A u on X (fig:mgv PAPER.md:113)."""
     fill_bc_ghosts(u, domain)
-    return b[X] - apply_A(u, X, h)
+    return b[X] - apply_A(u, X, h, stencil)
 
 
-def cheb_constants(h: float, lo_frac: float, hi_frac: float):
-    """theta, delta, sigma of the Chebyshev interval [a, b] (R8; lambda_max = 12/h^2)."""
-    lam = 12.0 / (h * h)
+def lambda_max(h: float, stencil: str = "7pt") -> float:
+    """Largest eigenvalue bound of A_l (Appendix A of SURVEY): 12/h^2 for the 7-point
+    operator (attained); for the 27-point operator the supremum of its symbol
+    (8/3 - 2/3 (c1c2 + c2c3 + c1c3) - 2/3 c1c2c3)/h^2 over c_d in [-1, 1], which is 4/h^2
+    at (c1, c2, c3) = (-1, 1, 1) (R28)."""
+    return (12.0 if stencil == "7pt" else 4.0) / (h * h)
+
+
+def cheb_constants(h: float, lo_frac: float, hi_frac: float, stencil: str = "7pt"):
+    """theta, delta, sigma of the Chebyshev interval [a, b] (R8; lambda_max per stencil)."""
+    lam = lambda_max(h, stencil)
     a, b = lo_frac * lam, hi_frac * lam
     theta = 0.5 * (b + a)
     delta = 0.5 * (b - a)
@@ -85,7 +113,7 @@ def cheb_constants(h: float, lo_frac: float, hi_frac: float):
 
 
 def cheb(deg: int, u: Field, b: Field, X: Box, h: float, domain: Box,
-         lo_frac: float, hi_frac: float) -> None:
+         lo_frac: float, hi_frac: float, stencil: str = "7pt") -> None:
     """u <- S^deg(L, u, b) on X: one degree-`deg` Chebyshev polynomial (R8).
 
     Three-term Chebyshev recurrence:  x1 = x0 + r0/theta;
@@ -96,18 +124,18 @@ def cheb(deg: int, u: Field, b: Field, X: Box, h: float, domain: Box,
     """
     if deg <= 0:
         return
-    theta, delta, sigma = cheb_constants(h, lo_frac, hi_frac)
+    theta, delta, sigma = cheb_constants(h, lo_frac, hi_frac, stencil)
     x_prev = u.copy()
     fill_bc_ghosts(x_prev, domain)
     x = x_prev.copy()
-    x[X] = x_prev[X] + (b[X] - apply_A(x_prev, X, h)) / theta
+    x[X] = x_prev[X] + (b[X] - apply_A(x_prev, X, h, stencil)) / theta
     rho_prev = 1.0 / sigma
     for _ in range(1, deg):
         rho = 1.0 / (2.0 * sigma - rho_prev)
         fill_bc_ghosts(x, domain)
         x_new = x.copy()
         x_new[X] = (x[X] + rho * rho_prev * (x[X] - x_prev[X])
-                    + (2.0 * rho / delta) * (b[X] - apply_A(x, X, h)))
+                    + (2.0 * rho / delta) * (b[X] - apply_A(x, X, h, stencil)))
         x_prev, x, rho_prev = x, x_new, rho
     u[X] = x[X]
 
@@ -144,7 +172,7 @@ def prolong(src: Field, Y: Box) -> np.ndarray:
     return out
 
 
-def dense_operator(domain: Box, h: float) -> np.ndarray:
+def dense_operator(domain: Box, h: float, stencil: str = "7pt") -> np.ndarray:
     """The matrix of A on a (tiny) domain, column j = A e_j (used for the exact solve)."""
     n = domain.volume
     A = np.zeros((n, n))
@@ -152,11 +180,11 @@ def dense_operator(domain: Box, h: float) -> np.ndarray:
         e = Field(domain.grow(1), fill=0.0)
         e.a[1:-1, 1:-1, 1:-1].flat[j] = 1.0
         fill_bc_ghosts(e, domain)
-        A[:, j] = apply_A(e, domain, h).ravel()
+        A[:, j] = apply_A(e, domain, h, stencil).ravel()
     return A
 
 
-def exact_solve(b: np.ndarray, domain: Box, h: float) -> np.ndarray:
+def exact_solve(b: np.ndarray, domain: Box, h: float, stencil: str = "7pt") -> np.ndarray:
     """u = A^{-1} b on the coarsest grid (fig:mgv PAPER.md:121, R7): dense LU in fp64."""
-    A = dense_operator(domain, h)
+    A = dense_operator(domain, h, stencil)
     return np.linalg.solve(A, b.ravel()).reshape(domain.shape)

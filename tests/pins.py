@@ -69,3 +69,30 @@ def cheb_error_factor(d: int, lam, a: float, b: float):
 def gamma_of_r(r):
     """PAPER.md:150 (§3.2): Gamma = r / (4 r + 3)."""
     return r / (4.0 * r + 3.0)
+
+
+# ---- 27-point operator (SURVEY f1; SPEC weights: centre 8/3, faces 0, edges -1/6,
+# corners -1/12, times 1/h^2).  With reflected ghosts it is diagonalised by the same DST-II
+# basis: the 1D neighbour average (u_{i-1} + u_{i+1})/2 with reflected ends has eigenvalue
+# c_k = cos(k pi / n) on v_k, and the stencil is 8/3 - 2/3 (c1 c2 + c2 c3 + c1 c3)
+# - 2/3 c1 c2 c3 in those averages.
+def lam27(cz, cy, cx, h):
+    return (8.0 / 3.0 - (2.0 / 3.0) * (cz * cy + cy * cx + cz * cx) - (2.0 / 3.0) * cz * cy * cx) / (h * h)
+
+
+def eigvec3_27(shape, ks, h):
+    cs, vs = [], []
+    for d in range(3):
+        n, k = shape[d], ks[d]
+        i = np.arange(n)
+        cs.append(np.cos(k * np.pi / n))
+        vs.append(np.sin(k * np.pi * (i + 0.5) / n))
+    return lam27(cs[0], cs[1], cs[2], h), vs[0][:, None, None] * vs[1][None, :, None] * vs[2][None, None, :]
+
+
+def dst_solve27(f: np.ndarray, h: float) -> np.ndarray:
+    """u_h* with A27 u = f via orthonormal DST-II (eigenvalues lam27)."""
+    c = [np.cos(np.arange(1, n + 1) * np.pi / n) for n in f.shape]
+    lam = lam27(c[0][:, None, None], c[1][None, :, None], c[2][None, None, :], h)
+    fh = scipy.fft.dstn(f, type=2, norm="ortho", workers=-1)
+    return scipy.fft.idstn(fh / lam, type=2, norm="ortho", workers=-1)

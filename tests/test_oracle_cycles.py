@@ -155,3 +155,25 @@ def test_vsolve_tolerance_semantics():
     # a tolerance the zero guess already meets needs no cycle
     u0, it0, _ = O.vsolve(f, Config(n=n, M=4), rtol=1.0)
     assert it0 == 0 and np.all(u0 == 0)
+
+
+# ---- 27-point operator on the paper's domain [0,2]x[0,1]^2 ----
+def test_27pt_vcycle_contraction_and_fmg_accuracy():
+    from tests.pins import dst_solve27
+    N = 16
+    n, h = (2 * N, N, N), 1.0 / N
+    f = W.manufactured_f(n, h)
+    cfg = Config(n=n, M=3, h=h, stencil="27pt")
+    ustar = dst_solve27(f, h)
+    # V(2,2) contraction from a zero guess (PAPER.md:149-151 asks Gamma < 1/4)
+    its = O.vcycle_iterate(f, cfg, 4)
+    e = [np.linalg.norm(u - ustar) for u in its]
+    assert max(b / a for a, b in zip(e, e[1:])) < 0.25, e
+    # FMG: algebraic error of the order of the discretisation error (R11 bound r <= 3)
+    u = O.solve(f, cfg)
+    e_alg = np.abs(u - ustar).max()
+    e_disc = np.abs(ustar - W.manufactured_u(n, h)).max()
+    assert e_alg < 3.0 * e_disc, (e_alg, e_disc)
+    # the fixed point: the exact discrete solution is left unchanged by a V-cycle
+    it = O.vcycle_iterate(f, cfg, 1, u0=ustar)[0]
+    assert np.abs(it - ustar).max() < 1e-12 * np.abs(ustar).max()

@@ -255,3 +255,83 @@ def test_prolongation_weights_partition_of_unity_and_linear_exactness():
     assert fine[4, 2, 2] == 9 / 64 and fine[0, 2, 2] == 0.0
     # sum of all child weights of one coarse cell = 8 (each fine cell's weights sum to 1)
     assert fine.sum() == pytest.approx(8.0)
+
+
+# ----------------------------------------------------------------------------- 27-point
+# SURVEY f1 ("27-point stencil, second order"; weights per SPEC / reading R28)
+@pytest.mark.parametrize("shape,ks", [((4, 4, 4), (1, 1, 1)), ((6, 4, 8), (5, 2, 7)),
+                                      ((8, 8, 8), (8, 1, 1)), ((3, 5, 2), (2, 5, 1))])
+def test_27pt_operator_eigenpairs(shape, ks):
+    # pins the edge/corner ghost reflection (-1)^m: A27 v_k = lam27(k) v_k on the DST basis
+    h = 0.3
+    lam, v = pins.eigvec3_27(shape, ks, h)
+    dom = Box((0, 0, 0), shape)
+    u = Field(dom.grow(1))
+    u[dom] = v
+    O.fill_bc_ghosts(u, dom)
+    assert np.abs(O.apply_A(u, dom, h, "27pt") - lam * v).max() < 1e-12 * lam
+
+
+def test_27pt_lambda_max_bound_and_high_frequency_band():
+    # R28: sup of the symbol is 4/h^2 (at c = (-1, 1, 1)); over the high frequencies of
+    # full coarsening (some theta_d >= pi/2) its minimum is 4/3 /h^2 (at theta = (pi,pi,pi))
+    h = 1.0
+    th = np.linspace(0, np.pi, 181)
+    c = np.cos(th)
+    L = pins.lam27(c[:, None, None], c[None, :, None], c[None, None, :], h)
+    assert L.max() == pytest.approx(4.0, abs=1e-12) and L.min() == pytest.approx(0.0, abs=1e-12)
+    hi = (th[:, None, None] >= np.pi / 2) | (th[None, :, None] >= np.pi / 2) | (th[None, None, :] >= np.pi / 2)
+    assert L[hi].min() == pytest.approx(4.0 / 3.0, abs=1e-12)
+    from oracle.ops import lambda_max
+    assert lambda_max(0.5, "27pt") == 16.0 and lambda_max(0.5) == 48.0
+
+
+@pytest.mark.parametrize("poly", ["x2", "xy", "yz2", "lin"])
+def test_27pt_operator_exact_on_quadratics_interior(poly):
+    h = 0.1
+    dom = Box((0, 0, 0), (6, 6, 6))
+    big = dom.grow(1)
+    z, y, x = np.meshgrid(*[(np.arange(big.lo[d], big.hi[d]) + 0.5) * h for d in range(3)],
+                          indexing="ij")
+    f = {"x2": (x * x, -2.0), "xy": (x * y, 0.0), "yz2": (y * y + 3 * z * z, -8.0),
+         "lin": (2 * x - y + 0.5 * z + 1, 0.0)}[poly]
+    u = Field(big)
+    u.a = f[0]
+    assert np.abs(O.apply_A(u, dom, h, "27pt") - f[1]).max() < 1e-9
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 2), (4, 2, 2), (2, 4, 8)])
+def test_27pt_exact_solve_matches_dst(shape):
+    rng = np.random.default_rng(7)
+    b = rng.standard_normal(shape)
+    h = 0.5
+    u = O.exact_solve(b, Box((0, 0, 0), shape), h, "27pt")
+    assert np.abs(u - pins.dst_solve27(b, h)).max() < 1e-12 * np.abs(u).max()
+
+
+def test_27pt_discretisation_second_order_on_paper_domain():
+    # Omega = [0,2] x [0,1]^2, u = prod(x^4 - R^2 x^2): exact discrete
+    # solutions by DST converge at second order (ratio ~4 per halving)
+    errs = []
+    for N in (8, 16, 32, 64):
+        n = (2 * N, N, N)
+        h = 1.0 / N
+        f = W.manufactured_f(n, h)
+        u = W.manufactured_u(n, h)
+        errs.append(np.abs(pins.dst_solve27(f, h) - u).max())
+    ratios = [a / b for a, b in zip(errs, errs[1:])]
+    assert 3.5 < ratios[-1] < 4.5, ratios
+
+
+@pytest.mark.parametrize("deg", [1, 2])
+def test_27pt_chebyshev_eigenvector_response(deg):
+    shape, h = (8, 8, 8), 1 / 8
+    dom = Box((0, 0, 0), shape)
+    lm = 4 / h ** 2
+    for ks in [(1, 1, 1), (8, 1, 1), (8, 8, 8), (3, 6, 2)]:
+        lam, v = pins.eigvec3_27(shape, ks, h)
+        u = Field(dom.grow(1))
+        u[dom] = v
+        O.cheb(deg, u, Field(dom, fill=0.0), dom, h, dom, 1 / 3, 1.0, "27pt")
+        factor = pins.cheb_error_factor(deg, lam, lm / 3, lm)
+        assert np.abs(u[dom] - factor * v).max() < 1e-13

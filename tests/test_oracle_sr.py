@@ -228,3 +228,34 @@ def test_mbs_error_ratio_trend():
     assert mbs[0] < mbs[1] < mbs[2], mbs
     for S in (16, 8):
         assert er(S, ("mbs", 2)) <= er(S, None, 2) + 1e-12
+
+
+# ---- 27-point operator: the SR equivalences and the paper's e_r trends on the
+# paper's own domain [0,2]x[0,1]^2, R = (2,1,1) (Tables 1-2 trends)
+def test_27pt_sr_huge_buffer_and_one_segment_equal_fmg():
+    n, h = (64, 32, 32), 1 / 32
+    f = W.manufactured_f(n, h)
+    ref = O.solve(f, Config(n=n, M=4, h=h, stencil="27pt"))
+    big = O.solve(f, Config(n=n, M=4, h=h, seg=16, buffer=64, K=2, stencil="27pt"))
+    assert np.array_equal(big, ref)
+    n1 = (32, 32, 32)
+    f1 = W.manufactured_f(n1, 1 / 32)
+    one = O.solve(f1, Config(n=n1, M=4, seg=32, buffer=2, K=2, stencil="27pt"))
+    assert np.array_equal(one, O.solve(f1, Config(n=n1, M=4, stencil="27pt")))
+
+
+def test_27pt_error_ratio_trends_on_paper_domain():
+    N = 32
+    n, h = (2 * N, N, N), 1.0 / N
+    f = W.manufactured_f(n, h)
+    u = W.manufactured_u(n, h)
+    e_conv = np.abs(O.solve(f, Config(n=n, M=5, h=h, stencil="27pt")) - u).max()
+
+    def er(S, J, K, sched=None):
+        cfg = Config(n=n, M=5, h=h, seg=S, buffer=J, K=K, sched=sched, stencil="27pt")
+        return np.abs(O.solve(f, cfg) - u).max() / e_conv
+
+    by_J = [er(16, J, 2) for J in (1, 2, 4)]            # e_r falls with J
+    assert by_J[0] > by_J[1] > by_J[2], by_J
+    by_p = [er(S, 2, 2) for S in (32, 16, 8)]            # pN0V = 8, 4, 2
+    assert by_p[0] < by_p[1] < by_p[2], by_p
