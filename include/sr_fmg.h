@@ -74,8 +74,8 @@ typedef struct {
   int32_t alpha;      /* F(alpha, nu1, nu2) Chebyshev degrees;       */
   int32_t nu1;        /*   default (1, 2, 2)                                             */
   int32_t nu2;
-  double cheb_lo;     /* Chebyshev interval [lo, hi] * lambda_max, lambda_max = 12/h_l^2 */
-  double cheb_hi;     /*   default [1/6, 1] (reading R8)                                 */
+  double cheb_lo;     /* Chebyshev interval [lo, hi] * lambda_max (12/h_l^2, 7-point;    */
+  double cheb_hi;     /*   4/h_l^2, 27-point); lo = 0: default 1/6 (7-pt) / 1/3 (27-pt)  */
   int32_t world;      /* number of ranks (GPUs); 1 = single GPU                          */
   int32_t rank;
   int32_t pgrid[3];   /* rank grid; world == pgrid[0]*pgrid[1]*pgrid[2]                  */
@@ -84,6 +84,10 @@ typedef struct {
   void *stream;       /* cudaStream_t; NULL = legacy default stream                      */
   int32_t use_graph;  /* 1 (default): capture a solve into a CUDA graph and replay it    */
   int32_t comm;       /* world > 1: 0 = NCCL (default), 1 = test replay store (see below) */
+  int32_t stencil;    /* 7 (default): 7-point FD, A = -Lap_h (BASELINE); 27: the paper's    */
+                      /*   27-point operator (weights centre 8/3, edges     */
+                      /*   -1/6, corners -1/12, faces 0, /h^2), lambda_max = 4/h^2; runs  */
+                      /*   on the unfused kernels                                        */
 } sr_fmg_desc_t;
 
 typedef struct {

@@ -38,7 +38,7 @@ class Desc(ctypes.Structure):
         ("nu2", ctypes.c_int32), ("cheb_lo", ctypes.c_double), ("cheb_hi", ctypes.c_double),
         ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("pgrid", ctypes.c_int32 * 3),
         ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
-        ("use_graph", ctypes.c_int32), ("comm", ctypes.c_int32),
+        ("use_graph", ctypes.c_int32), ("comm", ctypes.c_int32), ("stencil", ctypes.c_int32),
     ]
 
 

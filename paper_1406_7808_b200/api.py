@@ -30,8 +30,8 @@ class LevelInfo:
 
 
 def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha=1, nu1=2,
-              nu2=2, cheb=(1.0 / 6.0, 1.0), device=None, use_graph=True, world=1, rank=0,
-              pgrid=(1, 1, 1)) -> Desc:
+              nu2=2, cheb=None, device=None, use_graph=True, world=1, rank=0,
+              pgrid=(1, 1, 1), stencil="7pt") -> Desc:
     if isinstance(n, int):
         n = (n, n, n)
     d = Desc()
@@ -48,7 +48,9 @@ def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha
     d.dtype = {"f64": _lib.SR_F64, "f32": _lib.SR_F32}[dtype]
     d.h = 0.0 if h is None else float(h)
     d.alpha, d.nu1, d.nu2 = int(alpha), int(nu1), int(nu2)
-    d.cheb_lo, d.cheb_hi = float(cheb[0]), float(cheb[1])
+    if cheb is not None:  # default: the stencil's interval (R8 / R28)
+        d.cheb_lo, d.cheb_hi = float(cheb[0]), float(cheb[1])
+    d.stencil = {"7pt": 7, "27pt": 27}[stencil]
     d.device = -1 if device is None else int(device)
     d.use_graph = 1 if use_graph else 0
     d.world, d.rank = int(world), int(rank)
@@ -93,12 +95,13 @@ class Solver:
     """
 
     def __init__(self, n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None,
-                 alpha=1, nu1=2, nu2=2, cheb=(1.0 / 6.0, 1.0), device=None, use_graph=True,
-                 world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, replay_store=None):
+                 alpha=1, nu1=2, nu2=2, cheb=None, device=None, use_graph=True,
+                 world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, replay_store=None,
+                 stencil="7pt"):
         if isinstance(n, int):
             n = (n, n, n)
         d = make_desc(n, M, seg, buffer, K, dtype, h, sched, alpha, nu1, nu2, cheb, device,
-                      use_graph, world, rank, pgrid)
+                      use_graph, world, rank, pgrid, stencil)
         if world > 1 and replay_store is None:
             if nccl_id is None:
                 raise ValueError("world > 1 needs nccl_id (see nccl_unique_id) or replay_store")

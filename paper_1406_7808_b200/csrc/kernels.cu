@@ -43,12 +43,52 @@ __device__ __forceinline__ T view_at(const View<T>& v, int s, const int a[3], co
   return v.p[(long long)s * v.ss + (long long)a[2] * v.sz + (long long)a[1] * v.sy + a[0]];
 }
 
+// The paper's 27-point operator (reading R28; SPEC weights): (A u)_i =
+// (8/3 u_i - 1/6 sum_{12 edge nbrs} - 1/12 sum_{8 corner nbrs}) / h^2, face weight 0.  A
+// neighbour outside Omega is the reflected ghost (-1)^m u(mirror), mirrored per dimension
+// (R3); the mirror cells are in-domain cells of the same storage box.
+template <class T>
+__device__ __forceinline__ T apply_A27(const Lvl& L, const T* __restrict__ u, long long off,
+                                       const int g[3]) {
+  const long long st[3] = {1, (long long)L.py, L.pz};
+  T e = T(0), k = T(0);
+#pragma unroll
+  for (int oz = -1; oz <= 1; ++oz)
+#pragma unroll
+    for (int oy = -1; oy <= 1; ++oy)
+#pragma unroll
+      for (int ox = -1; ox <= 1; ++ox) {
+        const int nz = (ox != 0) + (oy != 0) + (oz != 0);
+        if (nz < 2) continue;
+        const int o[3] = {ox, oy, oz};
+        long long d = 0;
+        T sg = T(1);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          int gn = g[q] + o[q];
+          if (gn < 0) {
+            gn = -1 - gn;
+            sg = -sg;
+          } else if (gn >= L.N[q]) {
+            gn = 2 * L.N[q] - 1 - gn;
+            sg = -sg;
+          }
+          d += (long long)(gn - g[q]) * st[q];
+        }
+        const T v = sg * u[off + d];
+        if (nz == 2) e += v;
+        else k += v;
+      }
+  return (T(8.0 / 3.0) * u[off] - e * T(1.0 / 6.0) - k * T(1.0 / 12.0)) * T(L.inv_h2);
+}
+
 // (A u) at local cell a / global cell g of segment storage `u` (offset `off`):
 // A = -Lap_h, 7 points (R1/R2); a neighbour outside Omega is the reflected ghost -u_i
 // (R3).  Neighbour sum order z-, z+, y-, y+, x-, x+ (as the oracle).
 template <class T>
 __device__ __forceinline__ T apply_A(const Lvl& L, const T* __restrict__ u, long long off,
                                      const int g[3]) {
+  if (L.st27) return apply_A27(L, u, off, g);
   const T c = u[off];
   T s = T(0);
   s += (g[2] > 0) ? u[off - L.pz] : -c;
@@ -500,6 +540,125 @@ __global__ void __launch_bounds__(kThreads) k_pyramid(const T* __restrict__ ff, 
   }
 }
 
+// ---- 27-point variants: one thread per storage cell, same regions and
+// arithmetic as k_cheb_step / k_tau / k_restrict with A = apply_A27 ------------------------
+__device__ __forceinline__ bool cell_of_box(const Lvl& L, long long i, int& s, int a[3],
+                                            int g[3], int p[3]) {
+  const long long per = (long long)L.E[0] * L.E[1] * L.E[2];
+  s = (int)(i / per);
+  long long r = i % per;
+  a[0] = (int)(r % L.E[0]);
+  r /= L.E[0];
+  a[1] = (int)(r % L.E[1]);
+  a[2] = (int)(r / L.E[1]);
+  int o[3];
+  seg_coords(L, s, p);
+  seg_origin(L, p, o);
+  bool in = true;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    g[d] = o[d] + a[d];
+    in = in && g[d] >= 0 && g[d] < L.N[d];
+  }
+  return in;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_cheb_step27(Lvl L, const T* __restrict__ cur,
+                                                          const T* prev, View<T> b, T* out,
+                                                          T c_mom, T c_res, int copy_gsr) {
+  const long long n = (long long)L.nsegs * L.E[0] * L.E[1] * L.E[2];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int s, a[3], g[3], p[3];
+    if (!cell_of_box(L, i, s, a, g, p)) continue;
+    const long long off = loc_off(L, s, a[0], a[1], a[2]);
+    bool c = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) c = c && a[d] >= 1 && a[d] <= L.E[d] - 2;
+    const T v0 = cur[off];
+    if (c) {
+      const T r = view_at(b, s, a, g) - apply_A27(L, cur, off, g);
+      T v = v0 + c_res * r;
+      if (prev != nullptr) v = v0 + c_mom * (v0 - prev[off]) + c_res * r;
+      out[off] = v;
+    } else if (copy_gsr) {
+      out[off] = v0;
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_tau27(Lvl L, const T* __restrict__ u,
+                                                    T* __restrict__ rhs, T* __restrict__ t,
+                                                    int jr) {
+  const long long n = (long long)L.nsegs * L.E[0] * L.E[1] * L.E[2];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int s, a[3], g[3], p[3];
+    if (!cell_of_box(L, i, s, a, g, p)) continue;
+    const long long off = loc_off(L, s, a[0], a[1], a[2]);
+    t[off] = u[off];
+    bool c = true, inF = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      c = c && a[d] >= 1 && a[d] <= L.E[d] - 2;
+      inF = inF && g[d] >= p[d] * L.S[d] - jr && g[d] < (p[d] + 1) * L.S[d] + jr;
+    }
+    if (c) {
+      const T Au = apply_A27(L, u, off, g);
+      rhs[off] = inF ? rhs[off] + Au : Au;
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_restrict27(Lvl Lf, const T* __restrict__ uf,
+                                                         View<T> bf, Lvl Lc, T* __restrict__ uc,
+                                                         T* __restrict__ rc, int jr) {
+  int B[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
+  const long long per = (long long)B[0] * B[1] * B[2];
+  const long long n = per * Lf.nsegs;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(i / per);
+    long long r = i % per;
+    int pf[3], of[3], pc[3], oc[3], X[3];
+    seg_coords(Lf, s, pf);
+    seg_origin(Lf, pf, of);
+    bool ok = true;
+    X[0] = pf[0] * (Lf.S[0] / 2) - jr + (int)(r % B[0]);
+    r /= B[0];
+    X[1] = pf[1] * (Lf.S[1] / 2) - jr + (int)(r % B[1]);
+    X[2] = pf[2] * (Lf.S[2] / 2) - jr + (int)(r / B[1]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) ok = ok && X[d] >= 0 && X[d] < Lc.N[d];
+    if (!ok) continue;
+    const int cs = (Lc.nsegs == 1) ? 0 : s;
+    seg_coords(Lc, cs, pc);
+    seg_origin(Lc, pc, oc);
+    T su = T(0), sr = T(0);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int g[3] = {2 * X[0] + (c & 1), 2 * X[1] + ((c >> 1) & 1), 2 * X[2] + (c >> 2)};
+      const int a[3] = {g[0] - of[0], g[1] - of[1], g[2] - of[2]};
+      const long long off = loc_off(Lf, s, a[0], a[1], a[2]);
+      su += uf[off];
+      sr += view_at(bf, s, a, g) - apply_A27(Lf, uf, off, g);
+    }
+    const long long co = loc_off(Lc, cs, X[0] - oc[0], X[1] - oc[1], X[2] - oc[2]);
+    uc[co] = su * T(0.125);
+    rc[co] = sr * T(0.125);
+  }
+}
+
+template <class T>
+unsigned grid_for(long long n) {
+  return (unsigned)std::max<long long>(1, std::min<long long>(148LL * 16, (n + kThreads - 1) / kThreads));
+}
+
 // sum over Omega of (b - A u)^2 on a conventional (single-segment) level, accumulated in
 // fp64 into acc[0] (V-cycle solver stopping test, reading R26)
 template <class T>
@@ -594,6 +753,12 @@ ColCfg col_cfg(int ex, int ey, int ez, int nsegs) {
 template <class T>
 void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* out, double c_mom,
                       double c_res, int copy_gsr, cudaStream_t st) {
+  if (L.st27) {
+    const long long n = (long long)L.nsegs * L.E[0] * L.E[1] * L.E[2];
+    k_cheb_step27<T><<<grid_for<T>(n), kThreads, 0, st>>>(L, cur, prev, b, out, (T)c_mom,
+                                                         (T)c_res, copy_gsr);
+    return;
+  }
   const ColCfg c = col_cfg(L.E[0], L.E[1], L.E[2], L.nsegs);
   k_cheb_step<T><<<c.grid, c.block, 0, st>>>(L, cur, prev, b, out, (T)c_mom, (T)c_res, copy_gsr,
                                              c.ntx, c.zchunk);
@@ -604,12 +769,22 @@ void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* u
                      cudaStream_t st) {
   int B[3];
   for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
+  if (Lf.st27) {
+    const long long n = (long long)B[0] * B[1] * B[2] * Lf.nsegs;
+    k_restrict27<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr);
+    return;
+  }
   const ColCfg c = col_cfg(B[0], B[1], B[2], Lf.nsegs);
   k_restrict<T><<<c.grid, c.block, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr, c.ntx, c.zchunk);
 }
 
 template <class T>
 void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st) {
+  if (Lc.st27) {
+    const long long n = (long long)Lc.nsegs * Lc.E[0] * Lc.E[1] * Lc.E[2];
+    k_tau27<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lc, u, rhs, t, jr);
+    return;
+  }
   const ColCfg c = col_cfg(Lc.E[0], Lc.E[1], Lc.E[2], Lc.nsegs);
   k_tau<T><<<c.grid, c.block, 0, st>>>(Lc, u, rhs, t, jr, c.ntx, c.zchunk);
 }

@@ -23,6 +23,7 @@ struct Lvl {
   long long ss;      // segment stride in elements
   int nsegs;
   double inv_h2;     // 1 / h_l^2
+  int st27;          // 1: the paper's 27-point operator; 0: 7-point (R1)
 };
 
 // Read-only right-hand-side view: either a dense global array over Omega_l without ghosts

@@ -180,7 +180,9 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
   if (d->dtype != SR_F64 && d->dtype != SR_F32) return bad("dtype must be SR_F64 or SR_F32");
   if (d->h < 0 || !std::isfinite(d->h)) return bad("h must be >= 0 and finite");
   if (d->alpha < 0 || d->nu1 < 0 || d->nu2 < 0) return bad("Chebyshev degrees must be >= 0");
-  if (!(d->cheb_lo > 0) || !(d->cheb_hi > d->cheb_lo)) return bad("need 0 < cheb_lo < cheb_hi");
+  if (!(d->cheb_lo >= 0) || !(d->cheb_hi > d->cheb_lo) || !(d->cheb_hi > 0))
+    return bad("need 0 <= cheb_lo < cheb_hi (cheb_lo = 0: the stencil's default)");
+  if (d->stencil != 7 && d->stencil != 27) return bad("stencil must be 7 or 27");
   if (d->world < 1) return bad("world must be >= 1");
   if (d->world != d->pgrid[0] * d->pgrid[1] * d->pgrid[2]) return bad("world != prod(pgrid)");
   if (d->rank < 0 || d->rank >= d->world) return bad("rank out of range");
@@ -281,8 +283,11 @@ void make_plan(sr_fmg* h) {
     L.ss = round_up(L.pz * L.E[2], 32);
     const double hl = h->h * (double)(1LL << (h->M - l));
     L.inv_h2 = 1.0 / (hl * hl);
-    const double lam = 12.0 / (hl * hl);  // R8: lambda_max(A_l) = 12/h_l^2
-    const double a = d->cheb_lo * lam, b = d->cheb_hi * lam;
+    L.st27 = d->stencil == 27 ? 1 : 0;
+    // R8: lambda_max(A_l) = 12/h_l^2 (7-point); R28: 4/h_l^2 (27-point, symbol supremum)
+    const double lam = (L.st27 ? 4.0 : 12.0) / (hl * hl);
+    const double lo = d->cheb_lo > 0 ? d->cheb_lo : (L.st27 ? 1.0 / 3.0 : 1.0 / 6.0);
+    const double a = lo * lam, b = d->cheb_hi * lam;
     h->theta[l] = 0.5 * (b + a);
     h->delta[l] = 0.5 * (b - a);
     h->sigma[l] = h->theta[l] / h->delta[l];
@@ -312,7 +317,32 @@ std::vector<double> coarsest_inverse(const Lvl& L0) {
   const int n = nx * ny * nz;
   std::vector<double> A((size_t)n * n, 0.0), I((size_t)n * n, 0.0);
   auto id = [&](int x, int y, int z) { return (z * ny + y) * nx + x; };
-  for (int z = 0; z < nz; ++z)
+  if (L0.st27) {  // 27-point (R28): reflected edge/corner ghosts (-1)^m u(mirror), per dim
+    const int N[3] = {nx, ny, nz};
+    for (int z = 0; z < nz; ++z)
+      for (int y = 0; y < ny; ++y)
+        for (int x = 0; x < nx; ++x) {
+          const int i = id(x, y, z);
+          A[(size_t)i * n + i] += (8.0 / 3.0) * L0.inv_h2;
+          for (int oz = -1; oz <= 1; ++oz)
+            for (int oy = -1; oy <= 1; ++oy)
+              for (int ox = -1; ox <= 1; ++ox) {
+                const int nzc = (ox != 0) + (oy != 0) + (oz != 0);
+                if (nzc < 2) continue;
+                const int c[3] = {x + ox, y + oy, z + oz};
+                int q[3];
+                double sg = 1.0;
+                for (int dd = 0; dd < 3; ++dd) {
+                  q[dd] = c[dd];
+                  if (q[dd] < 0) { q[dd] = -1 - q[dd]; sg = -sg; }
+                  if (q[dd] >= N[dd]) { q[dd] = 2 * N[dd] - 1 - q[dd]; sg = -sg; }
+                }
+                const double wgt = nzc == 2 ? 1.0 / 6.0 : 1.0 / 12.0;
+                A[(size_t)i * n + id(q[0], q[1], q[2])] -= sg * wgt * L0.inv_h2;
+              }
+        }
+  }
+  for (int z = 0; z < nz && !L0.st27; ++z)
     for (int y = 0; y < ny; ++y)
       for (int x = 0; x < nx; ++x) {
         const int i = id(x, y, z);
@@ -462,7 +492,9 @@ struct Schedule {
   bool flushing = false;
   int cops_top = 0;
   double cops_bytes = 0;
-  bool cx(int l) const { return h->cexec && srfmg::coarse_level_ok(h->L[l]); }
+  bool cx(int l) const {
+    return h->cexec && !h->L[l].st27 && srfmg::coarse_level_ok(h->L[l]);
+  }
   void emit(const srfmg::COp<T>& o, double bytes) {
     if (cops.n == srfmg::kCoarseMaxOps) flush();
     if (cops.n == 0) {
@@ -531,7 +563,8 @@ struct Schedule {
     const CellCounts& c = h->cells[l];
     // the fused pass marches z inside a CTA: use it only when segments x bands fill the
     // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
-    if (deg == 2 && h->fused && (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
+    if (deg == 2 && h->fused && !L.st27 &&
+        (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
         tma_rhs_ok(b) && srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
       const double rho0 = 1.0 / h->sigma[l];
@@ -555,7 +588,8 @@ struct Schedule {
       if (fin) final_done = true;
       return;
     }
-    if (deg == 1 && h->fused && (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
+    if (deg == 1 && h->fused && !L.st27 &&
+        (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
         tma_rhs_ok(b) && srfmg::cheb_spec_ok<T>(L)) {
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb1_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b),
@@ -707,7 +741,7 @@ struct Schedule {
 
   // ---- fused multi-stage passes (pass.cu) on SR levels
   bool pass_on(int l, int src, int nstep, int sink, const View<T>& b) {
-    if (!h->pass || l <= h->T || l < 1) return false;
+    if (!h->pass || l <= h->T || l < 1 || h->L[l].st27) return false;
     if (h->d.alpha != 1 || h->d.nu1 != 2 || h->d.nu2 != 2) return false;
     const Lvl& L = h->L[l];
     if (!h->force && (long long)L.nsegs * ((L.E[1] + 13) / 14) < 148) return false;
@@ -778,7 +812,7 @@ struct Schedule {
 
   void restrict_std(int l, View<T> b) {
     const int jr = jr_for(l);
-    if (h->fused && h->pass_restrict && l > h->T && tma_rhs_ok(b) &&
+    if (h->fused && h->pass_restrict && l > h->T && !h->L[l].st27 && tma_rhs_ok(b) &&
         (h->force || (long long)h->L[l].nsegs * ((h->L[l].E[1] + 13) / 14) >= 148) &&
         srfmg::pass_ok<T>(srfmg::kSrcLoad, 0, srfmg::kSinkRestrict, h->L[l], h->L[l - 1],
                           b.global)) {
@@ -1066,8 +1100,9 @@ void sr_fmg_desc_init(sr_fmg_desc_t* d) {
   d->alpha = 1;
   d->nu1 = 2;
   d->nu2 = 2;
-  d->cheb_lo = 1.0 / 6.0;
+  d->cheb_lo = 0.0;  // the stencil's default: 1/6 (7-point, R8) or 1/3 (27-point, R28)
   d->cheb_hi = 1.0;
+  d->stencil = 7;
   d->world = 1;
   d->pgrid[0] = d->pgrid[1] = d->pgrid[2] = 1;
   d->device = -1;

@@ -531,3 +531,37 @@ def test_vsolve_fp32_and_unsupported_sr_handle():
     with Solver(n, M, seg=16, buffer=2, K=2) as s:
         with pytest.raises(SrError):
             s.vsolve(torch.from_numpy(f).cuda())
+
+
+# ---- the paper's 27-point operator on its domain [0,2]x[0,1]^2 ----------
+ST27_CASES = [
+    # (name, n, M, seg, J, K, sched)
+    ("conv", (64, 32, 32), 4, 0, 0, 0, None),
+    ("K2-J2", (64, 32, 32), 4, 16, 2, 2, None),
+    ("K3-eq5", (64, 32, 32), 4, 16, 2, 3, (2, 1)),
+    ("K2-mbs", (64, 32, 32), 4, 16, 2, 2, ("mbs", 1)),
+    ("K2-S8", (128, 64, 64), 5, 8, 2, 2, None),
+]
+
+
+@pytest.mark.parametrize("case", ST27_CASES, ids=[c[0] for c in ST27_CASES])
+def test_27pt_solve_matches_oracle(case):
+    name, n, M, seg, J, K, sched = case
+    h = 2.0 / n[0]
+    f = W.make_rhs("manufactured", n, h=h) + 1e-3 * W.random_field(n)
+    ref = O.solve(f, O.Config(n=n, M=M, seg=seg, buffer=J, K=K, h=h, sched=sched, stencil="27pt"))
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, h=h, sched=sched, stencil="27pt")
+    assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
+
+
+def test_27pt_fp32_and_vsolve():
+    n, M = (64, 32, 32), 4
+    h = 2.0 / n[0]
+    f = W.make_rhs("manufactured", n, h=h)
+    ref = O.solve(f, O.Config(n=n, M=M, seg=16, buffer=2, K=2, h=h, stencil="27pt"))
+    u = _gpu_solve(f, n=n, M=M, seg=16, buffer=2, K=2, h=h, stencil="27pt", dtype="f32")
+    assert rel_l2(u, ref) <= TOL32
+    vref, cyc, hist = O.vsolve(f, O.Config(n=n, M=M, h=h, stencil="27pt"), rtol=1e-6)
+    with Solver(n, M, K=0, h=h, stencil="27pt") as s:
+        v, gcyc, grel = s.vsolve(torch.from_numpy(f).cuda(), rtol=1e-6)
+    assert gcyc == cyc and rel_l2(v.cpu().numpy(), vref) <= TOL64
