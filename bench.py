@@ -35,6 +35,9 @@ WORKLOADS = {
     "C2": ((128, 128, 128), 6, 32, 2, 3, "manufactured"),
     "C3": ((512, 512, 512), 8, 64, 2, 4, "manufactured+noise"),
     "C5": ((1024, 1024, 1024), 9, 128, 2, 4, "bumps"),
+    # the paper's own model problem: Omega = [0,2]x[0,1]^2, 27-point operator
+    # (use with --stencil 27pt), 64^3 segments, J = 2, K = 4, pN0V = 4
+    "P27": ((1024, 512, 512), 8, 64, 2, 4, "manufactured"),
 }
 # bounded CPU sample of C3 for the oracle: the same 8^3 segment grid, K = 4, J = 2, at
 # 128^3 (1/64 of the cells); about 7 s of numpy per solve on one core
@@ -54,6 +57,8 @@ def parse():
     ap.add_argument("--config", default=None, choices=sorted(WORKLOADS) + ["C4"],
                     help="default: C3 on 1 GPU, C4 (weak scaling, 512^3 per GPU) on N > 1")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--stencil", default="7pt", choices=["7pt", "27pt"],
+                    help="27pt: the paper's operator (SURVEY f1; unfused kernels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -187,16 +192,16 @@ def main():
     else:
         P = (1, 1, 1)
         n, M, seg, buf, K, rhs = WORKLOADS[config]
-        h = 1.0 / n[0]
+        h = 1.0 / n[0] if config != "P27" else 2.0 / n[0]
     nccl_id = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     solver = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=args.dtype, h=h, world=world,
-                    rank=rank, pgrid=P, nccl_id=nccl_id)
+                    rank=rank, pgrid=P, nccl_id=nccl_id, stencil=args.stencil)
     if world == 1 and config != "C4":
-        f_host = W.make_rhs(rhs, n).astype(npd)
+        f_host = W.make_rhs(rhs, n, h=h).astype(npd)
     else:
         # this rank's haloed block, evaluated directly (no global array on any rank)
         lo = [solver.block_lo[d] - solver.f_halo for d in range(3)]
@@ -296,7 +301,7 @@ def main():
         "data": f"synthetic ({rhs}" + (f", seed {W.SEED})" if "noise" in rhs else ")"),
         "config": {"workload": f"{config}: global {n[0]}x{n[1]}x{n[2]} cells "
                                f"({int(cells)} per GPU), M={M}, seg={seg}, buffer={buf}, "
-                               f"K={K} SR levels, F(1,2,2), rhs {rhs}",
+                               f"K={K} SR levels, F(1,2,2), rhs {rhs}, {args.stencil} operator",
                    "global_cells": cells * world, "pgrid": list(P),
                    "parallelism": (f"segment blocks pgrid {P}: SR levels without communication, "
                                    f"{solver.exchanges_per_solve} NCCL all-gathers per solve "

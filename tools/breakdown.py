@@ -19,10 +19,12 @@ from paper_1406_7808_b200 import Solver, kernel_names  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--dtype", default="f64")
+ap.add_argument("--stencil", default="7pt")
 a = ap.parse_args()
 n, M, seg, buf, K, rhs = WORKLOADS[a.config]
-s = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=a.dtype)
-f = torch.from_numpy(W.make_rhs(rhs, n).astype(np.float64 if a.dtype == "f64" else np.float32)).cuda()
+h = 1.0 / n[0] if a.config != "P27" else 2.0 / n[0]
+s = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=a.dtype, h=h, stencil=a.stencil)
+f = torch.from_numpy(W.make_rhs(rhs, n, h=h).astype(np.float64 if a.dtype == "f64" else np.float32)).cuda()
 u = torch.empty_like(f)
 for _ in range(3):
     s.solve(f, u)
