@@ -588,6 +588,97 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step27(Lvl L, const T* __rest
   }
 }
 
+// Column-marching 27-point Chebyshev step: thread per (x, y) storage column and z chunk;
+// the 3x3 neighbourhoods of planes z-1, z, z+1 stay in registers (9 loads per cell instead
+// of 20), reflected ghosts via per-column mirrored offsets and signs (R3, R28).
+template <class T, int RESID = 0>
+__global__ void __launch_bounds__(kThreads) k_cheb_step27c(Lvl L, const T* __restrict__ cur,
+                                                           const T* prev, View<T> b, T* out,
+                                                           T c_mom, T c_res, int copy_gsr,
+                                                           int ntx, int zchunk) {
+  Col c;
+  if (!col_index(L.E[0], L.E[1], L.E[2], ntx, zchunk, c)) return;
+  const int s = blockIdx.y;
+  int p[3], o[3];
+  seg_coords(L, s, p);
+  seg_origin(L, p, o);
+  const int gx = o[0] + c.ax, gy = o[1] + c.ay;
+  if (gx < 0 || gx >= L.N[0] || gy < 0 || gy >= L.N[1]) return;
+  const bool cxy = c.ax >= 1 && c.ax <= L.E[0] - 2 && c.ay >= 1 && c.ay <= L.E[1] - 2;
+  const long long col = (long long)s * L.ss + (long long)c.ay * L.py + c.ax;
+  // in-plane 3x3 neighbourhood: mirrored offsets and signs (index j = (dy+1)*3 + (dx+1))
+  long long xyo[9];
+  T xys[9];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    const int dx = j % 3 - 1, dy = j / 3 - 1;
+    int qx = gx + dx, qy = gy + dy;
+    T sg = T(1);
+    if (qx < 0) { qx = -1 - qx; sg = -sg; }
+    if (qx >= L.N[0]) { qx = 2 * L.N[0] - 1 - qx; sg = -sg; }
+    if (qy < 0) { qy = -1 - qy; sg = -sg; }
+    if (qy >= L.N[1]) { qy = 2 * L.N[1] - 1 - qy; sg = -sg; }
+    xyo[j] = (long long)(qy - gy) * L.py + (qx - gx);
+    // neighbours outside the storage box only belong to non-C columns (never used): no load
+    const int mx = c.ax + (qx - gx), my = c.ay + (qy - gy);
+    xys[j] = (mx >= 0 && mx < L.E[0] && my >= 0 && my < L.E[1]) ? sg : T(0);
+    if (xys[j] == T(0)) xyo[j] = 0;
+  }
+  const T* bc = b.global ? b.p + (long long)gy * b.sy + gx
+                         : b.p + (long long)s * b.ss + (long long)c.ay * b.sy + c.ax;
+  const int N2 = L.N[2];
+  // plane window w[k][j]: k = 0, 1, 2 for planes z-1, z, z+1 (signed, mirrored)
+  T w[3][9];
+  auto load_plane = [&](int z, T (&q)[9]) {  // storage plane z (global o[2] + z)
+    int gz = o[2] + z;
+    T sz = T(1);
+    if (gz < 0) { gz = -1 - gz; sz = -sz; }
+    if (gz >= N2) { gz = 2 * N2 - 1 - gz; sz = -sz; }
+    const int mz = gz - o[2];
+    if (mz < 0 || mz >= L.E[2]) {  // outside the storage box: only non-C planes use it
+#pragma unroll
+      for (int j = 0; j < 9; ++j) q[j] = T(0);
+      return;
+    }
+    const long long zo = (long long)mz * L.pz;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) q[j] = (sz * xys[j]) * cur[col + zo + xyo[j]];
+  };
+  const int z0 = c.z0, z1 = c.z1;
+  load_plane(z0 - 1, w[0]);
+  load_plane(z0, w[1]);
+  for (int z = z0; z < z1; ++z) {
+    load_plane(z + 1, w[2]);
+    const int gz = o[2] + z;
+    const long long off = col + (long long)z * L.pz;
+    if (gz >= 0 && gz < N2) {
+      const T v0 = w[1][4];
+      if (cxy && z >= 1 && z <= L.E[2] - 2) {
+        // edges: in-plane diagonals of plane z, and the 4-neighbourhood of planes z +- 1
+        const T e = (w[1][0] + w[1][2] + w[1][6] + w[1][8]) +
+                    ((w[0][1] + w[0][3] + w[0][5] + w[0][7]) + (w[2][1] + w[2][3] + w[2][5] + w[2][7]));
+        const T k = (w[0][0] + w[0][2] + w[0][6] + w[0][8]) + (w[2][0] + w[2][2] + w[2][6] + w[2][8]);
+        const T Au = (T(8.0 / 3.0) * v0 - e * T(1.0 / 6.0) - k * T(1.0 / 12.0)) * T(L.inv_h2);
+        const T r = bc[b.global ? (long long)gz * b.sz : (long long)z * b.sz] - Au;
+        if constexpr (RESID) {
+          out[off] = r;  // residual only (restriction, first pass)
+        } else {
+          T v = v0 + c_res * r;
+          if (prev != nullptr) v = v0 + c_mom * (v0 - prev[off]) + c_res * r;
+          out[off] = v;
+        }
+      } else if (copy_gsr) {
+        out[off] = v0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      w[0][j] = w[1][j];
+      w[1][j] = w[2][j];
+    }
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_tau27(Lvl L, const T* __restrict__ u,
                                                     T* __restrict__ rhs, T* __restrict__ t,
@@ -647,6 +738,50 @@ __global__ void __launch_bounds__(kThreads) k_restrict27(Lvl Lf, const T* __rest
       const long long off = loc_off(Lf, s, a[0], a[1], a[2]);
       su += uf[off];
       sr += view_at(bf, s, a, g) - apply_A27(Lf, uf, off, g);
+    }
+    const long long co = loc_off(Lc, cs, X[0] - oc[0], X[1] - oc[1], X[2] - oc[2]);
+    uc[co] = su * T(0.125);
+    rc[co] = sr * T(0.125);
+  }
+}
+
+// restriction from a precomputed fine residual r (27-point path): per coarse target cell
+// uc = avg8(u_f), rc = avg8(r)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_avg8_ur(Lvl Lf, const T* __restrict__ uf,
+                                                      const T* __restrict__ rf, Lvl Lc,
+                                                      T* __restrict__ uc, T* __restrict__ rc,
+                                                      int jr) {
+  int B[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
+  const long long per = (long long)B[0] * B[1] * B[2];
+  const long long n = per * Lf.nsegs;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(i / per);
+    long long r = i % per;
+    int pf[3], of[3], pc[3], oc[3], X[3];
+    seg_coords(Lf, s, pf);
+    seg_origin(Lf, pf, of);
+    X[0] = pf[0] * (Lf.S[0] / 2) - jr + (int)(r % B[0]);
+    r /= B[0];
+    X[1] = pf[1] * (Lf.S[1] / 2) - jr + (int)(r % B[1]);
+    X[2] = pf[2] * (Lf.S[2] / 2) - jr + (int)(r / B[1]);
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) ok = ok && X[d] >= 0 && X[d] < Lc.N[d];
+    if (!ok) continue;
+    const int cs = (Lc.nsegs == 1) ? 0 : s;
+    seg_coords(Lc, cs, pc);
+    seg_origin(Lc, pc, oc);
+    const long long f0 = loc_off(Lf, s, 2 * X[0] - of[0], 2 * X[1] - of[1], 2 * X[2] - of[2]);
+    T su = T(0), sr = T(0);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const long long off = f0 + (c & 1) + ((c >> 1) & 1) * (long long)Lf.py + (c >> 2) * Lf.pz;
+      su += uf[off];
+      sr += rf[off];
     }
     const long long co = loc_off(Lc, cs, X[0] - oc[0], X[1] - oc[1], X[2] - oc[2]);
     uc[co] = su * T(0.125);
@@ -754,9 +889,9 @@ template <class T>
 void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* out, double c_mom,
                       double c_res, int copy_gsr, cudaStream_t st) {
   if (L.st27) {
-    const long long n = (long long)L.nsegs * L.E[0] * L.E[1] * L.E[2];
-    k_cheb_step27<T><<<grid_for<T>(n), kThreads, 0, st>>>(L, cur, prev, b, out, (T)c_mom,
-                                                         (T)c_res, copy_gsr);
+    const ColCfg c = col_cfg(L.E[0], L.E[1], L.E[2], L.nsegs);
+    k_cheb_step27c<T><<<c.grid, c.block, 0, st>>>(L, cur, prev, b, out, (T)c_mom, (T)c_res,
+                                                  copy_gsr, c.ntx, c.zchunk);
     return;
   }
   const ColCfg c = col_cfg(L.E[0], L.E[1], L.E[2], L.nsegs);
@@ -766,12 +901,19 @@ void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* o
 
 template <class T>
 void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc, int jr,
-                     cudaStream_t st) {
+                     cudaStream_t st, T* scratch) {
   int B[3];
   for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
   if (Lf.st27) {
     const long long n = (long long)B[0] * B[1] * B[2] * Lf.nsegs;
-    k_restrict27<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr);
+    if (scratch) {  // residual by the column-marching 27-point sweep, then the averages
+      const ColCfg c = col_cfg(Lf.E[0], Lf.E[1], Lf.E[2], Lf.nsegs);
+      k_cheb_step27c<T, 1><<<c.grid, c.block, 0, st>>>(Lf, uf, nullptr, bf, scratch, T(0), T(0),
+                                                       0, c.ntx, c.zchunk);
+      k_avg8_ur<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, scratch, Lc, uc, rc, jr);
+    } else {
+      k_restrict27<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr);
+    }
     return;
   }
   const ColCfg c = col_cfg(B[0], B[1], B[2], Lf.nsegs);
@@ -840,7 +982,7 @@ void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const
   template void launch_cheb_step<T>(const Lvl&, const T*, const T*, View<T>, T*, double, double, \
                                     int, cudaStream_t);                                        \
   template void launch_restrict<T>(const Lvl&, const T*, View<T>, const Lvl&, T*, T*, int,      \
-                                   cudaStream_t);                                              \
+                                   cudaStream_t, T*);                                          \
   template void launch_tau<T>(const Lvl&, const T*, T*, T*, int, cudaStream_t);                 \
   template void launch_prolong<T>(const Lvl&, T*, const Lvl&, const T*, const T*, int,          \
                                   cudaStream_t);                                               \

@@ -46,9 +46,11 @@ struct View {
 template <class T>
 void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* out, double c_mom,
                       double c_res, int copy_gsr, cudaStream_t st);
+// scratch (optional, 27-point levels): a fine-level buffer the residual may be written to
+// (the free Chebyshev ping-pong buffer); without it a per-cell kernel is used
 template <class T>
 void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc, int jr,
-                     cudaStream_t st);
+                     cudaStream_t st, T* scratch = nullptr);
 template <class T>
 void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st);
 template <class T>

@@ -832,8 +832,9 @@ struct Schedule {
     double tgt = h->L[l].nsegs;
     for (int i = 0; i < 3; ++i) tgt *= (Lf.S[i] / 2 + 2 * jr);
     Launch g(h, st, KC_RESTRICT, l, w * (16.0 + 2.0) * tgt);
+    // the free ping-pong buffer of level l is scratch for the 27-point residual
     srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
-                              st);  // L113-115 / L233, L235
+                              st, (T*)h->B[l].u[1 - h->B[l].cur]);  // L113-115 / L233, L235
   }
 
   // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors.
