@@ -59,23 +59,26 @@ def _shift(u: Field, X: Box, o) -> np.ndarray:
     return u[Box([a + d for a, d in zip(X.lo, o)], [b + d for b, d in zip(X.hi, o)])]
 
 
-def apply_A(u: Field, X: Box, h: float, stencil: str = "7pt") -> np.ndarray:
+def apply_A(u: Field, X: Box, h: float, stencil: str = "7pt", gamma: float = 0.0) -> np.ndarray:
     """(A u)_i on X, A = -L_h (R1, R2).
 
     7pt:  (6 u_i - sum_{+-e_d} u_{i+-e_d}) / h^2.
     27pt: (8/3 u_i - 1/6 sum_{12 edge neighbours} - 1/12 sum_{8 corner neighbours}) / h^2,
           face neighbours weight 0 (SPEC "Stencil weights"; R28).
+    gamma > 0 (reading R29): the nonlinear FAS test operator A(u) = -L_h u +
+    gamma u^3 (monotone cubic reaction term, pointwise).
     Reads u on grow(X,1) as stored (ghosts, incl. edges/corners, filled by the caller).
     """
     c = u[X]
     s = np.zeros(X.shape)
+    nl = gamma * c * c * c if gamma else 0.0
     if stencil == "7pt":
         for d in range(3):
             for o in (-1, 1):
                 off = [0, 0, 0]
                 off[d] = o
                 s = s + _shift(u, X, off)
-        return (6.0 * c - s) / (h * h)
+        return (6.0 * c - s) / (h * h) + nl
     if stencil != "27pt":
         raise ValueError(f"unknown stencil {stencil!r}")
     e = np.zeros(X.shape)
@@ -86,13 +89,14 @@ def apply_A(u: Field, X: Box, h: float, stencil: str = "7pt") -> np.ndarray:
             e = e + _shift(u, X, o)
         elif nz == 3:
             k = k + _shift(u, X, o)
-    return ((8.0 / 3.0) * c - e / 6.0 - k / 12.0) / (h * h)
+    return ((8.0 / 3.0) * c - e / 6.0 - k / 12.0) / (h * h) + nl
 
 
-def residual(u: Field, b: Field, X: Box, h: float, domain: Box, stencil: str = "7pt") -> np.ndarray:
-    """r = b - A u on X (fig:mgv PAPER.md:113)."""
+def residual(u: Field, b: Field, X: Box, h: float, domain: Box, stencil: str = "7pt",
+             gamma: float = 0.0) -> np.ndarray:
+    """r = b - A(u) on X (fig:mgv PAPER.md:113)."""
     fill_bc_ghosts(u, domain)
-    return b[X] - apply_A(u, X, h, stencil)
+    return b[X] - apply_A(u, X, h, stencil, gamma)
 
 
 def lambda_max(h: float, stencil: str = "7pt") -> float:
@@ -113,7 +117,7 @@ def cheb_constants(h: float, lo_frac: float, hi_frac: float, stencil: str = "7pt
 
 
 def cheb(deg: int, u: Field, b: Field, X: Box, h: float, domain: Box,
-         lo_frac: float, hi_frac: float, stencil: str = "7pt") -> None:
+         lo_frac: float, hi_frac: float, stencil: str = "7pt", gamma: float = 0.0) -> None:
     """u <- S^deg(L, u, b) on X: one degree-`deg` Chebyshev polynomial (R8).
 
     Three-term Chebyshev recurrence:  x1 = x0 + r0/theta;
@@ -128,14 +132,14 @@ def cheb(deg: int, u: Field, b: Field, X: Box, h: float, domain: Box,
     x_prev = u.copy()
     fill_bc_ghosts(x_prev, domain)
     x = x_prev.copy()
-    x[X] = x_prev[X] + (b[X] - apply_A(x_prev, X, h, stencil)) / theta
+    x[X] = x_prev[X] + (b[X] - apply_A(x_prev, X, h, stencil, gamma)) / theta
     rho_prev = 1.0 / sigma
     for _ in range(1, deg):
         rho = 1.0 / (2.0 * sigma - rho_prev)
         fill_bc_ghosts(x, domain)
         x_new = x.copy()
         x_new[X] = (x[X] + rho * rho_prev * (x[X] - x_prev[X])
-                    + (2.0 * rho / delta) * (b[X] - apply_A(x, X, h, stencil)))
+                    + (2.0 * rho / delta) * (b[X] - apply_A(x, X, h, stencil, gamma)))
         x_prev, x, rho_prev = x, x_new, rho
     u[X] = x[X]
 
@@ -184,7 +188,20 @@ def dense_operator(domain: Box, h: float, stencil: str = "7pt") -> np.ndarray:
     return A
 
 
-def exact_solve(b: np.ndarray, domain: Box, h: float, stencil: str = "7pt") -> np.ndarray:
-    """u = A^{-1} b on the coarsest grid (fig:mgv PAPER.md:121, R7): dense LU in fp64."""
+def exact_solve(b: np.ndarray, domain: Box, h: float, stencil: str = "7pt",
+                gamma: float = 0.0) -> np.ndarray:
+    """u = A^{-1} b on the coarsest grid (fig:mgv PAPER.md:121, R7): dense LU in fp64.
+
+    gamma > 0 (R29): A(u) = A_lin u + gamma u^3 = b solved exactly by Newton's method with
+    the dense Jacobian A_lin + 3 gamma diag(u^2), to rounding."""
     A = dense_operator(domain, h, stencil)
-    return np.linalg.solve(A, b.ravel()).reshape(domain.shape)
+    bb = b.ravel()
+    u = np.linalg.solve(A, bb)
+    if gamma:
+        for _ in range(50):
+            F = A @ u + gamma * u ** 3 - bb
+            du = np.linalg.solve(A + np.diag(3.0 * gamma * u * u), F)
+            u = u - du
+            if np.abs(du).max() <= 1e-16 * max(np.abs(u).max(), 1e-300):
+                break
+    return u.reshape(domain.shape)

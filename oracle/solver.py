@@ -40,6 +40,7 @@ class Config:
     lo_frac: Optional[float] = None  # Chebyshev interval as fractions of lambda_max (R8):
     hi_frac: float = 1.0             #   default 1/6 (7-point) or 1/3 (27-point, R28)
     stencil: str = "7pt"             # "7pt" (R1, BASELINE) or "27pt" (f1)
+    nl_gamma: float = 0.0            # f4 (R29): A(u) = -L_h u + nl_gamma u^3 (FAS, nonlinear)
     fas: bool = True                 # False: correction scheme (I-hat = 0)
 
     def validate(self):
@@ -135,7 +136,8 @@ class Oracle:
     # Cheb helpers
     # ------------------------------------------------------------------------------
     def _cheb(self, deg, u, b, X, l):
-        cheb(deg, u, b, X, self.h[l], self.dom[l], self.lo_frac, self.cfg.hi_frac, self.st)
+        cheb(deg, u, b, X, self.h[l], self.dom[l], self.lo_frac, self.cfg.hi_frac, self.st,
+             self.cfg.nl_gamma)
 
     # ------------------------------------------------------------------------------
     # fig:mgv, FASMGV(L_l, u_l, b_l) on the conventional (global) levels; u_l in place
@@ -144,10 +146,10 @@ class Oracle:
         self.counters["vconv_visits"][l] += 1
         u, dom, h = self.u[l], self.dom[l], self.h[l]
         if l == 0:
-            u[dom] = exact_solve(b[dom], dom, h, self.st)
+            u[dom] = exact_solve(b[dom], dom, h, self.st, self.cfg.nl_gamma)
             return
         self._cheb(self.cfg.nu1, u, b, dom, l)                        # L112
-        r = Field(dom, array=residual(u, b, dom, h, dom, self.st))    # L113
+        r = Field(dom, array=residual(u, b, dom, h, dom, self.st, self.cfg.nl_gamma))  # L113
         uc, domc, hc = self.u[l - 1], self.dom[l - 1], self.h[l - 1]
         R = restrict_avg8(r, domc)                                    # L115  r_{k-1}
         if self.cfg.fas:
@@ -156,7 +158,7 @@ class Oracle:
             uc[domc] = 0.0                                            # Î = 0 (L127): CS
         t = uc.copy()                                                 # L116  t_{k-1}
         fill_bc_ghosts(uc, domc)
-        bc = Field(domc, array=R + apply_A(uc, domc, hc, self.st))    # L117  r + L u (Eq. 4)
+        bc = Field(domc, array=R + apply_A(uc, domc, hc, self.st, self.cfg.nl_gamma))  # L117 (Eq. 4)
         self.vconv(l - 1, bc)                                         # L117  w_{k-1}
         e = Field(uc.box, array=uc.a - t.a)
         fill_bc_ghosts(e, domc)
@@ -188,7 +190,7 @@ class Oracle:
         for p in self.segs:                                           # L232 (+ r for L235)
             C = self.C(l, p)
             self._cheb(self.cfg.nu1, self.us[l][p], self.bs[l][p], C, l)
-            r[p] = Field(C, array=residual(self.us[l][p], self.bs[l][p], C, h, dom, self.st))
+            r[p] = Field(C, array=residual(self.us[l][p], self.bs[l][p], C, h, dom, self.st, self.cfg.nl_gamma))
         if k == 1:
             # R16: level T is conventional; each segment restricts onto V_T^p only
             uT, domT, hT = self.u[T], self.dom[T], self.h[T]
@@ -204,7 +206,7 @@ class Oracle:
                 self.exchange_T(uT, RT)
             t = uT.copy()                                             # L234
             fill_bc_ghosts(uT, domT)
-            bT = Field(domT, array=RT[domT] + apply_A(uT, domT, hT, self.st))  # L235 (+ L u)
+            bT = Field(domT, array=RT[domT] + apply_A(uT, domT, hT, self.st, self.cfg.nl_gamma))  # L235
             self.vconv(T, bT)                                         # L237-238 FASMGV
             e = Field(uT.box, array=uT.a - t.a)
             fill_bc_ghosts(e, domT)
@@ -226,8 +228,8 @@ class Oracle:
                 fill_bc_ghosts(uc, domc)
                 Cc = self.C(lc, p)
                 bc = self.bs[lc][p]
-                bc[Cc] = apply_A(uc, Cc, hc, self.st)                 # L236 on C \ F
-                bc[Fb] = R + apply_A(uc, Fb, hc, self.st)             # L235 on F
+                bc[Cc] = apply_A(uc, Cc, hc, self.st, self.cfg.nl_gamma)  # L236 on C \ F
+                bc[Fb] = R + apply_A(uc, Fb, hc, self.st, self.cfg.nl_gamma)  # L235 on F
             self.vsr(lc)                                              # L240
             for p in self.segs:                                       # L241
                 e = Field(self.us[lc][p].box, array=self.us[lc][p].a - self.ts[lc][p].a)
@@ -320,7 +322,7 @@ def vsolve(f: np.ndarray, cfg: Config, rtol: float = 1e-4, maxit: int = 50):
     fn = float(np.linalg.norm(fM[dom]))
     hist = []
     for it in range(maxit + 1):
-        rel = float(np.linalg.norm(residual(u, fM, dom, h, dom, o.st))) / fn
+        rel = float(np.linalg.norm(residual(u, fM, dom, h, dom, o.st, o.cfg.nl_gamma))) / fn
         hist.append(rel)
         if rel <= rtol or it == maxit:
             return u[dom].copy(), it, hist

@@ -6,7 +6,7 @@ import pytest
 
 import oracle as O
 import workloads as W
-from oracle import Box, Config
+from oracle import Box, Config, Field
 from tests import pins
 
 
@@ -177,3 +177,61 @@ def test_27pt_vcycle_contraction_and_fmg_accuracy():
     # the fixed point: the exact discrete solution is left unchanged by a V-cycle
     it = O.vcycle_iterate(f, cfg, 1, u0=ustar)[0]
     assert np.abs(it - ustar).max() < 1e-12 * np.abs(ustar).max()
+
+
+# ---- nonlinear FAS (reading R29): A(u) = -Lap_h u + gamma u^3 -----------------
+GAMMA = 1.0e4   # gamma u^2 ~ 2.4 against lambda_min(-Lap) ~ 3 pi^2: a visible nonlinearity
+
+
+def _nl_problem(N, gamma=GAMMA):
+    n, h = (N, N, N), 1.0 / N
+    u = W.manufactured_u(n, h)
+    return n, h, u, W.manufactured_f(n, h) + gamma * u ** 3
+
+
+def test_nl_exact_coarse_solve_is_a_root():
+    # Newton with the dense Jacobian reaches the root of A(u) = b; checked against the
+    # operator written out independently (Kronecker assembly) and scipy's root finder
+    import scipy.optimize
+    shape, h = (2, 4, 4), 0.25
+    rng = np.random.default_rng(5)
+    b = 50.0 * rng.standard_normal(shape)
+    u = O.exact_solve(b, Box((0, 0, 0), shape), h, gamma=GAMMA)
+    A = pins.dense_A(shape, h)
+    F = A @ u.ravel() + GAMMA * u.ravel() ** 3 - b.ravel()
+    assert np.abs(F).max() < 1e-11 * np.abs(b).max()
+    v = scipy.optimize.fsolve(lambda x: A @ x + GAMMA * x ** 3 - b.ravel(),
+                              np.linalg.solve(A, b.ravel()), xtol=1e-14)
+    assert np.abs(u.ravel() - v).max() < 1e-10 * np.abs(v).max()
+
+
+def test_nl_operator_truncation_error_second_order():
+    # the discrete nonlinear operator applied to the manufactured u reproduces f to O(h^2)
+    errs = []
+    for N in (16, 32, 64):
+        n, h, u, f = _nl_problem(N)
+        dom = Box((0, 0, 0), u.shape)
+        uf = Field(dom.grow(1))
+        uf[dom] = u
+        r = O.residual(uf, Field(dom, array=f), dom, h, dom, gamma=GAMMA)
+        errs.append(np.abs(r[2:-2, 2:-2, 2:-2]).max())   # interior: boundary rows are O(1)
+    assert 3.5 < errs[0] / errs[1] < 4.5 and 3.5 < errs[1] / errs[2] < 4.5, errs
+
+
+def test_nl_fas_vcycle_contracts_and_fmg_reaches_discretisation_accuracy():
+    N, M = 32, 4
+    n, h, u, f = _nl_problem(N)
+    cfg = Config(n=n, M=M, nl_gamma=GAMMA)
+    ustar, it, hist = O.vsolve(f, cfg, rtol=1e-12, maxit=60)   # the discrete solution
+    assert hist[-1] <= 1e-12
+    ratios = [b / a for a, b in zip(hist[1:], hist[2:-1])]
+    assert max(ratios) < 0.25, ratios                       # FAS V(2,2) contraction
+    # the FAS fixed point: a V-cycle leaves the discrete solution unchanged
+    again = O.vcycle_iterate(f, cfg, 1, u0=ustar)[0]
+    assert np.abs(again - ustar).max() < 1e-11 * np.abs(ustar).max()
+    ufmg = O.solve(f, cfg)
+    e_alg = np.abs(ufmg - ustar).max()
+    e_disc = np.abs(ustar - u).max()
+    assert e_alg < 3.0 * e_disc, (e_alg, e_disc)
+    # and the nonlinearity matters: the linear solve of the same f is far off
+    assert np.abs(O.solve(f, Config(n=n, M=M)) - ustar).max() > 4 * e_disc

@@ -259,3 +259,15 @@ def test_27pt_error_ratio_trends_on_paper_domain():
     assert by_J[0] > by_J[1] > by_J[2], by_J
     by_p = [er(S, 2, 2) for S in (32, 16, 8)]            # pN0V = 8, 4, 2
     assert by_p[0] < by_p[1] < by_p[2], by_p
+
+
+def test_nl_sr_huge_buffer_and_one_segment_equal_fmg():
+    # nonlinear FAS through the SR hierarchy keeps the SR equivalences
+    n, h, g = (32, 32, 32), 1 / 32, 1.0e4
+    u = W.manufactured_u(n, h)
+    f = W.manufactured_f(n, h) + g * u ** 3
+    ref = O.solve(f, Config(n=n, M=4, nl_gamma=g))
+    assert np.array_equal(O.solve(f, Config(n=n, M=4, seg=16, buffer=32, K=2, nl_gamma=g)), ref)
+    assert np.array_equal(O.solve(f, Config(n=n, M=4, seg=32, buffer=2, K=2, nl_gamma=g)), ref)
+    sr = O.solve(f, Config(n=n, M=4, seg=16, buffer=2, K=2, nl_gamma=g))
+    assert np.abs(sr - u).max() < 5 * np.abs(ref - u).max()
