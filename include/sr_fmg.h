@@ -88,6 +88,9 @@ typedef struct {
                       /*   27-point operator (weights centre 8/3, edges     */
                       /*   -1/6, corners -1/12, faces 0, /h^2), lambda_max = 4/h^2; runs  */
                       /*   on the unfused kernels                                        */
+  double nl_gamma;    /* >= 0: nonlinear FAS test operator A(u) = -L_h u + nl_gamma u^3     */
+                      /*   (SURVEY f4); 0 (default) = linear.  Unfused kernels; Picard    */
+                      /*   iterations with A_lin^-1 for the exact coarsest solve          */
 } sr_fmg_desc_t;
 
 typedef struct {

@@ -39,6 +39,7 @@ class Desc(ctypes.Structure):
         ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("pgrid", ctypes.c_int32 * 3),
         ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("use_graph", ctypes.c_int32), ("comm", ctypes.c_int32), ("stencil", ctypes.c_int32),
+        ("nl_gamma", ctypes.c_double),
     ]
 
 

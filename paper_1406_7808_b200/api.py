@@ -31,7 +31,7 @@ class LevelInfo:
 
 def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha=1, nu1=2,
               nu2=2, cheb=None, device=None, use_graph=True, world=1, rank=0,
-              pgrid=(1, 1, 1), stencil="7pt") -> Desc:
+              pgrid=(1, 1, 1), stencil="7pt", nl_gamma=0.0) -> Desc:
     if isinstance(n, int):
         n = (n, n, n)
     d = Desc()
@@ -51,6 +51,7 @@ def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha
     if cheb is not None:  # default: the stencil's interval (R8 / R28)
         d.cheb_lo, d.cheb_hi = float(cheb[0]), float(cheb[1])
     d.stencil = {"7pt": 7, "27pt": 27}[stencil]
+    d.nl_gamma = float(nl_gamma)
     d.device = -1 if device is None else int(device)
     d.use_graph = 1 if use_graph else 0
     d.world, d.rank = int(world), int(rank)
@@ -69,6 +70,7 @@ def partition(n, M, seg, buffer, K, world, rank, pgrid, sched=None) -> dict:
 
 
 def nccl_unique_id() -> bytes:
+    import torch  # noqa: F401  (load PyTorch's NCCL first: the library reuses it)
     buf = ctypes.create_string_buffer(128)
     check(lib.sr_fmg_nccl_unique_id(buf))
     return buf.raw
@@ -97,12 +99,13 @@ class Solver:
     def __init__(self, n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None,
                  alpha=1, nu1=2, nu2=2, cheb=None, device=None, use_graph=True,
                  world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, replay_store=None,
-                 stencil="7pt"):
+                 stencil="7pt", nl_gamma=0.0):
         if isinstance(n, int):
             n = (n, n, n)
         d = make_desc(n, M, seg, buffer, K, dtype, h, sched, alpha, nu1, nu2, cheb, device,
-                      use_graph, world, rank, pgrid, stencil)
+                      use_graph, world, rank, pgrid, stencil, nl_gamma)
         if world > 1 and replay_store is None:
+            import torch  # noqa: F401  (PyTorch's NCCL is the one the library will reuse)
             if nccl_id is None:
                 raise ValueError("world > 1 needs nccl_id (see nccl_unique_id) or replay_store")
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -47,7 +47,7 @@ __device__ __forceinline__ T apply_A(const Lvl& L, const T* __restrict__ u, long
   s += (y < L.N[1] - 1) ? u[o + L.py] : -c;
   s += (x > 0) ? u[o - 1] : -c;
   s += (x < L.N[0] - 1) ? u[o + 1] : -c;
-  return (T(6) * c - s) * T(L.inv_h2);
+  return (T(6) * c - s) * T(L.inv_h2) + T(L.nlg) * c * c * c;
 }
 
 __device__ __forceinline__ void cell_of(int i, const int n[3], int& x, int& y, int& z) {
@@ -114,7 +114,7 @@ __device__ void op_column(const Lvl& L, const COp<T>& o, int tid, int nth) {
       if (z >= ze) break;
       const T d = dxy + T((z == 0 ? 1 : 0) + (z == L.N[2] - 1 ? 1 : 0));
       const T c = q[k + 1];
-      const T Au = (d * c - ((q[k] + q[k + 2]) + nb[k])) * T(L.inv_h2);
+      const T Au = (d * c - ((q[k] + q[k + 2]) + nb[k])) * T(L.inv_h2) + T(L.nlg) * c * c * c;
       const long long off = c0 + (long long)k * L.pz;
       if constexpr (TAU) {
         o.d[off] = c;           // t = u
@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kThreadsC, 1)
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   __shared__ T bs[1024];
+  __shared__ T us[1024];
   // the operation list and the level table are read from shared memory: dynamically
   // indexed kernel-parameter reads go through the constant cache and miss (~1 us per op)
   __shared__ COp<T> sop[kCoarseMaxOps];
@@ -269,12 +270,28 @@ __global__ void __launch_bounds__(kThreadsC, 1)
             bs[j] = rhs_at(o.v, x, y, z);
           }
           __syncthreads();
+          // nonlinear (R29): Picard sweeps u <- A_lin^-1 (b - nlg u^3), as k_coarsest
+          const int sweeps = L.nlg != 0.0 ? 41 : 1;
+          for (int it = 0; it < sweeps; ++it) {
+            for (int r = threadIdx.x; r < n0; r += kThreadsC) {
+              T acc = T(0);
+              for (int j = 0; j < n0; ++j) acc += o.a[(long long)r * n0 + j] * bs[j];
+              us[r] = acc;
+            }
+            __syncthreads();
+            if (it + 1 < sweeps) {
+              for (int j = threadIdx.x; j < n0; j += kThreadsC) {
+                int x, y, z;
+                cell_of(j, L.N, x, y, z);
+                bs[j] = rhs_at(o.v, x, y, z) - T(L.nlg) * us[j] * us[j] * us[j];
+              }
+              __syncthreads();
+            }
+          }
           for (int r = threadIdx.x; r < n0; r += kThreadsC) {
-            T acc = T(0);
-            for (int j = 0; j < n0; ++j) acc += o.a[(long long)r * n0 + j] * bs[j];
             int x, y, z;
             cell_of(r, L.N, x, y, z);
-            o.c[soff<T>(L, x, y, z)] = acc;
+            o.c[soff<T>(L, x, y, z)] = us[r];
           }
         }
         break;

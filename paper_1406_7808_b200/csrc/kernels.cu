@@ -79,7 +79,9 @@ __device__ __forceinline__ T apply_A27(const Lvl& L, const T* __restrict__ u, lo
         if (nz == 2) e += v;
         else k += v;
       }
-  return (T(8.0 / 3.0) * u[off] - e * T(1.0 / 6.0) - k * T(1.0 / 12.0)) * T(L.inv_h2);
+  const T c = u[off];
+  return (T(8.0 / 3.0) * c - e * T(1.0 / 6.0) - k * T(1.0 / 12.0)) * T(L.inv_h2) +
+         T(L.nlg) * c * c * c;
 }
 
 // (A u) at local cell a / global cell g of segment storage `u` (offset `off`):
@@ -97,7 +99,7 @@ __device__ __forceinline__ T apply_A(const Lvl& L, const T* __restrict__ u, long
   s += (g[1] < L.N[1] - 1) ? u[off + L.py] : -c;
   s += (g[0] > 0) ? u[off - 1] : -c;
   s += (g[0] < L.N[0] - 1) ? u[off + 1] : -c;
-  return (T(6) * c - s) * T(L.inv_h2);
+  return (T(6) * c - s) * T(L.inv_h2) + T(L.nlg) * c * c * c;
 }
 
 // ------------------------------------------------------------------------------------
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restri
         sum += yp ? nb[k][1] : -v0;
         sum += xm ? nb[k][2] : -v0;
         sum += xp ? nb[k][3] : -v0;
-        const T r = bv[k] - (T(6) * v0 - sum) * T(L.inv_h2);
+        const T r = bv[k] - ((T(6) * v0 - sum) * T(L.inv_h2) + T(L.nlg) * v0 * v0 * v0);
         T v = v0 + c_res * r;
         if (prev != nullptr) v = v0 + c_mom * (v0 - pv[k]) + c_res * r;
         out[col + zo] = v;
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restri
           sum += (dx == 0) ? q[dz + 1][dy * 2 + 1] : (xp ? u[yo + 1] : -v);
           const T bv = bcol[bz + dy * bf.sy + dx];
           su += v;
-          sr += bv - (T(6) * v - sum) * T(Lf.inv_h2);
+          sr += bv - ((T(6) * v - sum) * T(Lf.inv_h2) + T(Lf.nlg) * v * v * v);
         }
     }
     const long long co = (long long)cs * Lc.ss + (long long)(Z - oc[2]) * Lc.pz +
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(kThreads) k_tau(Lvl L, const T* __restrict__ u
         sum += yp ? nb[k][1] : -v0;
         sum += xm ? nb[k][2] : -v0;
         sum += xp ? nb[k][3] : -v0;
-        const T Au = (T(6) * v0 - sum) * T(L.inv_h2);
+        const T Au = (T(6) * v0 - sum) * T(L.inv_h2) + T(L.nlg) * v0 * v0 * v0;
         const bool inF = fxy && gz >= fz0 && gz < fz1;
         rhs[col + zo] = inF ? rv[k] + Au : Au;
       }
@@ -509,11 +511,31 @@ __global__ void k_coarsest(Lvl L, T* __restrict__ u, View<T> b, const T* __restr
     bs[j] = view_at(b, 0, a, g);
   }
   __syncthreads();
+  // nonlinear (R29): Picard iteration u <- A_lin^-1 (b - nlg u^3) from u = A_lin^-1 b; the
+  // contraction 3 nlg u^2 / lambda_min(A_0) is small on the coarsest grid, 40 sweeps reach
+  // the root to rounding
+  T* us = bs + n0;
+  const int sweeps = L.nlg != 0.0 ? 41 : 1;
+  for (int it = 0; it < sweeps; ++it) {
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) {
+      T acc = T(0);
+      for (int j = 0; j < n0; ++j) acc += ainv[(long long)i * n0 + j] * bs[j];
+      us[i] = acc;
+    }
+    __syncthreads();
+    if (it + 1 < sweeps) {
+      for (int j = threadIdx.x; j < n0; j += blockDim.x) {
+        int g[3] = {j % L.N[0], (j / L.N[0]) % L.N[1], j / (L.N[0] * L.N[1])};
+        int a[3] = {g[0] + 1, g[1] + 1, g[2] + 1};
+        const T x = us[j];
+        bs[j] = view_at(b, 0, a, g) - T(L.nlg) * x * x * x;
+      }
+      __syncthreads();
+    }
+  }
   for (int i = threadIdx.x; i < n0; i += blockDim.x) {
-    T acc = T(0);
-    for (int j = 0; j < n0; ++j) acc += ainv[(long long)i * n0 + j] * bs[j];
     int g[3] = {i % L.N[0], (i / L.N[0]) % L.N[1], i / (L.N[0] * L.N[1])};
-    u[loc_off(L, 0, g[0] + 1, g[1] + 1, g[2] + 1)] = acc;
+    u[loc_off(L, 0, g[0] + 1, g[1] + 1, g[2] + 1)] = us[i];
   }
 }
 
@@ -658,7 +680,8 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step27c(Lvl L, const T* __res
         const T e = (w[1][0] + w[1][2] + w[1][6] + w[1][8]) +
                     ((w[0][1] + w[0][3] + w[0][5] + w[0][7]) + (w[2][1] + w[2][3] + w[2][5] + w[2][7]));
         const T k = (w[0][0] + w[0][2] + w[0][6] + w[0][8]) + (w[2][0] + w[2][2] + w[2][6] + w[2][8]);
-        const T Au = (T(8.0 / 3.0) * v0 - e * T(1.0 / 6.0) - k * T(1.0 / 12.0)) * T(L.inv_h2);
+        const T Au = (T(8.0 / 3.0) * v0 - e * T(1.0 / 6.0) - k * T(1.0 / 12.0)) * T(L.inv_h2) +
+                     T(L.nlg) * v0 * v0 * v0;
         const T r = bc[b.global ? (long long)gz * b.sz : (long long)z * b.sz] - Au;
         if constexpr (RESID) {
           out[off] = r;  // residual only (restriction, first pass)
@@ -942,7 +965,7 @@ template <class T>
 void launch_coarsest(const Lvl& L0, T* u, View<T> b, const T* ainv, cudaStream_t st) {
   const int n0 = L0.N[0] * L0.N[1] * L0.N[2];
   const int thr = n0 < 1024 ? ((n0 + 31) / 32) * 32 : 1024;
-  k_coarsest<T><<<1, thr, n0 * sizeof(T), st>>>(L0, u, b, ainv);
+  k_coarsest<T><<<1, thr, 2 * n0 * sizeof(T), st>>>(L0, u, b, ainv);
 }
 
 template <class T>

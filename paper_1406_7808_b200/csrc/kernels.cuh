@@ -24,6 +24,7 @@ struct Lvl {
   int nsegs;
   double inv_h2;     // 1 / h_l^2
   int st27;          // 1: the paper's 27-point operator; 0: 7-point (R1)
+  double nlg;        // f4 (R29): A(u) = -L_h u + nlg u^3 (0: linear)
 };
 
 // Read-only right-hand-side view: either a dense global array over Omega_l without ghosts

@@ -183,6 +183,7 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
   if (!(d->cheb_lo >= 0) || !(d->cheb_hi > d->cheb_lo) || !(d->cheb_hi > 0))
     return bad("need 0 <= cheb_lo < cheb_hi (cheb_lo = 0: the stencil's default)");
   if (d->stencil != 7 && d->stencil != 27) return bad("stencil must be 7 or 27");
+  if (!(d->nl_gamma >= 0) || !std::isfinite(d->nl_gamma)) return bad("nl_gamma must be >= 0");
   if (d->world < 1) return bad("world must be >= 1");
   if (d->world != d->pgrid[0] * d->pgrid[1] * d->pgrid[2]) return bad("world != prod(pgrid)");
   if (d->rank < 0 || d->rank >= d->world) return bad("rank out of range");
@@ -284,6 +285,7 @@ void make_plan(sr_fmg* h) {
     const double hl = h->h * (double)(1LL << (h->M - l));
     L.inv_h2 = 1.0 / (hl * hl);
     L.st27 = d->stencil == 27 ? 1 : 0;
+    L.nlg = d->nl_gamma;
     // R8: lambda_max(A_l) = 12/h_l^2 (7-point); R28: 4/h_l^2 (27-point, symbol supremum)
     const double lam = (L.st27 ? 4.0 : 12.0) / (hl * hl);
     const double lo = d->cheb_lo > 0 ? d->cheb_lo : (L.st27 ? 1.0 / 3.0 : 1.0 / 6.0);
@@ -563,7 +565,7 @@ struct Schedule {
     const CellCounts& c = h->cells[l];
     // the fused pass marches z inside a CTA: use it only when segments x bands fill the
     // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
-    if (deg == 2 && h->fused && !L.st27 &&
+    if (deg == 2 && h->fused && !L.st27 && L.nlg == 0.0 &&
         (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
         tma_rhs_ok(b) && srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
@@ -588,7 +590,7 @@ struct Schedule {
       if (fin) final_done = true;
       return;
     }
-    if (deg == 1 && h->fused && !L.st27 &&
+    if (deg == 1 && h->fused && !L.st27 && L.nlg == 0.0 &&
         (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
         tma_rhs_ok(b) && srfmg::cheb_spec_ok<T>(L)) {
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
@@ -741,7 +743,7 @@ struct Schedule {
 
   // ---- fused multi-stage passes (pass.cu) on SR levels
   bool pass_on(int l, int src, int nstep, int sink, const View<T>& b) {
-    if (!h->pass || l <= h->T || l < 1 || h->L[l].st27) return false;
+    if (!h->pass || l <= h->T || l < 1 || h->L[l].st27 || h->L[l].nlg != 0.0) return false;
     if (h->d.alpha != 1 || h->d.nu1 != 2 || h->d.nu2 != 2) return false;
     const Lvl& L = h->L[l];
     if (!h->force && (long long)L.nsegs * ((L.E[1] + 13) / 14) < 148) return false;
@@ -812,7 +814,8 @@ struct Schedule {
 
   void restrict_std(int l, View<T> b) {
     const int jr = jr_for(l);
-    if (h->fused && h->pass_restrict && l > h->T && !h->L[l].st27 && tma_rhs_ok(b) &&
+    if (h->fused && h->pass_restrict && l > h->T && !h->L[l].st27 && h->L[l].nlg == 0.0 &&
+        tma_rhs_ok(b) &&
         (h->force || (long long)h->L[l].nsegs * ((h->L[l].E[1] + 13) / 14) >= 148) &&
         srfmg::pass_ok<T>(srfmg::kSrcLoad, 0, srfmg::kSinkRestrict, h->L[l], h->L[l - 1],
                           b.global)) {
@@ -988,8 +991,14 @@ NcclApi& nccl() {
   static bool tried = false;
   if (!tried) {
     tried = true;
-    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // prefer the NCCL the process already uses (e.g. PyTorch's, loaded by `import torch`):
+    // loading a second, older libnccl.so.2 first would shadow it for later loads; else an
+    // explicit SR_FMG_NCCL_LIB, else the loader's libnccl.so.2
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib)
+      if (const char* e = std::getenv("SR_FMG_NCCL_LIB")) lib = dlopen(e, RTLD_NOW | RTLD_LOCAL);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
     if (!lib) {
       api.why = std::string("cannot load libnccl.so.2: ") + dlerror();
       return api;
@@ -1104,6 +1113,7 @@ void sr_fmg_desc_init(sr_fmg_desc_t* d) {
   d->cheb_lo = 0.0;  // the stencil's default: 1/6 (7-point, R8) or 1/3 (27-point, R28)
   d->cheb_hi = 1.0;
   d->stencil = 7;
+  d->nl_gamma = 0.0;
   d->world = 1;
   d->pgrid[0] = d->pgrid[1] = d->pgrid[2] = 1;
   d->device = -1;

@@ -565,3 +565,37 @@ def test_27pt_fp32_and_vsolve():
     with Solver(n, M, K=0, h=h, stencil="27pt") as s:
         v, gcyc, grel = s.vsolve(torch.from_numpy(f).cuda(), rtol=1e-6)
     assert gcyc == cyc and rel_l2(v.cpu().numpy(), vref) <= TOL64
+
+
+# ---- nonlinear FAS: A(u) = -Lap_h u + gamma u^3 --------------------------
+NL_GAMMA = 1.0e4
+NL_CASES = [
+    ("conv", (32, 32, 32), 4, 0, 0, 0),
+    ("K2", (32, 32, 32), 4, 16, 2, 2),
+    ("K3-S16", (64, 64, 64), 5, 16, 2, 3),
+]
+
+
+@pytest.mark.parametrize("case", NL_CASES, ids=[c[0] for c in NL_CASES])
+def test_nonlinear_fas_matches_oracle(case):
+    name, n, M, seg, J, K = case
+    h = 1.0 / n[0]
+    u = W.manufactured_u(n, h)
+    f = W.manufactured_f(n, h) + NL_GAMMA * u ** 3
+    ref = O.solve(f, O.Config(n=n, M=M, seg=seg, buffer=J, K=K, nl_gamma=NL_GAMMA))
+    g = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, nl_gamma=NL_GAMMA)
+    assert rel_l2(g, ref) <= TOL64, (name, rel_l2(g, ref))
+
+
+def test_nonlinear_vsolve_and_fp32():
+    n, M = (32, 32, 32), 4
+    h = 1.0 / n[0]
+    u = W.manufactured_u(n, h)
+    f = W.manufactured_f(n, h) + NL_GAMMA * u ** 3
+    vref, cyc, _ = O.vsolve(f, O.Config(n=n, M=M, nl_gamma=NL_GAMMA), rtol=1e-8)
+    with Solver(n, M, K=0, nl_gamma=NL_GAMMA) as s:
+        v, gcyc, _ = s.vsolve(torch.from_numpy(f).cuda(), rtol=1e-8)
+    assert gcyc == cyc and rel_l2(v.cpu().numpy(), vref) <= TOL64
+    ref = O.solve(f, O.Config(n=n, M=M, seg=16, buffer=2, K=2, nl_gamma=NL_GAMMA))
+    g32 = _gpu_solve(f, n=n, M=M, seg=16, buffer=2, K=2, nl_gamma=NL_GAMMA, dtype="f32")
+    assert rel_l2(g32, ref) <= TOL32
