@@ -101,6 +101,7 @@ struct sr_fmg {
   bool sync_debug = false;
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
   bool force = false; // SR_FMG_FORCE_FUSED=1: use them even on levels too small to fill the GPU
+  int fused_min_e = 0; // SR_FMG_FUSED_MIN_E: smallest storage extent given to the TMA kernels
   // fused multi-stage SR passes (pass.cu), SR_FMG_PASS=1|3|4.  pass_entry picks the
   // FMG-entry chain: 4 = Pi+S1+S2+restrict, 3 = Pi+S1+S2 then restrict, 1 = Pi+S1
   bool pass = false;
@@ -566,7 +567,7 @@ struct Schedule {
     // the fused pass marches z inside a CTA: use it only when segments x bands fill the
     // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
     if (deg == 2 && h->fused && !L.st27 && L.nlg == 0.0 &&
-        (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
+        (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 && L.E[1] >= h->fused_min_e)) &&
         tma_rhs_ok(b) && srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
       const double rho0 = 1.0 / h->sigma[l];
@@ -591,7 +592,7 @@ struct Schedule {
       return;
     }
     if (deg == 1 && h->fused && !L.st27 && L.nlg == 0.0 &&
-        (h->force || (long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148) &&
+        (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 && L.E[1] >= h->fused_min_e)) &&
         tma_rhs_ok(b) && srfmg::cheb_spec_ok<T>(L)) {
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb1_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b),
@@ -674,7 +675,8 @@ struct Schedule {
     }
     Launch g(h, st, KC_PROLONG, l,
              w * (add ? 2.0 : 1.0) * c.cg + w * (add ? 2.0 : 1.0) * h->cells[l - 1].cg / 8.0);
-    if (h->fused && (h->force || srfmg::prolong_tma_ok<T>(h->L[l], h->L[l - 1])))
+    if (h->fused && (h->force || (srfmg::prolong_tma_ok<T>(h->L[l], h->L[l - 1]) &&
+                                  h->L[l].E[1] >= h->fused_min_e)))
       srfmg::launch_prolong_tma<T>(h->L[l], U(l), h->L[l - 1], U(l - 1), (const T*)h->B[l - 1].t,
                                    add, st);
     else
@@ -1173,6 +1175,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->force = ff && ff[0] == '1';
   // fused passes: opt-in until they beat the separate kernels.  SR_FMG_PASS=1|3|4 turns on
   // all three kinds with that entry chain; SR_FMG_PASS_{ENTRY,DOWN,UP} override per kind
+  if (const char* e = std::getenv("SR_FMG_FUSED_MIN_E")) h->fused_min_e = std::atoi(e);
   const char* ce = std::getenv("SR_FMG_CEXEC");
   h->cexec = !(ce && ce[0] == '0');
   const char* fp = std::getenv("SR_FMG_PASS");
