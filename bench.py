@@ -151,11 +151,15 @@ def run_reference(args):
     tot = sum(ts)
     value = cells * len(ts) / tot
     line = {
-        "impl": "reference", "metric": "fine-grid cells solved/s (FMG+SR)", "value": value,
+        "impl": "reference", "metric": "fine-grid cells solved/s (FMG+SR, fp64)", "value": value,
         "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config or 'C3'} (bounded CPU sample)",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic ({ORACLE_SAMPLE['rhs']}, seed {W.SEED})",
+        # our arm's workload; every step is a bounded sample of it (same segment grid, K, J)
+        "config": {"workload": "C3: global 512x512x512 cells (134217728 per GPU), M=8, "
+                               "seg=64, buffer=2, K=4 SR levels, F(1,2,2), rhs "
+                               "manufactured+noise, 7pt operator",
                    "sample": sample_desc()},
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle",
                          "sample": sample_desc()},
