@@ -46,6 +46,18 @@ bool launch_cheb1_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
 template <class T>
 bool encode_dense_tmap(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows);
 
+// TMA-fed Chebyshev pass for the 27-point operator (fused27.cu): nst = 1 (degree 1) or 2
+// (both steps of degree 2) in one HBM pass; fin.p: last pass, genuine cells -> user u.
+template <class T>
+bool cheb27_fused_ok(const Lvl& L);
+template <class T>
+void launch_cheb27_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, int nst,
+                         double c0, double cm, double cr, cudaStream_t st, FinalOut<T> fin);
+
+// r = b - A u (27-point) on the C cells of every segment into r (same layout as u)
+template <class T>
+void launch_resid27_fused(const Lvl& L, const T* u, T* r, FusedRhs<T> b, cudaStream_t st);
+
 // A geometry-specialised instantiation exists for this level's row pitch.
 template <class T>
 bool cheb_spec_ok(const Lvl& L);

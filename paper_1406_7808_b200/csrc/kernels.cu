@@ -944,6 +944,14 @@ void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* u
 }
 
 template <class T>
+void launch_restrict_from_resid(const Lvl& Lf, const T* uf, const T* rf, const Lvl& Lc, T* uc,
+                                T* rc, int jr, cudaStream_t st) {
+  long long n = Lf.nsegs;
+  for (int d = 0; d < 3; ++d) n *= Lf.S[d] / 2 + 2 * jr;
+  k_avg8_ur<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, rf, Lc, uc, rc, jr);
+}
+
+template <class T>
 void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st) {
   if (Lc.st27) {
     const long long n = (long long)Lc.nsegs * Lc.E[0] * Lc.E[1] * Lc.E[2];
@@ -1007,6 +1015,8 @@ void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const
   template void launch_restrict<T>(const Lvl&, const T*, View<T>, const Lvl&, T*, T*, int,      \
                                    cudaStream_t, T*);                                          \
   template void launch_tau<T>(const Lvl&, const T*, T*, T*, int, cudaStream_t);                 \
+  template void launch_restrict_from_resid<T>(const Lvl&, const T*, const T*, const Lvl&, T*, T*,  \
+                                              int, cudaStream_t);                                \
   template void launch_prolong<T>(const Lvl&, T*, const Lvl&, const T*, const T*, int,          \
                                   cudaStream_t);                                               \
   template void launch_coarsest<T>(const Lvl&, T*, View<T>, const T*, cudaStream_t);            \

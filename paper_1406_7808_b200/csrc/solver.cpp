@@ -600,6 +600,28 @@ struct Schedule {
       bb.cur = 1 - bb.cur;
       return;
     }
+    if ((deg == 1 || deg == 2) && h->fused && L.st27 && L.nlg == 0.0 && tma_rhs_ok(b) &&
+        (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148) &&
+        srfmg::cheb27_fused_ok<T>(L)) {
+      // 27-point operator: the whole polynomial in one TMA-fed pass (fused27.cu)
+      const double rho0 = 1.0 / h->sigma[l];
+      const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
+      const bool fin = last && final_out != nullptr;
+      srfmg::FinalOut<T> fo{};
+      if (fin) {
+        fo.p = final_out;
+        for (int i = 0; i < 3; ++i) fo.bo[i] = h->blk_lo[i];
+        fo.sy = h->blk_n[0];
+        fo.sz = (long long)h->blk_n[0] * h->blk_n[1];
+      }
+      Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
+      srfmg::launch_cheb27_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b), deg,
+                                    1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st,
+                                    fo);
+      bb.cur = 1 - bb.cur;
+      if (fin) final_done = true;
+      return;
+    }
     int lat = bb.cur, oth = 1 - bb.cur;
     if (cx(l)) {  // recorded for the coarse-level executor (same steps, same ping-pong)
       double rho_prev = 1.0 / h->sigma[l];
@@ -837,6 +859,16 @@ struct Schedule {
     double tgt = h->L[l].nsegs;
     for (int i = 0; i < 3; ++i) tgt *= (Lf.S[i] / 2 + 2 * jr);
     Launch g(h, st, KC_RESTRICT, l, w * (16.0 + 2.0) * tgt);
+    const Lvl& L = h->L[l];
+    if (L.st27 && L.nlg == 0.0 && h->fused && tma_rhs_ok(b) && srfmg::cheb27_fused_ok<T>(L) &&
+        (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148)) {
+      // 27-point: TMA-fed residual pass into the free ping-pong buffer, then the averages
+      T* scratch = (T*)h->B[l].u[1 - h->B[l].cur];
+      srfmg::launch_resid27_fused<T>(L, U(l), scratch, frhs(b), st);
+      srfmg::launch_restrict_from_resid<T>(L, U(l), scratch, h->L[l - 1], U(l - 1),
+                                           (T*)h->B[l - 1].rhs, jr, st);
+      return;
+    }
     // the free ping-pong buffer of level l is scratch for the 27-point residual
     srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
                               st, (T*)h->B[l].u[1 - h->B[l].cur]);  // L113-115 / L233, L235

@@ -544,8 +544,11 @@ ST27_CASES = [
 ]
 
 
+@pytest.mark.parametrize("force", ["0", "1"])
 @pytest.mark.parametrize("case", ST27_CASES, ids=[c[0] for c in ST27_CASES])
-def test_27pt_solve_matches_oracle(case):
+def test_27pt_solve_matches_oracle(case, force, monkeypatch):
+    # force = 1: the TMA-fed 27-point Chebyshev pass (fused27.cu) on every level it fits
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", force)
     name, n, M, seg, J, K, sched = case
     h = 2.0 / n[0]
     f = W.make_rhs("manufactured", n, h=h) + 1e-3 * W.random_field(n)

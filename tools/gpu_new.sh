@@ -1,1 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -k "nonlinear or 27pt" > gpurun_out/pytest_new.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_new.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -k "27pt" > gpurun_out/pytest_new.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_new.log
+timeout 600 python bench.py --config P27 --stencil 27pt --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_p27.log 2>&1
+timeout 600 python tools/breakdown.py --config P27 --stencil 27pt > gpurun_out/bd_p27_27.log 2>&1
