@@ -626,6 +626,9 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
   if (alt == 4 && try_spec<T, 72, 14, 8>(L, a, b, nst, st)) return true;
   if (alt == 5 && try_spec<T, 72, 22, 6>(L, a, b, nst, st)) return true;
   if (alt == 6 && try_spec<T, 72, 10, 4>(L, a, b, nst, st)) return true;
+  if (alt == 7 && try_spec<T, 72, 14, 3>(L, a, b, nst, st)) return true;
+  if (alt == 8 && try_spec<T, 72, 14, 2>(L, a, b, nst, st)) return true;
+  if (alt == 9 && try_spec<T, 72, 16, 6>(L, a, b, nst, st)) return true;
   // E = 38 / 22 boxes (32^3 / 16^3 segments): SR_FMG_CHEB2_ALT40 / _ALT24 pick band shapes
   static int a40 = -1, a24 = -1;
   if (a40 < 0) {

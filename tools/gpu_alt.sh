@@ -1,2 +1,1 @@
-for a in 1 4 5 6; do SR_FMG_CHEB2_ALT=$a timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --dtype f32 > gpurun_out/bench_alt32_$a.log 2>&1; done
-for a in 4 6; do SR_FMG_CHEB2_ALT=$a timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_alt64_$a.log 2>&1; done
+for a in 1 7 8 9; do SR_FMG_CHEB2_ALT=$a timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_alt64_$a.log 2>&1; done
