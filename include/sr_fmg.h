@@ -134,6 +134,10 @@ typedef struct {
  * h 0, F(1,2,2), interval [1/6, 1], world 1, device -1, stream NULL, use_graph 1. */
 void sr_fmg_desc_init(sr_fmg_desc_t *d);
 
+/* sizeof(sr_fmg_desc_t) as compiled into the library: bindings check their struct layout
+ * against it before passing a descriptor (the struct grew with stencil and nl_gamma). */
+size_t sr_fmg_desc_size(void);
+
 /* North-star form: cube N^3, fp64, constant buffer, current device, default stream. */
 sr_status_t sr_fmg_create(int64_t N, int32_t M, int32_t seg, int32_t buffer,
                           int32_t sr_levels, sr_fmg_t **out);

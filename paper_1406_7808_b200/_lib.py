@@ -25,7 +25,7 @@ EXPORTED = [
     "sr_fmg_debug_level_io", "sr_fmg_debug_op", "sr_fmg_profile_select", "sr_fmg_profile_read",
     "sr_fmg_partition", "sr_fmg_nccl_unique_id", "sr_fmg_replay_store_create",
     "sr_fmg_replay_store_destroy", "sr_fmg_set_replay", "sr_fmg_solve_host_async",
-    "sr_fmg_synchronize", "sr_fmg_vsolve",
+    "sr_fmg_synchronize", "sr_fmg_vsolve", "sr_fmg_desc_size",
 ]
 
 
@@ -92,6 +92,7 @@ def _load():
         "sr_fmg_solve_host_async": (I32, [P, P, P]),
         "sr_fmg_synchronize": (I32, [P]),
         "sr_fmg_vsolve": (I32, [P, P, P, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]),
+        "sr_fmg_desc_size": (ctypes.c_size_t, []),
         "sr_fmg_set_stream": (I32, [P, P]),
         "sr_fmg_destroy": (None, [P]),
         "sr_fmg_get_info": (I32, [P, ctypes.POINTER(Info)]),
@@ -117,6 +118,9 @@ def _load():
 
 
 lib = _load()
+if lib.sr_fmg_desc_size() != ctypes.sizeof(Desc):
+    raise ImportError(f"{LIB_PATH}: sr_fmg_desc_t is {lib.sr_fmg_desc_size()} bytes but the "
+                      f"binding's Desc is {ctypes.sizeof(Desc)}: rebuild the library")
 
 
 class SrError(RuntimeError):

@@ -1134,6 +1134,8 @@ void free_all(sr_fmg* h) {
 // =====================================================================================
 extern "C" {
 
+size_t sr_fmg_desc_size(void) { return sizeof(sr_fmg_desc_t); }
+
 void sr_fmg_desc_init(sr_fmg_desc_t* d) {
   if (!d) return;
   std::memset(d, 0, sizeof(*d));
