@@ -91,15 +91,24 @@ def noise(n, sigma=1e-3, seed=SEED) -> np.ndarray:
     return sigma * rng.standard_normal(size=(n[2], n[1], n[0]), dtype=np.float64)
 
 
-def gaussian_bumps(n, h, count=16, seed=SEED) -> np.ndarray:
-    """f(x) = sum_m a_m exp(-|x - c_m|^2 / (2 w_m^2)) (reading R22)."""
+def gaussian_bumps_params(count=16, seed=SEED):
+    """The bumps' (centre, width, amplitude), drawn bump by bump in the order c, w, a from
+    PCG64(seed) (reading R22)."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    g = [centres(n[d], h) for d in range(3)]
-    f = np.zeros((n[2], n[1], n[0]), dtype=np.float64)
+    out = []
     for _ in range(count):
         c = rng.uniform(0.0, 1.0, size=3)
         w = rng.uniform(0.02, 0.1)
         a = rng.standard_normal()
+        out.append((c, w, a))
+    return out
+
+
+def gaussian_bumps(n, h, count=16, seed=SEED) -> np.ndarray:
+    """f(x) = sum_m a_m exp(-|x - c_m|^2 / (2 w_m^2)) (reading R22)."""
+    g = [centres(n[d], h) for d in range(3)]
+    f = np.zeros((n[2], n[1], n[0]), dtype=np.float64)
+    for c, w, a in gaussian_bumps_params(count, seed):
         e = [np.exp(-((g[d] - c[d]) ** 2) / (2.0 * w * w)) for d in range(3)]
         f += a * (e[2][:, None, None] * e[1][None, :, None] * e[0][None, None, :])
     return f
