@@ -344,11 +344,15 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
   const bool tin = tok && gxv >= 0 && gxv < L.N[0];
   const bool tcx = tx >= 1 && tx <= Ex - 2;
   const int dxo = (gxv == 0 ? 1 : 0) + (gxv == L.N[0] - 1 ? 1 : 0);
-  unsigned ld_mask = 0, ex_mask = 0, c_mask = 0, w_mask = 0, yb_mask = 0;
+  // rw_mask: the band's storage rows -- written whole (every column of the pitch, cells
+  // outside Omega and the padding with their unchanged value) so no DRAM sector is written
+  // partially (no read-for-ownership)
+  unsigned ld_mask = 0, ex_mask = 0, c_mask = 0, w_mask = 0, yb_mask = 0, rw_mask = 0;
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) {
     const int y = y0 + k;
     const int gy = oy + y;
+    if (y >= r0 && y < r1) rw_mask |= 1u << k;
     const bool in = tin && y < s1 && gy >= 0 && gy < L.N[1];
     if (tok && y < q1) ld_mask |= 1u << k;
     if (tok && y < s1) ex_mask |= 1u << k;
@@ -408,8 +412,8 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
           u1w[k * PY] = v1;
         } else {
           // degree 1: the first step is the result (C updated, GSR copied)
-          if (((w_mask >> k) & 1u) && gz >= 0 && gz < L.N[2])
-            ob[(long long)z * pz + k * PY] = v1;
+          if (((rw_mask >> k) & 1u) && gz >= 0 && gz < L.N[2])
+            ob[(long long)z * pz + k * PY] = ((w_mask >> k) & 1u) ? v1 : v0;
         }
       }
     }
@@ -442,10 +446,10 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
           const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
           const T r = fp[k * G::FP] - ((dk[k] + dz) * c1 - sum) * ih2;
           const T v2 = ((act >> k) & 1u) ? c1 + cm * (c1 - u0v) + cr * r : u0v;
-          if (!((w_mask >> k) & 1u)) continue;
           if constexpr (FIN == 0) {
-            orow[k * PY] = v2;
+            if ((rw_mask >> k) & 1u) orow[k * PY] = ((w_mask >> k) & 1u) ? v2 : u0v;
           } else {
+            if (!((w_mask >> k) & 1u)) continue;
             // last pass of the solve (R19): genuine cells straight to the user's u
             const int y = y0 + k;
             const int vlo = L.J + 1;
