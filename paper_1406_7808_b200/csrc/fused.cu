@@ -360,6 +360,19 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
     if (in && y >= r0 && y < r1) w_mask |= 1u << k;
     yb_mask |= (unsigned)((gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0)) << (2 * k);
   }
+  // FIN: the genuine (x, y) cells of the band's output rows and their column in the user's u
+  unsigned gen_mask = 0;
+  T* fbase = nullptr;
+  if constexpr (FIN != 0) {
+    const int vlo = L.J + 1;
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) {
+      const int y = y0 + k;
+      if (((w_mask >> k) & 1u) && tx >= vlo && tx < vlo + L.S[0] && y >= vlo && y < vlo + L.S[1])
+        gen_mask |= 1u << k;
+    }
+    fbase = a.fin.p + (long long)(oy + y0 - a.fin.bo[1]) * a.fin.sy + (gxv - a.fin.bo[0]);
+  }
   // diagonal of A per slot (6 + reflected x/y neighbours, R3); the z part is per plane
   T dk[MAXS];
 #pragma unroll
@@ -437,6 +450,9 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
         const T* fp = fb + (zz % G::RF) * G::FS;
         T* orow = ob + (long long)zz * pz;
         const unsigned act = zc ? c_mask : 0u;
+        // last pass: genuine cells of a genuine plane go to the user's u (R19)
+        const unsigned gw = (FIN && zz >= L.J + 1 && zz < L.J + 1 + L.S[2]) ? gen_mask : 0u;
+        T* frow = FIN ? fbase + (long long)(gz - a.fin.bo[2]) * a.fin.sz : nullptr;
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) {
           const T u0v = u0q[k][J1];
@@ -449,14 +465,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
           if constexpr (FIN == 0) {
             if ((rw_mask >> k) & 1u) orow[k * PY] = ((w_mask >> k) & 1u) ? v2 : u0v;
           } else {
-            if (!((w_mask >> k) & 1u)) continue;
-            // last pass of the solve (R19): genuine cells straight to the user's u
-            const int y = y0 + k;
-            const int vlo = L.J + 1;
-            if (tx >= vlo && tx < vlo + L.S[0] && y >= vlo && y < vlo + L.S[1] &&
-                zz >= vlo && zz < vlo + L.S[2])
-              a.fin.p[(long long)(gz - a.fin.bo[2]) * a.fin.sz +
-                      (long long)(oy + y - a.fin.bo[1]) * a.fin.sy + (gxv - a.fin.bo[0])] = v2;
+            if ((gw >> k) & 1u) frow[k * a.fin.sy] = v2;
           }
         }
       }

@@ -73,4 +73,13 @@ template <class T>
 void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
                         cudaStream_t st);
 
+// FMG entry in one pass (pset.cu): u_out = Pi(w) on the storage of every segment of level L
+// (R10), then one degree-1 Chebyshev step on C (R8, c0 = 1/theta); GSR keeps Pi(w).
+// The rhs must be a dense global array.  false: no instantiation fits (nothing launched).
+template <class T>
+bool pset1_fused_ok(const Lvl& L, const Lvl& Lc, int rhs_global);
+template <class T>
+bool launch_pset1_fused(const Lvl& L, const Lvl& Lc, const T* w, T* uout, FusedRhs<T> b,
+                        double c0, cudaStream_t st);
+
 }  // namespace srfmg

@@ -108,6 +108,7 @@ struct sr_fmg {
   int pass_entry = 0;      // 0: unfused entry
   bool pass_down = false;  // (LOAD, 2, RESTRICT)
   bool pass_up = false;    // (PADD, 2, STORE|FINAL)
+  bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
   bool pass_restrict = false;  // (LOAD, 0, RESTRICT) for the restriction (SR_FMG_PASS_RESTRICT=1;
                               // measured equal to k_restrict in fp64, slower in fp32)
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
@@ -706,6 +707,26 @@ struct Schedule {
                                st);
   }
 
+  // FMG entry Pi + S^1 (alpha = 1) in one TMA pass (pset.cu), on the levels the fused
+  // Chebyshev pass takes (enough segments x bands to fill the GPU)
+  bool pset1_on(int l, const View<T>& b) {
+    const Lvl& L = h->L[l];
+    return h->pset1 && h->fused && h->d.alpha == 1 && !cx(l) && !L.st27 && L.nlg == 0.0 &&
+           b.global && tma_rhs_ok(b) &&
+           (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
+                         L.E[1] >= h->fused_min_e)) &&
+           srfmg::pset1_fused_ok<T>(L, h->L[l - 1], 1);
+  }
+  void pset1(int l, const View<T>& b) {
+    const Lvl& L = h->L[l];
+    const CellCounts& c = h->cells[l];
+    // algorithmic words: u written (storage), rhs read (C), coarse u read (1/8 of storage)
+    Launch g(h, st, KC_PASS_ENTRY, l, w * (c.cg + c.compute + h->cells[l - 1].cg / 8.0));
+    LevelBufs& bb = h->B[l];
+    srfmg::launch_pset1_fused<T>(L, h->L[l - 1], U(l - 1), (T*)bb.u[bb.cur], frhs(b),
+                                 1.0 / h->theta[l], st);  // (pset1_on checked the fit)
+  }
+
   // ---- multi-GPU exchanges: every rank owns a block of level T; an
   // all-gather assembles the full level-T arrays on every rank
   void rank_blockT(int r, int lo[3]) const {
@@ -895,6 +916,8 @@ struct Schedule {
         restricted = true;
       } else if (h->pass_entry == 1 && pass_on(l, kSrcPset, 1, kSinkStore, b)) {
         run_pass(l, kSrcPset, 1, kSinkStore, b);  // Pi, S^1
+      } else if (pset1_on(l, b)) {
+        pset1(l, b);                 // Pi onto C ∪ GSR and S^1, one pass
       } else {
         prolong(l, 0);               // Pi onto C ∪ GSR
         cheb(l, h->d.alpha, b);      // S^alpha
@@ -1221,6 +1244,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_PASS_DOWN")) h->pass_down = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PASS_UP")) h->pass_up = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PASS_RESTRICT")) h->pass_restrict = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
   h->pass = h->fused && (h->pass_entry || h->pass_down || h->pass_up);
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);

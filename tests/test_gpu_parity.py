@@ -394,6 +394,35 @@ def test_fused_passes_match_oracle(case, mode, cl, monkeypatch):
     assert rel_l2(u, b) <= 1e-13, (name, mode, rel_l2(u, b))
 
 
+# FMG entry Pi + S^1 in one TMA pass (pset.cu) vs prolongation + degree-1 step: the buffer
+# widths J = 0..3 give every residue of the storage origin mod 4 (fine row pairs vs coarse
+# rows in y, fine plane pairs vs coarse planes in z)
+PSET_CASES = [
+    ("J2-S64", (128, 128, 128), 6, 64, 2, 2, "manufactured+noise"),
+    ("J1-S64", (128, 128, 128), 6, 64, 1, 2, "bumps"),
+    ("J3-S64", (128, 128, 128), 6, 64, 3, 3, "random"),
+    ("J0-S64", (128, 128, 128), 6, 64, 0, 2, "manufactured+noise"),
+    ("J2-S32", (128, 128, 128), 6, 32, 2, 2, "manufactured+noise"),
+    ("noncubic", (128, 64, 192), 5, 64, 2, 2, "random"),
+]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", PSET_CASES, ids=[c[0] for c in PSET_CASES])
+def test_fused_fmg_entry_matches_oracle(case, dtype, monkeypatch):
+    name, n, M, seg, J, K, rhs = case
+    f = W.make_rhs(rhs, n)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_PSET1", "1")
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    monkeypatch.setenv("SR_FMG_PSET1", "0")
+    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    assert rel_l2(u, b) <= (1e-13 if dtype == "f64" else 1e-5), (name, rel_l2(u, b))
+    if dtype == "f64":
+        ref = _oracle(rhs, f, n, M, seg, J, K)
+        assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
+
+
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_restriction_pass_matches_oracle(dtype, monkeypatch):
     # the TMA-fed residual + restriction pass (pass.cu with no Chebyshev steps) on the E = 70
