@@ -522,7 +522,11 @@ struct Schedule {
       cops.prof = nullptr;
       if (pe && pe[0] == '1') {  // debug: per-operation timestamps, printed after the launch
         static unsigned long long* buf = nullptr;
-        if (!buf) cudaMallocManaged(&buf, sizeof(unsigned long long) * (srfmg::kCoarseMaxOps + 1));
+        // mapped pinned host memory: a managed buffer page-faults on the first write of every
+        // launch and inflates the first operation by ~35 us
+        if (!buf)
+          cudaHostAlloc((void**)&buf, sizeof(unsigned long long) * (srfmg::kCoarseMaxOps + 1),
+                        cudaHostAllocMapped);
         cops.prof = buf;
         srfmg::launch_coarse_exec<T>(cops, st);
         cudaStreamSynchronize(st);
