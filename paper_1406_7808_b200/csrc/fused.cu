@@ -53,6 +53,20 @@ struct Cheb2Args {
 
 long long round_up_ll(long long v, long long m) { return (v + m - 1) / m * m; }
 
+// bit k of m ? a : b as a predicated select (selp): both operands are computed first
+__device__ __forceinline__ double sel_bit(unsigned m, int k, double a, double b) {
+  double r;
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n selp.f64 %0, %1, %2, p;\n}"
+      : "=d"(r) : "d"(a), "d"(b), "r"((m >> k) & 1u));
+  return r;
+}
+__device__ __forceinline__ float sel_bit(unsigned m, int k, float a, float b) {
+  float r;
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n selp.f32 %0, %1, %2, p;\n}"
+      : "=f"(r) : "f"(a), "f"(b), "r"((m >> k) & 1u));
+  return r;
+}
+
 template <class T, int MAXS, int NTMAX>
 __global__ void __launch_bounds__(NTMAX, 1)
     k_cheb2(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
@@ -461,7 +475,8 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
           const T yp = (k == MAXS - 1) ? u1r[MAXS * PY] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
           const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
           const T r = fp[k * G::FP] - ((dk[k] + dz) * c1 - sum) * ih2;
-          const T v2 = ((act >> k) & 1u) ? c1 + cm * (c1 - u0v) + cr * r : u0v;
+          // (a select, not a branch: the compiler would sink the stencil loads into one)
+          const T v2 = sel_bit(act, k, c1 + cm * (c1 - u0v) + cr * r, u0v);
           if constexpr (FIN == 0) {
             if ((rw_mask >> k) & 1u) orow[k * PY] = ((w_mask >> k) & 1u) ? v2 : u0v;
           } else {
