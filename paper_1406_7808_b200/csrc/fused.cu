@@ -475,8 +475,11 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
           const T yp = (k == MAXS - 1) ? u1r[MAXS * PY] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
           const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
           const T r = fp[k * G::FP] - ((dk[k] + dz) * c1 - sum) * ih2;
-          // (a select, not a branch: the compiler would sink the stencil loads into one)
-          const T v2 = sel_bit(act, k, c1 + cm * (c1 - u0v) + cr * r, u0v);
+          // wide bands: a select, not a branch (the compiler would sink the stencil loads into
+          // one); the E = 22 / 14 boxes measure faster with the branch
+          T v2;
+          if constexpr (PY >= 40) v2 = sel_bit(act, k, c1 + cm * (c1 - u0v) + cr * r, u0v);
+          else v2 = ((act >> k) & 1u) ? c1 + cm * (c1 - u0v) + cr * r : u0v;
           if constexpr (FIN == 0) {
             if ((rw_mask >> k) & 1u) orow[k * PY] = ((w_mask >> k) & 1u) ? v2 : u0v;
           } else {
