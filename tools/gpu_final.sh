@@ -9,3 +9,5 @@ timeout 600 ncu --profile-from-start off --set full --import-source on --clock-c
 timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r1.log 2>&1
 timeout 300 python bench.py --steps 10 --warmup 3 --dtype f32 --no-cpu-baseline > gpurun_out/bench_r1_f32.log 2>&1
 timeout 600 python tools/breakdown.py > gpurun_out/breakdown_r1.log 2>&1
+timeout 600 python bench.py --config P27 --stencil 27pt --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_r1_p27.log 2>&1
+timeout 600 python tools/breakdown.py --dtype f32 > gpurun_out/breakdown_r1_f32.log 2>&1
