@@ -907,7 +907,11 @@ ColCfg col_cfg(int ex, int ey, int ez, int nsegs, long long target_default = 200
     return e ? std::atoll(e) : 0LL;
   }();
   const long long target = target_env > 0 ? target_env : target_default;
-  int zsplit = (int)std::min<long long>((target + cols - 1) / cols, std::max(1, ez / 4));
+  static const int minz = [] {  // fewest planes per z-chunk (SR_FMG_COL_MINZ, tuning)
+    const char* e = std::getenv("SR_FMG_COL_MINZ");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  int zsplit = (int)std::min<long long>((target + cols - 1) / cols, std::max(1, ez / minz));
   zsplit = std::max(zsplit, 1);
   c.zchunk = (ez + zsplit - 1) / zsplit;
   zsplit = (ez + c.zchunk - 1) / c.zchunk;
