@@ -218,11 +218,13 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restri
 // One thread per coarse (X, Y) column, marching coarse Z; the 2x2 fine child columns'
 // planes 2Z-1..2Z+2 live in registers.
 // ------------------------------------------------------------------------------------
+// bc.p != null (bf is f_l and bc = f_{l-1} = avg8(f_l), the R6 pyramid): the residual
+// average is taken as avg8(b - A u) = bc - avg8(A u), so the fine b is not read at all.
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restrict__ uf,
                                                        View<T> bf, Lvl Lc, T* __restrict__ uc,
                                                        T* __restrict__ rc, int jr, int ntx,
-                                                       int zchunk) {
+                                                       int zchunk, View<T> bc) {
   const int s = blockIdx.y;
   int B[3], lo[3];
 #pragma unroll
@@ -292,15 +294,21 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restri
           sum += (dy == 0) ? q[dz + 1][2 + dx] : (yp ? u[yo + fpy] : -v);
           sum += (dx == 0) ? (xm ? u[yo - 1] : -v) : q[dz + 1][dy * 2];
           sum += (dx == 0) ? q[dz + 1][dy * 2 + 1] : (xp ? u[yo + 1] : -v);
-          const T bv = bcol[bz + dy * bf.sy + dx];
+          const T Au = (T(6) * v - sum) * T(Lf.inv_h2) + T(Lf.nlg) * v * v * v;
           su += v;
-          sr += bv - ((T(6) * v - sum) * T(Lf.inv_h2) + T(Lf.nlg) * v * v * v);
+          if (bc.p) {
+            sr -= Au;
+          } else {
+            const T bv = bcol[bz + dy * bf.sy + dx];
+            sr += bv - Au;
+          }
         }
     }
     const long long co = (long long)cs * Lc.ss + (long long)(Z - oc[2]) * Lc.pz +
                          (long long)(Y - oc[1]) * Lc.py + (X - oc[0]);
     uc[co] = su * T(0.125);
-    rc[co] = sr * T(0.125);
+    rc[co] = bc.p ? bc.p[(long long)Z * bc.sz + (long long)Y * bc.sy + X] + sr * T(0.125)
+                  : sr * T(0.125);
     // planes 2Z+1, 2Z+2 are planes 2(Z+1)-1, 2(Z+1) of the next step
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -936,7 +944,7 @@ void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* o
 
 template <class T>
 void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc, int jr,
-                     cudaStream_t st, T* scratch) {
+                     cudaStream_t st, T* scratch, View<T> bc) {
   int B[3];
   for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
   if (Lf.st27) {
@@ -953,7 +961,7 @@ void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* u
   }
   // 800k threads: 0.657 -> 0.616 ms at C3's finest level, 0.281 -> 0.247 ms at E = 38
   const ColCfg c = col_cfg(B[0], B[1], B[2], Lf.nsegs, 800000);
-  k_restrict<T><<<c.grid, c.block, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr, c.ntx, c.zchunk);
+  k_restrict<T><<<c.grid, c.block, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr, c.ntx, c.zchunk, bc);
 }
 
 template <class T>
@@ -1026,7 +1034,7 @@ void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const
   template void launch_cheb_step<T>(const Lvl&, const T*, const T*, View<T>, T*, double, double, \
                                     int, cudaStream_t);                                        \
   template void launch_restrict<T>(const Lvl&, const T*, View<T>, const Lvl&, T*, T*, int,      \
-                                   cudaStream_t, T*);                                          \
+                                   cudaStream_t, T*, View<T>);                                 \
   template void launch_tau<T>(const Lvl&, const T*, T*, T*, int, cudaStream_t);                 \
   template void launch_restrict_from_resid<T>(const Lvl&, const T*, const T*, const Lvl&, T*, T*,  \
                                               int, cudaStream_t);                                \

@@ -49,9 +49,11 @@ void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* o
                       double c_res, int copy_gsr, cudaStream_t st);
 // scratch (optional, 27-point levels): a fine-level buffer the residual may be written to
 // (the free Chebyshev ping-pong buffer); without it a per-cell kernel is used
+// bc (optional, 7-point): the coarse f_{l-1} = avg8(bf) when bf is f_l (R6 pyramid); the
+// restricted residual is then bc - avg8(A u) and the fine b is not read
 template <class T>
 void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc, int jr,
-                     cudaStream_t st, T* scratch = nullptr);
+                     cudaStream_t st, T* scratch = nullptr, View<T> bc = View<T>{});
 template <class T>
 void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st);
 // uc = avg8(uf), rc = avg8(rf) on the restriction targets (rf: precomputed fine residual)

@@ -109,6 +109,7 @@ struct sr_fmg {
   bool pass_down = false;  // (LOAD, 2, RESTRICT)
   bool pass_up = false;    // (PADD, 2, STORE|FINAL)
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
+  bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
   bool pass_restrict = false;  // (LOAD, 0, RESTRICT) for the restriction (SR_FMG_PASS_RESTRICT=1;
                               // measured equal to k_restrict in fp64, slower in fp32)
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
@@ -562,6 +563,7 @@ struct Schedule {
 
   // S^deg(L_l, u_l, b) on C_l of every segment (R8): ping-pong between the two buffers
   T* final_out = nullptr;  // user u: the last level-M smoothing writes it directly (R19)
+  bool pyr = false;        // the f pyramid f_l (R6) of this solve is built
   bool final_done = false;
 
   void cheb(int l, int deg, View<T> b, bool last = false) {
@@ -883,8 +885,11 @@ struct Schedule {
     const Lvl& Lf = h->L[l];
     double tgt = h->L[l].nsegs;
     for (int i = 0; i < 3; ++i) tgt *= (Lf.S[i] / 2 + 2 * jr);
-    Launch g(h, st, KC_RESTRICT, l, w * (16.0 + 2.0) * tgt);
     const Lvl& L = h->L[l];
+    // b = f_l (an FMG visit, or the finest level): its average f_{l-1} is the R6 pyramid, so
+    // the restricted residual is f_{l-1} - avg8(A u) and f_l need not be read (7-point)
+    const bool use_pyr = pyr && b.global && !L.st27 && h->restrict_pyr;
+    Launch g(h, st, KC_RESTRICT, l, w * (use_pyr ? 8.0 + 1.0 + 2.0 : 16.0 + 2.0) * tgt);
     if (L.st27 && L.nlg == 0.0 && h->fused && tma_rhs_ok(b) && srfmg::cheb27_fused_ok<T>(L) &&
         (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148)) {
       // 27-point: TMA-fed residual pass into the free ping-pong buffer, then the averages
@@ -896,7 +901,8 @@ struct Schedule {
     }
     // the free ping-pong buffer of level l is scratch for the 27-point residual
     srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
-                              st, (T*)h->B[l].u[1 - h->B[l].cur]);  // L113-115 / L233, L235
+                              st, (T*)h->B[l].u[1 - h->B[l].cur],
+                              use_pyr ? fview(l - 1) : View<T>{});  // L113-115 / L233, L235
   }
 
   // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors.
@@ -993,6 +999,7 @@ struct Schedule {
       srfmg::launch_pyramid<T>(l == M ? f : (const T*)h->B[l].fpyr, L.N[0], L.N[1], L.N[2],
                                (T*)h->B[l - 1].fpyr, st);
     }
+    pyr = true;
     coarsest(fview(0));  // fig:fmg L137-138
     for (int l = 1; l <= M; ++l)  // fig:fmg L139-142 (l <= T), fig:fmgsr L220-223 (l > T)
       vcycle(l, fview(l), /*entry=*/true);
@@ -1249,6 +1256,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_PASS_UP")) h->pass_up = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PASS_RESTRICT")) h->pass_restrict = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
   h->pass = h->fused && (h->pass_entry || h->pass_down || h->pass_up);
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
