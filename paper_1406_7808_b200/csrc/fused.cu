@@ -48,6 +48,12 @@ struct Cheb2Args {
   int bw;            // rhs tensor-map box width (global rhs; 16-byte aligned start)
   T c0, cm, cr;
   FinalOut<T> fin;   // fin.p non-null: write only genuine cells, to the user's u block (last pass)
+  // tau fused in front (FIN = 2, rhs_seg holds the restricted residual R on F, in a buffer
+  // of its own): the pass first forms rhs = R + A u0 on F, A u0 on C \ F and t = u0
+  // (Eq. 4) and writes both
+  T* rhs_out;
+  T* tout;
+  int jr;
   int foff[3];       // global index of the dense rhs array's first element (tensor coords)
 };
 
@@ -377,7 +383,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
   // FIN: the genuine (x, y) cells of the band's output rows and their column in the user's u
   unsigned gen_mask = 0;
   T* fbase = nullptr;
-  if constexpr (FIN != 0) {
+  if constexpr (FIN == 1) {
     const int vlo = L.J + 1;
 #pragma unroll
     for (int k = 0; k < MAXS; ++k) {
@@ -386,6 +392,23 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
         gen_mask |= 1u << k;
     }
     fbase = a.fin.p + (long long)(oy + y0 - a.fin.bo[1]) * a.fin.sy + (gxv - a.fin.bo[0]);
+  }
+  // FIN = 2: the slots in F = grow(V, jr) (x, y) and the rows of the rhs / t outputs
+  unsigned f_mask = 0;
+  int fz0 = 0, fz1 = 0;
+  T* rob = nullptr;
+  T* tob = nullptr;
+  if constexpr (FIN == 2) {
+    const bool fx = gxv >= px * L.S[0] - a.jr && gxv < (px + 1) * L.S[0] + a.jr;
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) {
+      const int gy = oy + y0 + k;
+      if (fx && gy >= pyy * L.S[1] - a.jr && gy < (pyy + 1) * L.S[1] + a.jr) f_mask |= 1u << k;
+    }
+    fz0 = pzz * L.S[2] - a.jr;
+    fz1 = (pzz + 1) * L.S[2] + a.jr;
+    rob = a.rhs_out + (long long)s * L.ss + (long long)y0 * PY + tx;
+    tob = a.tout + (long long)s * L.ss + (long long)y0 * PY + tx;
   }
   // diagonal of A per slot (6 + reflected x/y neighbours, R3); the z part is per plane
   T dk[MAXS];
@@ -425,6 +448,9 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) u0q[k][IP] = (z + 1 < Ez) ? pn[k * PY] : T(0);
       const unsigned act = zc ? c_mask : 0u;
+      // FIN = 2: this plane's rhs / t rows (in-domain planes only), and F in z
+      const bool zin = gz >= 0 && gz < L.N[2];
+      const unsigned fm = (FIN == 2 && gz >= fz0 && gz < fz1) ? f_mask : 0u;
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
         // branch-free: every slot computes, the C-cell predicate selects
@@ -432,7 +458,23 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
         const T ym = (k == 0) ? pl[-PY] : u0q[k > 0 ? k - 1 : 0][I0];
         const T yp = (k == MAXS - 1) ? pl[MAXS * PY] : u0q[k + 1 < MAXS ? k + 1 : k][I0];
         const T sum = ((u0q[k][IM] + u0q[k][IP]) + (ym + yp)) + (pl[k * PY - 1] + pl[k * PY + 1]);
-        const T r = fp[k * G::FP] - ((dk[k] + dz) * v0 - sum) * ih2;
+        T r;
+        if constexpr (FIN == 2) {
+          // tau (Eq. 4, fig:mgvsr L234-236): rhs = R + A u0 on F, A u0 on C \ F; then the
+          // first step's residual rhs - A u0 as the unfused pair computes it
+          const T Au = ((dk[k] + dz) * v0 - sum) * ih2;
+          const T Rv = fp[k * G::FP];
+          const T bv = ((fm >> k) & 1u) ? Rv + Au : Au;
+          r = bv - Au;
+          const bool cc = (act >> k) & 1u;
+          const_cast<T*>(fp)[k * G::FP] = cc ? bv : Rv;  // stage 2 reads the new rhs
+          if (zin && ((rw_mask >> k) & 1u)) {
+            rob[(long long)z * pz + k * PY] = cc ? bv : Rv;  // whole rows: others unchanged
+            tob[(long long)z * pz + k * PY] = v0;           // t = u0 (0 outside Omega)
+          }
+        } else {
+          r = fp[k * G::FP] - ((dk[k] + dz) * v0 - sum) * ih2;
+        }
         const T v1 = ((act >> k) & 1u) ? v0 + c0 * r : v0;
         if constexpr (NST == 2) {
           u1q[k][I0] = v1;
@@ -465,8 +507,8 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
         T* orow = ob + (long long)zz * pz;
         const unsigned act = zc ? c_mask : 0u;
         // last pass: genuine cells of a genuine plane go to the user's u (R19)
-        const unsigned gw = (FIN && zz >= L.J + 1 && zz < L.J + 1 + L.S[2]) ? gen_mask : 0u;
-        T* frow = FIN ? fbase + (long long)(gz - a.fin.bo[2]) * a.fin.sz : nullptr;
+        const unsigned gw = (FIN == 1 && zz >= L.J + 1 && zz < L.J + 1 + L.S[2]) ? gen_mask : 0u;
+        T* frow = FIN == 1 ? fbase + (long long)(gz - a.fin.bo[2]) * a.fin.sz : nullptr;
 #pragma unroll
         for (int k = 0; k < MAXS; ++k) {
           const T u0v = u0q[k][J1];
@@ -480,7 +522,7 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
           T v2;
           if constexpr (PY >= 40) v2 = sel_bit(act, k, c1 + cm * (c1 - u0v) + cr * r, u0v);
           else v2 = ((act >> k) & 1u) ? c1 + cm * (c1 - u0v) + cr * r : u0v;
-          if constexpr (FIN == 0) {
+          if constexpr (FIN != 1) {
             if ((rw_mask >> k) & 1u) orow[k * PY] = ((w_mask >> k) & 1u) ? v2 : u0v;
           } else {
             if ((gw >> k) & 1u) frow[k * a.fin.sy] = v2;
@@ -622,6 +664,7 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
     kern<<<grid, nt, smem, st>>>(map, a);
   };
   const bool fin = a.fin.p != nullptr;
+  if (b.global && a.tout) return false;
   if (b.global) {
     using G2 = SpecGeom<T, PY, BH, MAXS, 1, 2>;
     using G1 = SpecGeom<T, PY, BH, MAXS, 1, 1>;
@@ -632,7 +675,10 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
   } else {
     using G2 = SpecGeom<T, PY, BH, MAXS, 0, 2>;
     using G1 = SpecGeom<T, PY, BH, MAXS, 0, 1>;
-    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 1>, G2::SMEM, G2::NT);
+    if (a.tout) {  // tau fused in front (FIN = 2)
+      if (nst != 2 || fin) return false;
+      go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 2>, G2::SMEM, G2::NT);
+    } else if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 1>, G2::SMEM, G2::NT);
     else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 0, 2>, G2::SMEM, G2::NT);
     else go(k_cheb2s<T, PY, BH, MAXS, 0, 1>, G1::SMEM, G1::NT);
   }
@@ -688,6 +734,33 @@ bool encode_dense_tmap(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows
 }
 template bool encode_dense_tmap<double>(CUtensorMap*, const FusedRhs<double>&, int, int);
 template bool encode_dense_tmap<float>(CUtensorMap*, const FusedRhs<float>&, int, int);
+
+// tau + degree-2 pass (FIN = 2): rhs holds R on F on entry and the tau rhs on exit
+template <class T>
+bool launch_tau_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, const T* R, T* rhs, T* t,
+                            int jr, double c0, double cm, double cr, cudaStream_t st) {
+  Cheb2Args<T> a{};
+  a.L = L;
+  a.uin = u_in;
+  a.uout = u_out;
+  a.rhs_seg = R;
+  a.rhs_global = 0;
+  a.rhs_out = rhs;
+  a.tout = t;
+  a.jr = jr;
+  a.c0 = (T)c0;
+  a.cm = (T)cm;
+  a.cr = (T)cr;
+  FusedRhs<T> b{};
+  b.p = R;
+  b.global = 0;
+  return launch_spec<T>(L, a, b, 2, st);
+}
+template bool launch_tau_cheb2_fused<double>(const Lvl&, const double*, double*, const double*,
+                                             double*, double*, int, double, double, double,
+                                             cudaStream_t);
+template bool launch_tau_cheb2_fused<float>(const Lvl&, const float*, float*, const float*, float*,
+                                            float*, int, double, double, double, cudaStream_t);
 
 template <class T>
 bool cheb2_final_ok(const Lvl& L) {

@@ -35,6 +35,12 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
                         double cr, cudaStream_t st, FinalOut<T> fin = FinalOut<T>{});
 template <class T>
 bool cheb2_final_ok(const Lvl& L);
+// tau (Eq. 4: rhs = R + A u on F, A u on C \ F; t = u) fused in front of the degree-2 pass.
+// R (restricted residual) is read from its own buffer: the pass writes rhs while the
+// neighbouring bands still read their halo rows of R.  false: nothing launched.
+template <class T>
+bool launch_tau_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, const T* R, T* rhs, T* t,
+                            int jr, double c0, double cm, double cr, cudaStream_t st);
 
 // One degree-1 Chebyshev step (single stencil stage) with the same TMA pipeline; returns
 // false (nothing launched) when no geometry-specialised instantiation matches the level.

@@ -40,6 +40,8 @@ struct LevelBufs {
   void* t = nullptr;                // t snapshot (levels < M)
   void* fpyr = nullptr;             // dense f_l over Omega_l (levels <= T, and < M on 1 GPU)
   void* floc = nullptr;             // multi-GPU: this rank's haloed block of f_l, T <= l < M
+  void* rres = nullptr;             // SR levels T < l < M: restricted residual R when the tau
+                                    // is fused into the next pass (read there, rhs written)
 };
 
 // collectives of the multi-GPU path: all-gather of equal per-rank blocks
@@ -110,6 +112,7 @@ struct sr_fmg {
   bool pass_up = false;    // (PADD, 2, STORE|FINAL)
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
   bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
+  bool tau_fuse = true;      // tau inside the next pre-smoothing pass; SR_FMG_TAU_FUSE=0 off
   bool pass_restrict = false;  // (LOAD, 0, RESTRICT) for the restriction (SR_FMG_PASS_RESTRICT=1;
                               // measured equal to k_restrict in fp64, slower in fp32)
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
@@ -564,9 +567,15 @@ struct Schedule {
   // S^deg(L_l, u_l, b) on C_l of every segment (R8): ping-pong between the two buffers
   T* final_out = nullptr;  // user u: the last level-M smoothing writes it directly (R19)
   bool pyr = false;        // the f pyramid f_l (R6) of this solve is built
+  int pend_tau = -1;       // level whose tau is deferred into its first Chebyshev pass
+  int pend_jr = 0;
   bool final_done = false;
 
   void cheb(int l, int deg, View<T> b, bool last = false) {
+    if (pend_tau == l && deg != 2) {  // (safety net: tau_fuse_ok asked for nu1 = 2)
+      pend_tau = -1;
+      tau_from_rres(l, pend_jr);
+    }
     if (deg <= 0) return;
     const Lvl& L = h->L[l];
     LevelBufs& bb = h->B[l];
@@ -581,6 +590,22 @@ struct Schedule {
       const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
       const bool fin = last && final_out != nullptr && srfmg::cheb2_final_ok<T>(L);
       const double nv = (double)L.N[0] * L.N[1] * L.N[2];
+      if (pend_tau == l && !fin) {  // tau (Eq. 4) fused in front of the pre-smoothing pass
+        pend_tau = -1;
+        bool done;
+        {
+          Launch g(h, st, KC_CHEB_FUSED, l,
+                   w * (3.0 * c.compute + 2.0 * (c.cg - c.compute) + c.compute + c.storage));
+          done = srfmg::launch_tau_cheb2_fused<T>(
+              L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], (const T*)bb.rres, (T*)bb.rhs,
+              (T*)bb.t, pend_jr, 1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
+        }
+        if (done) {
+          bb.cur = 1 - bb.cur;
+          return;
+        }
+        tau_from_rres(l, pend_jr);  // no instantiation: the separate kernel, then the pass
+      }
       Launch g(h, st, KC_CHEB_FUSED, l,
                fin ? w * (2.0 * c.compute + nv)
                    : w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
@@ -597,6 +622,10 @@ struct Schedule {
       bb.cur = 1 - bb.cur;
       if (fin) final_done = true;
       return;
+    }
+    if (pend_tau == l) {  // (safety net: the fused pass did not apply)
+      pend_tau = -1;
+      tau_from_rres(l, pend_jr);
     }
     if (deg == 1 && h->fused && !L.st27 && L.nlg == 0.0 &&
         (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 && L.E[1] >= h->fused_min_e)) &&
@@ -900,9 +929,37 @@ struct Schedule {
       return;
     }
     // the free ping-pong buffer of level l is scratch for the 27-point residual
-    srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, jr,
-                              st, (T*)h->B[l].u[1 - h->B[l].cur],
+    // R goes to the level's rres buffer when its tau rides in the next pass (that pass
+    // writes rhs while neighbouring bands still read R)
+    T* rc = tau_fuse_ok(l - 1) ? (T*)h->B[l - 1].rres : (T*)h->B[l - 1].rhs;
+    srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), rc, jr, st,
+                              (T*)h->B[l].u[1 - h->B[l].cur],
                               use_pyr ? fview(l - 1) : View<T>{});  // L113-115 / L233, L235
+  }
+
+  void tau_from_rres(int lc, int jr) {  // the separate tau on R parked in rres
+    const Lvl& L = h->L[lc];
+    flush();
+    cudaMemcpyAsync(h->B[lc].rhs, h->B[lc].rres, (size_t)L.ss * L.nsegs * sizeof(T),
+                    cudaMemcpyDeviceToDevice, st);
+    tau_std(lc, jr);
+  }
+  void tau_std(int lc, int jr) {
+    const CellCounts& c = h->cells[lc];
+    Launch g(h, st, KC_TAU, lc, w * (2.0 * c.storage + 2.0 * c.compute));
+    srfmg::launch_tau<T>(h->L[lc], U(lc), (T*)h->B[lc].rhs, (T*)h->B[lc].t, jr, st);
+  }
+  // the tau of SR level lc can ride in the first pass of vcycle(lc): the same conditions
+  // as the fused degree-2 pre-smoothing with the segment-storage rhs
+  bool tau_fuse_ok(int lc) const {
+    const Lvl& L = h->L[lc];
+    return h->tau_fuse && h->B[lc].rres && lc > h->T && h->fused && !h->pass &&
+           !h->pass_restrict &&
+           h->d.nu1 == 2 && !L.st27 &&
+           L.nlg == 0.0 &&
+           (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
+                         L.E[1] >= h->fused_min_e)) &&
+           srfmg::cheb2_fused_ok<T>(L) && srfmg::cheb_spec_ok<T>(L);
   }
 
   // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors.
@@ -949,11 +1006,11 @@ struct Schedule {
       o.c = (T*)h->B[l - 1].rhs;
       o.d = (T*)h->B[l - 1].t;
       emit(o, w * 4.0 * h->cells[l - 1].compute);
+    } else if (tau_fuse_ok(l - 1)) {
+      pend_tau = l - 1;  // L234-236 inside the first pass of vcycle(l - 1)
+      pend_jr = jr;
     } else {
-      const CellCounts& c = h->cells[l - 1];
-      Launch g(h, st, KC_TAU, l - 1, w * (2.0 * c.storage + 2.0 * c.compute));
-      srfmg::launch_tau<T>(h->L[l - 1], U(l - 1), (T*)h->B[l - 1].rhs, (T*)h->B[l - 1].t, jr,
-                           st);  // L116-117 / L234-236
+      tau_std(l - 1, jr);  // L116-117 / L234-236
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
     const bool last = l == h->M && final_out != nullptr;
@@ -1140,6 +1197,7 @@ void free_all(sr_fmg* h) {
   for (auto& b : h->B) {
     cudaFree(b.u[0]);
     cudaFree(b.u[1]);
+    cudaFree(b.rres);
     cudaFree(b.rhs);
     cudaFree(b.t);
     cudaFree(b.fpyr);
@@ -1257,6 +1315,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_PASS_RESTRICT")) h->pass_restrict = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_TAU_FUSE")) h->tau_fuse = std::atoi(e) != 0;
   h->pass = h->fused && (h->pass_entry || h->pass_down || h->pass_up);
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
@@ -1280,6 +1339,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
     ok = ok && alloc(&h->B[l].u[0], bytes) && alloc(&h->B[l].u[1], bytes);
     if (l < h->M) {
       ok = ok && alloc(&h->B[l].rhs, bytes) && alloc(&h->B[l].t, bytes);
+      if (l > h->T && h->tau_fuse) ok = ok && alloc(&h->B[l].rres, bytes);
       if (h->world == 1 || l <= h->T)
         ok = ok && alloc(&h->B[l].fpyr, (size_t)L.N[0] * L.N[1] * L.N[2] * h->esize);
       if (h->world > 1 && l >= h->T) {
