@@ -17,7 +17,7 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libsrfmg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["kernels.cu", "fused.cu", "fused27.cu", "prolong.cu", "pset.cu", "pass.cu", "coarse.cu",
+SOURCES = ["kernels.cu", "fused.cu", "fused27.cu", "prolong.cu", "pset.cu", "up.cu", "pass.cu", "coarse.cu",
            "solver.cpp"]
 HEADERS = ["kernels.cuh", "fused.cuh", "tma.cuh", "pass.cuh", "coarse.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

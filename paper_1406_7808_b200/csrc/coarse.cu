@@ -14,6 +14,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "coarse.cuh"
 
@@ -316,7 +317,11 @@ bool coarse_level_ok(const Lvl& L) {
 }
 
 bool coarse_level_tiny(const Lvl& L) {
-  return coarse_level_ok(L) && (long long)L.N[0] * L.N[1] * L.N[2] <= 512;
+  static const long long lim = [] {  // cells up to which CTA 0 alone runs a level's ops
+    const char* e = std::getenv("SR_FMG_CEXEC_TINY");
+    return e ? std::atoll(e) : 512LL;
+  }();
+  return coarse_level_ok(L) && (long long)L.N[0] * L.N[1] * L.N[2] <= lim;
 }
 
 template <class T>

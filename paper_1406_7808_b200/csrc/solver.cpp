@@ -113,6 +113,8 @@ struct sr_fmg {
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
   bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
   bool tau_fuse = true;      // tau inside the next pre-smoothing pass; SR_FMG_TAU_FUSE=0 off
+  bool up_fuse = false;      // correction + post-smoothing in one pass (up.cu), opt-in
+                             // (SR_FMG_UP_FUSE=1): slower in fp64, DESIGN.md §9
   bool pass_restrict = false;  // (LOAD, 0, RESTRICT) for the restriction (SR_FMG_PASS_RESTRICT=1;
                               // measured equal to k_restrict in fp64, slower in fp32)
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
@@ -937,6 +939,40 @@ struct Schedule {
                               use_pyr ? fview(l - 1) : View<T>{});  // L113-115 / L233, L235
   }
 
+  // correction + degree-2 post-smoothing in one pass (up.cu), on the levels the fused
+  // Chebyshev pass takes
+  bool up_on(int l, const View<T>& b) const {
+    const Lvl& L = h->L[l];
+    return h->up_fuse && h->fused && !h->pass && !cx(l) && h->d.nu2 == 2 && !L.st27 &&
+           L.nlg == 0.0 && tma_rhs_ok(b) &&
+           (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
+                         L.E[1] >= h->fused_min_e)) &&
+           srfmg::up2_fused_ok<T>(L, h->L[l - 1]);
+  }
+  void up2(int l, const View<T>& b, bool last) {
+    const Lvl& L = h->L[l];
+    LevelBufs& bb = h->B[l];
+    const CellCounts& c = h->cells[l];
+    const double rho0 = 1.0 / h->sigma[l];
+    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
+    const bool fin = last && final_out != nullptr;
+    srfmg::FinalOut<T> fo{};
+    const double nv = (double)h->blk_n[0] * h->blk_n[1] * h->blk_n[2];
+    if (fin) {
+      fo.p = final_out;
+      for (int i = 0; i < 3; ++i) fo.bo[i] = h->blk_lo[i];
+      fo.sy = h->blk_n[0];
+      fo.sz = (long long)h->blk_n[0] * h->blk_n[1];
+    }
+    // algorithmic words: u read (C u GSR), rhs (C), w and t (1/8 each), u or user u written
+    Launch g(h, st, KC_PASS_UP, l, w * (c.cg + c.compute + c.cg / 4.0 + (fin ? nv : c.cg)));
+    srfmg::launch_up2_fused<T>(L, h->L[l - 1], (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
+                               U(l - 1), (const T*)h->B[l - 1].t, frhs(b), 1.0 / h->theta[l],
+                               rho1 * rho0, 2.0 * rho1 / h->delta[l], st, fo);
+    bb.cur = 1 - bb.cur;
+    if (fin) final_done = true;
+  }
+
   void tau_from_rres(int lc, int jr) {  // the separate tau on R parked in rres
     const Lvl& L = h->L[lc];
     flush();
@@ -1018,6 +1054,8 @@ struct Schedule {
       run_pass(l, kSrcPadd, 2, kSinkFinal, b);  // L241-242, genuine cells -> user u (R19)
     } else if (h->pass_up && !last && pass_on(l, kSrcPadd, 2, kSinkStore, b)) {
       run_pass(l, kSrcPadd, 2, kSinkStore, b);  // L241-242 in one pass
+    } else if (up_on(l, b)) {
+      up2(l, b, last);  // L241-242 in one pass (at l = M: the solve's last pass)
     } else {
       prolong(l, 1);                    // L118 / L241
       cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
@@ -1316,6 +1354,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_TAU_FUSE")) h->tau_fuse = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_UP_FUSE")) h->up_fuse = std::atoi(e) != 0;
   h->pass = h->fused && (h->pass_entry || h->pass_down || h->pass_up);
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);

@@ -425,6 +425,24 @@ def test_fused_fmg_entry_matches_oracle(case, dtype, monkeypatch):
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("case", PSET_CASES, ids=[c[0] for c in PSET_CASES])
+def test_up_pass_correction_and_smoothing(case, dtype, monkeypatch):
+    # u += P(w - t) and the degree-2 post-smoothing in one pass (up.cu) vs the correction
+    # kernel followed by the fused Chebyshev pass: equal up to rounding; oracle parity
+    name, n, M, seg, J, K, rhs = case
+    f = W.make_rhs(rhs, n)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_UP_FUSE", "1")
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    monkeypatch.setenv("SR_FMG_UP_FUSE", "0")
+    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    assert rel_l2(u, b) <= (1e-13 if dtype == "f64" else 1e-5), (name, rel_l2(u, b))
+    if dtype == "f64":
+        ref = _oracle(rhs, f, n, M, seg, J, K)
+        assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", PSET_CASES, ids=[c[0] for c in PSET_CASES])
 def test_tau_fused_into_presmoothing(case, dtype, monkeypatch):
     # tau (Eq. 4) computed inside the first degree-2 pass of the coarse SR level's V-cycle
     # vs the separate tau kernel: the same rhs, t and smoothing up to rounding; oracle parity
@@ -492,6 +510,8 @@ def test_fused_pass_launch_count(monkeypatch):
         s.solve(torch.from_numpy(W.make_rhs("manufactured", n)).cuda())
         fused = s.launches_per_solve
     monkeypatch.setenv("SR_FMG_PASS", "0")
+    for k in ("SR_FMG_UP_FUSE", "SR_FMG_TAU_FUSE", "SR_FMG_PSET1"):  # the unfused schedule
+        monkeypatch.setenv(k, "0")
     with Solver(n, 6, seg=64, buffer=2, K=2) as s:
         s.solve(torch.from_numpy(W.make_rhs("manufactured", n)).cuda())
         unfused = s.launches_per_solve

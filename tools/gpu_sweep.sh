@@ -1,9 +1,7 @@
 mkdir -p gpurun_out
 : > gpurun_out/sweep.log
-for kv in "X=0" "X=1"; do
+for kv in "SR_FMG_CEXEC_TINY=512" "SR_FMG_CEXEC_TINY=4096" "SR_FMG_CEXEC_TINY=40000"; do
   echo "== $kv" >> gpurun_out/sweep.log
   env $kv timeout 300 python tools/breakdown.py > gpurun_out/bd.log 2>&1
-  grep -E "solve|k_cheb2" gpurun_out/bd.log >> gpurun_out/sweep.log
-  env $kv timeout 300 python tools/breakdown.py --dtype f32 > gpurun_out/bd.log 2>&1
-  grep -E "solve|k_cheb2" gpurun_out/bd.log >> gpurun_out/sweep.log
+  grep -E "solve|coarse" gpurun_out/bd.log >> gpurun_out/sweep.log
 done
