@@ -25,6 +25,11 @@ CASES = [
     ("2x2x1", (64, 64, 64), 5, 16, 2, 3, (2, 2, 1), "f64"),
     ("2x2x2", (64, 64, 64), 5, 8, 2, 2, (2, 2, 2), "f64"),
     ("4x1x2-f32", (128, 64, 64), 5, 16, 1, 2, (4, 1, 2), "f32"),
+    # 32^3 and 64^3 segments: the fused FMG entry (pset.cu), the tau inside the coarse
+    # pre-smoothing and the pyramid restriction run with nonzero segment / f offsets per rank
+    ("2x1x1-S32", (128, 64, 64), 5, 32, 2, 2, (2, 1, 1), "f64"),
+    ("1x2x2-S64", (128, 128, 128), 6, 64, 2, 2, (1, 2, 2), "f64"),
+    ("2x1x1-S64-f32", (128, 64, 64), 5, 64, 2, 2, (2, 1, 1), "f32"),
 ]
 
 
