@@ -52,7 +52,8 @@ typedef enum {
   SR_ERR_UNSUPPORTED_CONFIG = 2,/* valid, but outside what this build supports          */
   SR_ERR_OUT_OF_MEMORY = 3,
   SR_ERR_CUDA = 4,
-  SR_ERR_NCCL = 5
+  SR_ERR_NCCL = 5,
+  SR_ERR_NONFINITE = 6          /* sr_fmg_vsolve: the residual norm became NaN or Inf    */
 } sr_status_t;
 
 typedef enum { SR_F64 = 0, SR_F32 = 1 } sr_dtype_t;
@@ -91,6 +92,13 @@ typedef struct {
   double nl_gamma;    /* >= 0: nonlinear FAS test operator A(u) = -L_h u + nl_gamma u^3     */
                       /*   (SURVEY f4); 0 (default) = linear.  Unfused kernels; Picard    */
                       /*   iterations with A_lin^-1 for the exact coarsest solve          */
+  /* Optional device allocator for the workspace (e.g. a framework's caching allocator):  */
+  /* alloc(bytes, ctx) returns device memory or NULL; free(p, ctx) releases it.  Both NULL */
+  /* (default): cudaMalloc / cudaFree.  Used for every device buffer the handle owns, from */
+  /* create (and the host-pipeline slots, on first use) to destroy.                         */
+  void *(*alloc)(size_t bytes, void *ctx);
+  void (*free)(void *p, void *ctx);
+  void *alloc_ctx;
 } sr_fmg_desc_t;
 
 typedef struct {

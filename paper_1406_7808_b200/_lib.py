@@ -11,11 +11,12 @@ LIB_PATH = os.path.join(_HERE, "libsrfmg.so")
 MAX_LEVELS = 24
 
 SR_OK, SR_ERR_INVALID_ARGUMENT, SR_ERR_UNSUPPORTED_CONFIG = 0, 1, 2
-SR_ERR_OUT_OF_MEMORY, SR_ERR_CUDA, SR_ERR_NCCL = 3, 4, 5
+SR_ERR_OUT_OF_MEMORY, SR_ERR_CUDA, SR_ERR_NCCL, SR_ERR_NONFINITE = 3, 4, 5, 6
 SR_F64, SR_F32 = 0, 1
 
 STATUS_NAMES = {0: "SR_OK", 1: "SR_ERR_INVALID_ARGUMENT", 2: "SR_ERR_UNSUPPORTED_CONFIG",
-                3: "SR_ERR_OUT_OF_MEMORY", 4: "SR_ERR_CUDA", 5: "SR_ERR_NCCL"}
+                3: "SR_ERR_OUT_OF_MEMORY", 4: "SR_ERR_CUDA", 5: "SR_ERR_NCCL",
+                6: "SR_ERR_NONFINITE"}
 
 # every symbol include/sr_fmg.h declares (checked by tests/test_abi.py)
 EXPORTED = [
@@ -29,6 +30,12 @@ EXPORTED = [
 ]
 
 
+# optional device allocator of the descriptor: void *alloc(size_t, void *ctx),
+# void free(void *, void *ctx)
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class Desc(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_int64 * 3), ("M", ctypes.c_int32), ("seg", ctypes.c_int32),
@@ -40,6 +47,7 @@ class Desc(ctypes.Structure):
         ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("use_graph", ctypes.c_int32), ("comm", ctypes.c_int32), ("stencil", ctypes.c_int32),
         ("nl_gamma", ctypes.c_double),
+        ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
     ]
 
 

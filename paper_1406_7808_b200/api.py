@@ -99,11 +99,30 @@ class Solver:
     def __init__(self, n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None,
                  alpha=1, nu1=2, nu2=2, cheb=None, device=None, use_graph=True,
                  world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, replay_store=None,
-                 stencil="7pt", nl_gamma=0.0):
+                 stencil="7pt", nl_gamma=0.0, allocator=None):
         if isinstance(n, int):
             n = (n, n, n)
         d = make_desc(n, M, seg, buffer, K, dtype, h, sched, alpha, nu1, nu2, cheb, device,
                       use_graph, world, rank, pgrid, stencil, nl_gamma)
+        if allocator == "torch":
+            # the workspace comes from PyTorch's caching allocator (desc.alloc / desc.free);
+            # the callbacks must outlive the handle
+            import torch
+
+            def _alloc(nbytes, ctx):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes))
+                except RuntimeError:  # out of memory: the library reports it
+                    return None
+
+            def _free(ptr, ctx):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            self._alloc_cb = _lib.ALLOC_FN(_alloc)
+            self._free_cb = _lib.FREE_FN(_free)
+            d.alloc, d.free = self._alloc_cb, self._free_cb
+        elif allocator is not None:
+            raise ValueError("allocator must be None (cudaMalloc) or 'torch'")
         if world > 1 and replay_store is None:
             import torch  # noqa: F401  (PyTorch's NCCL is the one the library will reuse)
             if nccl_id is None:

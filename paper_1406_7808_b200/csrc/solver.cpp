@@ -1222,6 +1222,20 @@ struct ReplayComm : Comm {
   }
 };
 
+// device memory of a handle: the descriptor's allocator hooks, else cudaMalloc / cudaFree
+cudaError_t dev_alloc(sr_fmg* h, void** p, size_t bytes) {
+  if (h->d.alloc) {
+    *p = h->d.alloc(bytes, h->d.alloc_ctx);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMalloc(p, bytes);
+}
+void dev_free(sr_fmg* h, void* p) {
+  if (!p) return;
+  if (h->d.free) h->d.free(p, h->d.alloc_ctx);
+  else cudaFree(p);
+}
+
 void free_all(sr_fmg* h) {
   for (auto& g : h->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -1233,22 +1247,22 @@ void free_all(sr_fmg* h) {
   if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
   if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
   for (auto& b : h->B) {
-    cudaFree(b.u[0]);
-    cudaFree(b.u[1]);
-    cudaFree(b.rres);
-    cudaFree(b.rhs);
-    cudaFree(b.t);
-    cudaFree(b.fpyr);
-    cudaFree(b.floc);
+    dev_free(h, b.u[0]);
+    dev_free(h, b.u[1]);
+    dev_free(h, b.rres);
+    dev_free(h, b.rhs);
+    dev_free(h, b.t);
+    dev_free(h, b.fpyr);
+    dev_free(h, b.floc);
   }
-  cudaFree(h->xsend);
-  cudaFree(h->xrecv);
+  dev_free(h, h->xsend);
+  dev_free(h, h->xrecv);
   delete h->comm;
   h->comm = nullptr;
-  cudaFree(h->ainv);
+  dev_free(h, h->ainv);
   for (int i = 0; i < 2; ++i) {
-    cudaFree(h->host_f[i]);
-    cudaFree(h->host_u[i]);
+    dev_free(h, h->host_f[i]);
+    dev_free(h, h->host_u[i]);
   }
   for (auto& r : h->prof) {
     cudaEventDestroy(r.a);
@@ -1367,7 +1381,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->B.assign(h->M + 1, LevelBufs{});
   auto alloc = [&](void** p, size_t bytes) -> bool {
     if (bytes == 0) bytes = 16;
-    if (cudaMalloc(p, bytes) != cudaSuccess) return false;
+    if (dev_alloc(h, p, bytes) != cudaSuccess) return false;
     h->workspace += (long long)bytes;
     return cudaMemset(*p, 0, bytes) == cudaSuccess;
   };
@@ -1522,12 +1536,18 @@ sr_status_t sr_fmg_vsolve(sr_fmg_t* h, const void* f, void* u, double rtol, int3
     sr_status_t r = norm2(fn);  // u = 0: the residual is f
     if (r != SR_OK) return r;
     int it = 0;
-    double rel = fn > 0 ? 1.0 : 0.0;
+    double rel = !std::isfinite(fn) ? fn : (fn > 0 ? 1.0 : 0.0);
     for (;; ++it) {
       if (it > 0) {
         r = norm2(rn);
         if (r != SR_OK) return r;
         rel = fn > 0 ? rn / fn : 0.0;
+      }
+      if (!std::isfinite(rel)) {  // diverged (or a non-finite f): stop, report
+        s.unbind();
+        if (cycles) *cycles = it;
+        if (relres) *relres = rel;
+        return fail(h, SR_ERR_NONFINITE, "vsolve: the residual norm is not finite");
       }
       if (rel <= rtol || it == maxit) break;
       s.vcycle(M, s.fview(M));  // fig:mgv from level M
@@ -1569,8 +1589,8 @@ sr_status_t sr_fmg_solve_host_async(sr_fmg_t* h, const void* f_host, void* u_hos
   }
   const int k = (int)(h->hcalls & 1);
   if (!h->host_f[k]) {
-    CU(h, cudaMalloc(&h->host_f[k], fbytes));
-    CU(h, cudaMalloc(&h->host_u[k], ubytes));
+    CU(h, dev_alloc(h, &h->host_f[k], fbytes));
+    CU(h, dev_alloc(h, &h->host_u[k], ubytes));
   }
   // f -> slot k once the solve two calls back has finished reading it
   CU(h, cudaStreamWaitEvent(h->s_h2d, h->ev_solve[k], 0));

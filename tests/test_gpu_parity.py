@@ -720,3 +720,40 @@ def test_c5_full_size_linearity_and_scaling():
         d = float(torch.linalg.vector_norm(u13 - (u1 + u3)) / torch.linalg.vector_norm(u13))
         assert d <= 1e-12, d
         assert torch.isfinite(u1).all()
+
+
+# ---- ABI details of SURVEY §8(b): the descriptor's allocator hooks, SR_ERR_NONFINITE ------
+def test_torch_caching_allocator_backs_the_workspace():
+    # desc.alloc / desc.free through PyTorch's caching allocator: same results bitwise, the
+    # workspace is visible to torch while the handle lives and returned at close
+    n = (64, 64, 64)
+    f = torch.from_numpy(W.make_rhs("manufactured+noise", n)).cuda()
+    with Solver(n, 5, seg=16, buffer=2, K=2) as s:
+        ref = s.solve(f).cpu().numpy()
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    s = Solver(n, 5, seg=16, buffer=2, K=2, allocator="torch")
+    during = torch.cuda.memory_allocated()
+    assert during - before >= s.workspace_bytes
+    u = s.solve(f).cpu().numpy()
+    u2 = s.solve_host(f.cpu()).numpy()  # host-pipeline device slots: the hooks again
+    s.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() <= before + 4096
+    assert np.array_equal(u, ref)
+    assert np.array_equal(u2, ref)
+
+
+def test_vsolve_nonfinite_rhs_is_reported():
+    from paper_1406_7808_b200 import SrError
+    from paper_1406_7808_b200._lib import SR_ERR_NONFINITE
+    n, M = (32, 32, 32), 4
+    f = W.make_rhs("manufactured", n)
+    bad = f.copy()
+    bad[3, 4, 5] = np.nan
+    with Solver(n, M, K=0) as s:
+        with pytest.raises(SrError) as ei:
+            s.vsolve(torch.from_numpy(bad).cuda())
+        assert ei.value.status == SR_ERR_NONFINITE
+        u, cyc, rel = s.vsolve(torch.from_numpy(f).cuda())  # the handle stays usable
+        assert rel <= 1e-4 and np.isfinite(u.cpu().numpy()).all()
