@@ -35,6 +35,7 @@ WORKLOADS = {
     "C2": ((128, 128, 128), 6, 32, 2, 3, "manufactured"),
     "C3": ((512, 512, 512), 8, 64, 2, 4, "manufactured+noise"),
     "C5": ((1024, 1024, 1024), 9, 128, 2, 4, "bumps"),
+    "C5-s32": ((1024, 1024, 1024), 9, 32, 2, 4, "bumps"),  # C5's other segment size
     # the paper's own model problem: Omega = [0,2]x[0,1]^2, 27-point operator
     # (use with --stencil 27pt), 64^3 segments, J = 2, K = 4, pN0V = 4
     "P27": ((1024, 512, 512), 8, 64, 2, 4, "manufactured"),

@@ -718,6 +718,15 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
   if (a40 == 2 && try_spec<T, 40, 10, 4>(L, a, b, nst, st)) return true;
   if (a24 == 1 && try_spec<T, 24, 11, 4>(L, a, b, nst, st)) return true;
   if (a24 == 2 && try_spec<T, 24, 8, 3>(L, a, b, nst, st)) return true;
+  // E = 134 (128^3 segments, C5): 14-row bands of 544 threads, one CTA per SM
+  // (SR_FMG_CHEB2_ALT136=1: 6-row bands, two CTAs per SM)
+  static int a136 = -1;
+  if (a136 < 0) {
+    const char* e = std::getenv("SR_FMG_CHEB2_ALT136");
+    a136 = e ? std::atoi(e) : 0;
+  }
+  if (a136 == 1 && try_spec<T, 136, 6, 4>(L, a, b, nst, st)) return true;
+  if (try_spec<T, 136, 14, 4>(L, a, b, nst, st)) return true;
   if constexpr (sizeof(T) == 8)
     return try_spec<T, 72, 35, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
            try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);
@@ -820,7 +829,7 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
 template <class T>
 bool cheb_spec_ok(const Lvl& L) {
   if (!spec_enabled() || !get_encode() || ((long long)L.N[0] * sizeof(T)) % 16) return false;
-  const int pys[4] = {72, 40, 24, 16};
+  const int pys[5] = {136, 72, 40, 24, 16};
   for (int p : pys)
     if (L.py == p && L.E[0] <= p) return true;
   return false;

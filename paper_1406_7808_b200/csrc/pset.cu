@@ -294,7 +294,7 @@ bool try_pset(const Lvl& L, const Lvl& Lc, const T* w, T* uout, const FusedRhs<T
   if (L.py != PY || L.E[0] > PY || !b.global) return false;
   const int cpl = (int)(((long long)G::CROWS * Lc.py + G::A - 1) / G::A * G::A);
   const size_t smem = G::smem(cpl);
-  const int smax = (NB >= 4 ? 56 : NB == 3 ? 75 : 113) * 1024;  // NB CTAs per SM
+  const int smax = (NB >= 4 ? 56 : NB == 3 ? 75 : NB == 2 ? 113 : 227) * 1024;  // CTAs per SM
   if (smem > (size_t)smax) return false;
   if (!launch) return true;
   PsetArgs<T> a{};
@@ -329,6 +329,7 @@ bool pset_geom(int alt, const Lvl& L, const Lvl& Lc, const T* w, T* uout, const 
   if (alt == 1 && try_pset<T, 72, 14, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch)) return true;
   if (alt == 3 && try_pset<T, 40, 14, 4, ZQ, 3>(L, Lc, w, uout, b, c0, st, launch)) return true;
   return try_pset<T, 72, 10, 4, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch) ||
+         try_pset<T, 136, 10, 4, ZQ, 1>(L, Lc, w, uout, b, c0, st, launch) ||
          try_pset<T, 40, 10, 4, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch) ||
          try_pset<T, 40, 12, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch);
 }

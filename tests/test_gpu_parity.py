@@ -404,6 +404,7 @@ PSET_CASES = [
     ("J0-S64", (128, 128, 128), 6, 64, 0, 2, "manufactured+noise"),
     ("J2-S32", (128, 128, 128), 6, 32, 2, 2, "manufactured+noise"),
     ("noncubic", (128, 64, 192), 5, 64, 2, 2, "random"),
+    ("S128", (128, 128, 128), 6, 128, 2, 2, "bumps"),  # E = 134 boxes (C5's 128^3 segments)
 ]
 
 
