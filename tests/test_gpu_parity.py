@@ -758,3 +758,32 @@ def test_vsolve_nonfinite_rhs_is_reported():
         assert ei.value.status == SR_ERR_NONFINITE
         u, cyc, rel = s.vsolve(torch.from_numpy(f).cuda())  # the handle stays usable
         assert rel <= 1e-4 and np.isfinite(u.cpu().numpy()).all()
+
+
+def test_allocator_failure_releases_everything():
+    # an allocator that fails part-way through create: SR_ERR_OUT_OF_MEMORY, no handle, and
+    # every buffer handed out before the failure is given back through desc.free
+    import ctypes
+    from paper_1406_7808_b200 import _lib
+    from paper_1406_7808_b200.api import make_desc
+    live, calls = set(), [0]
+
+    def _alloc(nbytes, ctx):
+        calls[0] += 1
+        if calls[0] > 5:
+            return None
+        p = torch.cuda.caching_allocator_alloc(int(nbytes))
+        live.add(p)
+        return p
+
+    def _free(p, ctx):
+        live.discard(p)
+        torch.cuda.caching_allocator_delete(p)
+
+    acb, fcb = _lib.ALLOC_FN(_alloc), _lib.FREE_FN(_free)
+    d = make_desc((64, 64, 64), 5, 16, 2, 2)
+    d.alloc, d.free = acb, fcb
+    h = ctypes.c_void_p()
+    st = _lib.lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(h))
+    assert st == _lib.SR_ERR_OUT_OF_MEMORY and not h.value
+    assert calls[0] == 6 and not live
