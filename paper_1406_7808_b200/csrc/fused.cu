@@ -695,8 +695,9 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
   }
   // E = 70 (64^3 segments, J = 2): 5 bands of 14 rows, 2+ CTAs per SM by default (fp64:
   // 0.77 vs 0.85 ms for 2 bands of 35 at C3's finest level); SR_FMG_CHEB2_ALT picks others
-  // fp32: 10-row bands (0.506 vs 0.522 ms per C3 finest pass, measured)
-  if (alt == 1 && sizeof(T) == 4 && try_spec<T, 72, 10, 4>(L, a, b, nst, st)) return true;
+  // fp32: 14-row bands of 8 cells per thread (C3 finest pair 0.991 vs 1.032 ms for 10-row
+  // bands of 4, measured)
+  if (alt == 1 && sizeof(T) == 4 && try_spec<T, 72, 14, 8>(L, a, b, nst, st)) return true;
   if (alt == 1 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
   if (alt == 2 && try_spec<T, 72, 18, 4>(L, a, b, nst, st)) return true;
   if (alt == 3 && try_spec<T, 72, 24, 4>(L, a, b, nst, st)) return true;
