@@ -327,6 +327,10 @@ bool pset_geom(int alt, const Lvl& L, const Lvl& Lc, const T* w, T* uout, const 
                double c0, cudaStream_t st, bool launch) {
   constexpr int NB = sizeof(T) == 4 ? 3 : 2;
   if (alt == 1 && try_pset<T, 72, 14, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch)) return true;
+  // fp32: 14-row bands of 8 cells per thread (0.365 vs 0.414 ms at C3's finest level)
+  if (sizeof(T) == 4 && alt != 1 &&
+      try_pset<T, 72, 14, 8, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch))
+    return true;
   if (alt == 3 && try_pset<T, 40, 14, 4, ZQ, 3>(L, Lc, w, uout, b, c0, st, launch)) return true;
   return try_pset<T, 72, 10, 4, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch) ||
          try_pset<T, 136, 10, 4, ZQ, 1>(L, Lc, w, uout, b, c0, st, launch) ||
