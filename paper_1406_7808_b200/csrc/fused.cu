@@ -717,10 +717,9 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
   }
   if (a40 == 1 && try_spec<T, 40, 13, 4>(L, a, b, nst, st)) return true;
   if (a40 == 2 && try_spec<T, 40, 10, 4>(L, a, b, nst, st)) return true;
-  if (a40 == 3 && try_spec<T, 40, 14, 8>(L, a, b, nst, st)) return true;
+  // (measured at C3 level 7, fp64: 19-row bands of 3 cells 0.60 ms; 22-row bands of 6
+  // cells 0.71, 16 of 6 0.73, 22 of 8 0.76; fp32: 22 of 8 0.38, 14 of 8 0.45, 38 of 8 0.57)
   if (a40 == 4 && try_spec<T, 40, 22, 8>(L, a, b, nst, st)) return true;
-  if (a40 == 5 && try_spec<T, 40, 38, 8>(L, a, b, nst, st)) return true;
-  if (a24 == 3 && try_spec<T, 24, 22, 8>(L, a, b, nst, st)) return true;
   // fp32 at E = 38: 22-row bands of 8 cells per thread (C3 level 7: 0.38 vs 0.51 ms)
   if (sizeof(T) == 4 && a40 == 0 && try_spec<T, 40, 22, 8>(L, a, b, nst, st)) return true;
   if (a24 == 1 && try_spec<T, 24, 11, 4>(L, a, b, nst, st)) return true;
