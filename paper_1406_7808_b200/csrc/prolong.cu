@@ -9,6 +9,7 @@
 // 2P and 2P+1).  Reflected coarse ghosts (R3) enter as signed weights (x, y) and signed
 // interpolants (z).  Output is written straight from registers (coalesced rows).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 
 #include "fused.cuh"
@@ -217,7 +218,14 @@ template <class T>
 void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
                         cudaStream_t st) {
   constexpr int MAXS = 3;
-  const int nb = (Lf.E[1] + 17) / 18;
+  static const int tgt_env = [] {  // target band height (SR_FMG_PROLONG_BH, tuning)
+    const char* e = std::getenv("SR_FMG_PROLONG_BH");
+    return e ? std::max(3, std::atoi(e)) : 0;
+  }();
+  // measured at C3: 18-row bands at E = 70 (0.55 ms; 10: 0.61, 24: 0.66), two 19-row bands at
+  // E = 38 (0.22 ms for the level's two launches; three of 13: 0.24)
+  const int tgt = tgt_env ? tgt_env : (Lf.E[1] <= 40 ? 24 : 18);
+  const int nb = (Lf.E[1] + tgt - 1) / tgt;
   const int BH = (Lf.E[1] + nb - 1) / nb;
   ProlongArgs<T> a{};
   a.Lf = Lf;
