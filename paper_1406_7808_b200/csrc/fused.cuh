@@ -60,6 +60,11 @@ template <class T>
 void launch_cheb27_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, int nst,
                          double c0, double cm, double cr, cudaStream_t st, FinalOut<T> fin);
 
+// tau (Eq. 4) fused in front of the degree-2 27-point pass (R in its own buffer; rhs and t
+// written); false: no instantiation, nothing launched
+template <class T>
+bool launch_tau_cheb27_fused(const Lvl& L, const T* u_in, T* u_out, const T* R, T* rhs, T* t,
+                             int jr, double c0, double cm, double cr, cudaStream_t st);
 // r = b - A u (27-point) on the C cells of every segment into r (same layout as u)
 template <class T>
 void launch_resid27_fused(const Lvl& L, const T* u, T* r, FusedRhs<T> b, cudaStream_t st);

@@ -38,6 +38,11 @@ struct C27Args {
   T c0, cm, cr;
   FinalOut<T> fin;
   int foff[3];
+  // FIN = 3: tau (Eq. 4) in front of the degree-2 pass: rhs_seg holds R (its own buffer),
+  // rhs = R + A u0 on F, A u0 on C \ F and t = u0 are written (as k_cheb2s FIN = 2)
+  T* rhs_out;
+  T* tout;
+  int jr;
 };
 
 template <class T, int PY, int BH, int MAXS, int RG>
@@ -141,6 +146,19 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
     sym[k] = ylo ? T(-1) : T(1);
     syp[k] = yhi ? T(-1) : T(1);
   }
+  // FIN = 3: slots in F = grow(V, jr) (x, y), F in z, and the rhs / t rows
+  unsigned f_mask = 0;
+  int fz0 = 0, fz1 = 0;
+  if constexpr (FIN == 3) {
+    const bool fx = gx >= px * L.S[0] - a.jr && gx < (px + 1) * L.S[0] + a.jr;
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) {
+      const int gy = oy + y0 + k;
+      if (fx && gy >= pyy * L.S[1] - a.jr && gy < (pyy + 1) * L.S[1] + a.jr) f_mask |= 1u << k;
+    }
+    fz0 = pzz * L.S[2] - a.jr;
+    fz1 = (pzz + 1) * L.S[2] + a.jr;
+  }
   const int po = (y0 - s0 + 1) * PY + tx;  // own row 0 in a u0 / u1 plane
   const int fo = (y0 - s0) * G::FP + tx + fsh;
   T* const ob = oseg + (long long)y0 * PY + tx;
@@ -196,10 +214,27 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
       const T* fp = fs + (z % G::RF) * G::FS + fo;
       T* u1w = u1s + (z % G::R1) * G::PL + po;
       const unsigned act = zc ? c_mask : 0u;
+      const unsigned fm = (FIN == 3 && gz >= fz0 && gz < fz1) ? f_mask : 0u;
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
         const T v0 = p0[k * PY];
-        const T r = fp[k * G::FP] - A27(pm, p0, pp, szm, szp, k, v0);
+        T r;
+        if constexpr (FIN == 3) {
+          // tau (Eq. 4, fig:mgvsr L234-236) and the first step's residual rhs - A u0
+          const T Au = A27(pm, p0, pp, szm, szp, k, v0);
+          const T Rv = fp[k * G::FP];
+          const T bv = ((fm >> k) & 1u) ? Rv + Au : Au;
+          r = bv - Au;
+          const bool cc = (act >> k) & 1u;
+          const_cast<T*>(fp)[k * G::FP] = cc ? bv : Rv;  // stage 2 reads the new rhs
+          if (((w_mask >> k) & 1u) && gz >= 0 && gz < L.N[2]) {
+            const long long o = (long long)s * L.ss + (long long)z * pz + (long long)(y0 + k) * PY + tx;
+            if (cc) a.rhs_out[o] = bv;
+            a.tout[o] = v0;  // t = u0
+          }
+        } else {
+          r = fp[k * G::FP] - A27(pm, p0, pp, szm, szp, k, v0);
+        }
         const T v1 = ((act >> k) & 1u) ? v0 + c0 * r : v0;
         if constexpr (FIN == 2) {  // residual mode: r = b - A u0 on C (restriction input)
           if (((w_mask >> k) & 1u) && gz >= 0 && gz < L.N[2]) ob[(long long)z * pz + k * PY] = r;
@@ -243,7 +278,7 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
             const T r = fp[k * G::FP] - A27(pm, p0, pp, szm, szp, k, c1);
             const T v2 = ((act >> k) & 1u) ? c1 + cm * (c1 - u0r[k][J]) + cr * r : u0r[k][J];
             if (!((w_mask >> k) & 1u)) continue;
-            if constexpr (FIN == 0) {
+            if constexpr (FIN != 1) {
               orow[k * PY] = v2;
             } else {
               const int y = y0 + k, vlo = L.J + 1;
@@ -284,6 +319,7 @@ bool try27(const Lvl& L, const C27Args<T>& a, const FusedRhs<T>& b, int nst, int
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, nt, smem, st>>>(map, a);
   };
+  if (b.global && fin == 3) return false;
   if (b.global) {
     if (!encode_dense_tmap<T>(&map, b, G::FP, BH + 2)) return false;
     if (fin == 2) go(k_cheb27s<T, PY, BH, MAXS, 1, 1, 2>, G::SMEM, G::NT);
@@ -293,7 +329,8 @@ bool try27(const Lvl& L, const C27Args<T>& a, const FusedRhs<T>& b, int nst, int
     else go(k_cheb27s<T, PY, BH, MAXS, 1, 1, 0>, G::SMEM, G::NT);
   } else {
     using G0 = G27<T, PY, BH, MAXS, 0>;
-    if (fin == 2) go(k_cheb27s<T, PY, BH, MAXS, 0, 1, 2>, G0::SMEM, G0::NT);
+    if (fin == 3) go(k_cheb27s<T, PY, BH, MAXS, 0, 2, 3>, G0::SMEM, G0::NT);
+    else if (fin == 2) go(k_cheb27s<T, PY, BH, MAXS, 0, 1, 2>, G0::SMEM, G0::NT);
     else if (nst == 2 && fin) go(k_cheb27s<T, PY, BH, MAXS, 0, 2, 1>, G0::SMEM, G0::NT);
     else if (nst == 2) go(k_cheb27s<T, PY, BH, MAXS, 0, 2, 0>, G0::SMEM, G0::NT);
     else if (fin) go(k_cheb27s<T, PY, BH, MAXS, 0, 1, 1>, G0::SMEM, G0::NT);
@@ -335,6 +372,33 @@ void launch_cheb27_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, i
   for (int d = 0; d < 3; ++d) a.foff[d] = b.global ? b.off[d] : 0;
   dispatch27<T>(L, a, b, nst, fin.p != nullptr ? 1 : 0, st, true);
 }
+
+// tau (Eq. 4) fused in front of the degree-2 27-point pass: R read from its own buffer
+template <class T>
+bool launch_tau_cheb27_fused(const Lvl& L, const T* u_in, T* u_out, const T* R, T* rhs, T* t,
+                             int jr, double c0, double cm, double cr, cudaStream_t st) {
+  C27Args<T> a{};
+  a.L = L;
+  a.uin = u_in;
+  a.uout = u_out;
+  a.rhs_seg = R;
+  a.c0 = (T)c0;
+  a.cm = (T)cm;
+  a.cr = (T)cr;
+  a.rhs_out = rhs;
+  a.tout = t;
+  a.jr = jr;
+  FusedRhs<T> b{};
+  b.p = R;
+  b.global = 0;
+  return dispatch27<T>(L, a, b, 2, 3, st, true);
+}
+template bool launch_tau_cheb27_fused<double>(const Lvl&, const double*, double*, const double*,
+                                              double*, double*, int, double, double, double,
+                                              cudaStream_t);
+template bool launch_tau_cheb27_fused<float>(const Lvl&, const float*, float*, const float*,
+                                             float*, float*, int, double, double, double,
+                                             cudaStream_t);
 
 template <class T>
 void launch_resid27_fused(const Lvl& L, const T* u, T* r, FusedRhs<T> b, cudaStream_t st) {

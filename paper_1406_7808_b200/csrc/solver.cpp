@@ -625,10 +625,6 @@ struct Schedule {
       if (fin) final_done = true;
       return;
     }
-    if (pend_tau == l) {  // (safety net: the fused pass did not apply)
-      pend_tau = -1;
-      tau_from_rres(l, pend_jr);
-    }
     if (deg == 1 && h->fused && !L.st27 && L.nlg == 0.0 &&
         (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 && L.E[1] >= h->fused_min_e)) &&
         tma_rhs_ok(b) && srfmg::cheb_spec_ok<T>(L)) {
@@ -652,6 +648,22 @@ struct Schedule {
         fo.sy = h->blk_n[0];
         fo.sz = (long long)h->blk_n[0] * h->blk_n[1];
       }
+      if (pend_tau == l && deg == 2 && !fin) {  // tau (Eq. 4) in front of the pass
+        pend_tau = -1;
+        bool done;
+        {
+          Launch g(h, st, KC_CHEB_FUSED, l,
+                   w * (3.0 * c.compute + 2.0 * (c.cg - c.compute) + c.compute + c.storage));
+          done = srfmg::launch_tau_cheb27_fused<T>(
+              L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], (const T*)bb.rres, (T*)bb.rhs,
+              (T*)bb.t, pend_jr, 1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
+        }
+        if (done) {
+          bb.cur = 1 - bb.cur;
+          return;
+        }
+        tau_from_rres(l, pend_jr);
+      }
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb27_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b), deg,
                                     1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st,
@@ -659,6 +671,10 @@ struct Schedule {
       bb.cur = 1 - bb.cur;
       if (fin) final_done = true;
       return;
+    }
+    if (pend_tau == l) {  // (safety net: the fused pass did not apply)
+      pend_tau = -1;
+      tau_from_rres(l, pend_jr);
     }
     int lat = bb.cur, oth = 1 - bb.cur;
     if (cx(l)) {  // recorded for the coarse-level executor (same steps, same ping-pong)
@@ -921,19 +937,18 @@ struct Schedule {
     // the restricted residual is f_{l-1} - avg8(A u) and f_l need not be read (7-point)
     const bool use_pyr = pyr && b.global && !L.st27 && h->restrict_pyr;
     Launch g(h, st, KC_RESTRICT, l, w * (use_pyr ? 8.0 + 1.0 + 2.0 : 16.0 + 2.0) * tgt);
+    // R goes to the level's rres buffer when its tau rides in the next pass (that pass
+    // writes rhs while neighbouring bands still read R)
+    T* rc = tau_fuse_ok(l - 1) ? (T*)h->B[l - 1].rres : (T*)h->B[l - 1].rhs;
     if (L.st27 && L.nlg == 0.0 && h->fused && tma_rhs_ok(b) && srfmg::cheb27_fused_ok<T>(L) &&
         (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148)) {
       // 27-point: TMA-fed residual pass into the free ping-pong buffer, then the averages
       T* scratch = (T*)h->B[l].u[1 - h->B[l].cur];
       srfmg::launch_resid27_fused<T>(L, U(l), scratch, frhs(b), st);
-      srfmg::launch_restrict_from_resid<T>(L, U(l), scratch, h->L[l - 1], U(l - 1),
-                                           (T*)h->B[l - 1].rhs, jr, st);
+      srfmg::launch_restrict_from_resid<T>(L, U(l), scratch, h->L[l - 1], U(l - 1), rc, jr, st);
       return;
     }
     // the free ping-pong buffer of level l is scratch for the 27-point residual
-    // R goes to the level's rres buffer when its tau rides in the next pass (that pass
-    // writes rhs while neighbouring bands still read R)
-    T* rc = tau_fuse_ok(l - 1) ? (T*)h->B[l - 1].rres : (T*)h->B[l - 1].rhs;
     srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), rc, jr, st,
                               (T*)h->B[l].u[1 - h->B[l].cur],
                               use_pyr ? fview(l - 1) : View<T>{});  // L113-115 / L233, L235
@@ -989,10 +1004,12 @@ struct Schedule {
   // as the fused degree-2 pre-smoothing with the segment-storage rhs
   bool tau_fuse_ok(int lc) const {
     const Lvl& L = h->L[lc];
-    return h->tau_fuse && h->B[lc].rres && lc > h->T && h->fused && !h->pass &&
-           !h->pass_restrict &&
-           h->d.nu1 == 2 && !L.st27 &&
-           L.nlg == 0.0 &&
+    const bool base = h->tau_fuse && h->B[lc].rres && lc > h->T && h->fused && !h->pass &&
+                      !h->pass_restrict && h->d.nu1 == 2 && L.nlg == 0.0;
+    if (L.st27)  // the 27-point pass (fused27.cu) under the conditions cheb() uses
+      return base && (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148) &&
+             srfmg::cheb27_fused_ok<T>(L);
+    return base &&
            (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
                          L.E[1] >= h->fused_min_e)) &&
            srfmg::cheb2_fused_ok<T>(L) && srfmg::cheb_spec_ok<T>(L);

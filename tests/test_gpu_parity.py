@@ -787,3 +787,20 @@ def test_allocator_failure_releases_everything():
     st = _lib.lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(h))
     assert st == _lib.SR_ERR_OUT_OF_MEMORY and not h.value
     assert calls[0] == 6 and not live
+
+
+@pytest.mark.parametrize("case", [("S32", (128, 64, 64), 5, 32, 2, 2), ("S16", (64, 32, 32), 4, 16, 2, 2)],
+                         ids=["S32", "S16"])
+def test_27pt_tau_fused_into_presmoothing(case, monkeypatch):
+    # the 27-point pass with the tau (Eq. 4) in front (fused27.cu FIN = 3) vs k_tau27
+    name, n, M, seg, J, K = case
+    h = 2.0 / n[0]
+    f = W.make_rhs("manufactured", n, h=h) + 1e-3 * W.random_field(n)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_TAU_FUSE", "1")
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt")
+    monkeypatch.setenv("SR_FMG_TAU_FUSE", "0")
+    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt")
+    assert rel_l2(u, b) <= 1e-13, (name, rel_l2(u, b))
+    ref = O.solve(f, O.Config(n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt"))
+    assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
