@@ -66,8 +66,10 @@ template <class T>
 bool launch_tau_cheb27_fused(const Lvl& L, const T* u_in, T* u_out, const T* R, T* rhs, T* t,
                              int jr, double c0, double cm, double cr, cudaStream_t st);
 // r = b - A u (27-point) on the C cells of every segment into r (same layout as u)
+// nof = 1: r = -A u (the rhs is not streamed; the restriction adds f_{l-1} from the pyramid)
 template <class T>
-void launch_resid27_fused(const Lvl& L, const T* u, T* r, FusedRhs<T> b, cudaStream_t st);
+void launch_resid27_fused(const Lvl& L, const T* u, T* r, FusedRhs<T> b, cudaStream_t st,
+                          int nof = 0);
 
 // A geometry-specialised instantiation exists for this level's row pitch.
 template <class T>

@@ -43,6 +43,7 @@ struct C27Args {
   T* rhs_out;
   T* tout;
   int jr;
+  int nof;  // FIN = 2 only: write -A u (the rhs is not streamed; R6 pyramid restriction)
 };
 
 template <class T, int PY, int BH, int MAXS, int RG>
@@ -114,9 +115,11 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
                &bars[G::RU + sl]);
   };
   constexpr int FLAG = NST == 2 ? 2 : 0;  // iterations an rhs plane stays in use
+  const bool nof = FIN == 2 && a.nof;
   if (threadIdx.x == 0) {  // fill both rings
     for (int z = 0; z < min(G::RU, Ez); ++z) issue_u0(z);
-    for (int z = 0; z < min(G::RF, Ez); ++z) issue_f(z);
+    if (!nof)
+      for (int z = 0; z < min(G::RF, Ez); ++z) issue_f(z);
   }
 
   const int tx = threadIdx.x % PY, g = threadIdx.x / PY;
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
     if (z < Ez) {  // ------------------------------------------ stage 1 at plane z
       if (z + 1 < Ez) mbar_wait(&bars[(z + 1) % G::RU], ((z + 1) / G::RU) & 1);
       mbar_wait(&bars[z % G::RU], (z / G::RU) & 1);
-      mbar_wait(&bars[G::RU + z % G::RF], (z / G::RF) & 1);
+      if (!nof) mbar_wait(&bars[G::RU + z % G::RF], (z / G::RF) & 1);
       const int gz = oz + z;
       const bool zc = gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2;
       const T* pm;
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
             a.tout[o] = v0;  // t = u0
           }
         } else {
-          r = fp[k * G::FP] - A27(pm, p0, pp, szm, szp, k, v0);
+          r = (nof ? T(0) : fp[k * G::FP]) - A27(pm, p0, pp, szm, szp, k, v0);
         }
         const T v1 = ((act >> k) & 1u) ? v0 + c0 * r : v0;
         if constexpr (FIN == 2) {  // residual mode: r = b - A u0 on C (restriction input)
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
     __syncthreads();  // the only barrier of the plane step
     if (threadIdx.x == 0) {
       if (z >= 1 && z - 1 + G::RU < Ez) issue_u0(z - 1 + G::RU);  // plane z-1 consumed
-      if (z - FLAG >= 0 && z - FLAG + G::RF < Ez) issue_f(z - FLAG + G::RF);
+      if (!nof && z - FLAG >= 0 && z - FLAG + G::RF < Ez) issue_f(z - FLAG + G::RF);
     }
   };
   const int nz = Ez + (NST == 2 ? 2 : 0);
@@ -401,20 +404,22 @@ template bool launch_tau_cheb27_fused<float>(const Lvl&, const float*, float*, c
                                              cudaStream_t);
 
 template <class T>
-void launch_resid27_fused(const Lvl& L, const T* u, T* r, FusedRhs<T> b, cudaStream_t st) {
+void launch_resid27_fused(const Lvl& L, const T* u, T* r, FusedRhs<T> b, cudaStream_t st,
+                          int nof) {
   C27Args<T> a{};
   a.L = L;
   a.uin = u;
   a.uout = r;
   a.rhs_seg = b.global ? nullptr : b.p;
+  a.nof = nof;
   a.c0 = T(1);
   for (int d = 0; d < 3; ++d) a.foff[d] = b.global ? b.off[d] : 0;
   dispatch27<T>(L, a, b, 1, 2, st, true);
 }
 template void launch_resid27_fused<double>(const Lvl&, const double*, double*, FusedRhs<double>,
-                                           cudaStream_t);
+                                           cudaStream_t, int);
 template void launch_resid27_fused<float>(const Lvl&, const float*, float*, FusedRhs<float>,
-                                          cudaStream_t);
+                                          cudaStream_t, int);
 
 template bool cheb27_fused_ok<double>(const Lvl&);
 template bool cheb27_fused_ok<float>(const Lvl&);

@@ -783,7 +783,7 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) k_avg8_ur(Lvl Lf, const T* __restrict__ uf,
                                                       const T* __restrict__ rf, Lvl Lc,
                                                       T* __restrict__ uc, T* __restrict__ rc,
-                                                      int jr) {
+                                                      int jr, View<T> bc) {
   int B[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) B[d] = Lf.S[d] / 2 + 2 * jr;
@@ -817,7 +817,9 @@ __global__ void __launch_bounds__(kThreads) k_avg8_ur(Lvl Lf, const T* __restric
     }
     const long long co = loc_off(Lc, cs, X[0] - oc[0], X[1] - oc[1], X[2] - oc[2]);
     uc[co] = su * T(0.125);
-    rc[co] = sr * T(0.125);
+    // bc.p: rf holds -A u only, R = f_{l-1} - avg8(A u) with f_{l-1} the R6 pyramid
+    rc[co] = bc.p ? bc.p[(long long)X[2] * bc.sz + (long long)X[1] * bc.sy + X[0]] + sr * T(0.125)
+                  : sr * T(0.125);
   }
 }
 
@@ -953,7 +955,8 @@ void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* u
       const ColCfg c = col_cfg(Lf.E[0], Lf.E[1], Lf.E[2], Lf.nsegs);
       k_cheb_step27c<T, 1><<<c.grid, c.block, 0, st>>>(Lf, uf, nullptr, bf, scratch, T(0), T(0),
                                                        0, c.ntx, c.zchunk);
-      k_avg8_ur<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, scratch, Lc, uc, rc, jr);
+      k_avg8_ur<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, scratch, Lc, uc, rc, jr,
+                                                        View<T>{});
     } else {
       k_restrict27<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr);
     }
@@ -966,10 +969,10 @@ void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* u
 
 template <class T>
 void launch_restrict_from_resid(const Lvl& Lf, const T* uf, const T* rf, const Lvl& Lc, T* uc,
-                                T* rc, int jr, cudaStream_t st) {
+                                T* rc, int jr, cudaStream_t st, View<T> bc) {
   long long n = Lf.nsegs;
   for (int d = 0; d < 3; ++d) n *= Lf.S[d] / 2 + 2 * jr;
-  k_avg8_ur<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, rf, Lc, uc, rc, jr);
+  k_avg8_ur<T><<<grid_for<T>(n), kThreads, 0, st>>>(Lf, uf, rf, Lc, uc, rc, jr, bc);
 }
 
 template <class T>
@@ -1037,7 +1040,7 @@ void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const
                                    cudaStream_t, T*, View<T>);                                 \
   template void launch_tau<T>(const Lvl&, const T*, T*, T*, int, cudaStream_t);                 \
   template void launch_restrict_from_resid<T>(const Lvl&, const T*, const T*, const Lvl&, T*, T*,  \
-                                              int, cudaStream_t);                                \
+                                              int, cudaStream_t, View<T>);                       \
   template void launch_prolong<T>(const Lvl&, T*, const Lvl&, const T*, const T*, int,          \
                                   cudaStream_t);                                               \
   template void launch_coarsest<T>(const Lvl&, T*, View<T>, const T*, cudaStream_t);            \

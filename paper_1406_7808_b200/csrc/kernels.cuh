@@ -59,7 +59,7 @@ void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st
 // uc = avg8(uf), rc = avg8(rf) on the restriction targets (rf: precomputed fine residual)
 template <class T>
 void launch_restrict_from_resid(const Lvl& Lf, const T* uf, const T* rf, const Lvl& Lc, T* uc,
-                                T* rc, int jr, cudaStream_t st);
+                                T* rc, int jr, cudaStream_t st, View<T> bc = View<T>{});
 template <class T>
 void launch_prolong(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
                     cudaStream_t st);

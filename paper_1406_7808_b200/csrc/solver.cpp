@@ -944,8 +944,11 @@ struct Schedule {
         (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148)) {
       // 27-point: TMA-fed residual pass into the free ping-pong buffer, then the averages
       T* scratch = (T*)h->B[l].u[1 - h->B[l].cur];
-      srfmg::launch_resid27_fused<T>(L, U(l), scratch, frhs(b), st);
-      srfmg::launch_restrict_from_resid<T>(L, U(l), scratch, h->L[l - 1], U(l - 1), rc, jr, st);
+      // f-visit: R = f_{l-1} - avg8(A u) from the R6 pyramid, f_l not streamed
+      const bool pyr27 = pyr && b.global && h->restrict_pyr;
+      srfmg::launch_resid27_fused<T>(L, U(l), scratch, frhs(b), st, pyr27 ? 1 : 0);
+      srfmg::launch_restrict_from_resid<T>(L, U(l), scratch, h->L[l - 1], U(l - 1), rc, jr, st,
+                                           pyr27 ? fview(l - 1) : View<T>{});
       return;
     }
     // the free ping-pong buffer of level l is scratch for the 27-point residual

@@ -804,3 +804,19 @@ def test_27pt_tau_fused_into_presmoothing(case, monkeypatch):
     assert rel_l2(u, b) <= 1e-13, (name, rel_l2(u, b))
     ref = O.solve(f, O.Config(n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt"))
     assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
+
+
+def test_27pt_restriction_via_pyramid(monkeypatch):
+    # f-visits of the 27-point path: the residual pass writes -A u and the averages add the
+    # pyramid's f_{l-1} (f_l not streamed); same solve up to rounding, oracle parity
+    n, M, seg, J, K = (128, 64, 64), 5, 32, 2, 2
+    h = 2.0 / n[0]
+    f = W.make_rhs("manufactured", n, h=h) + 1e-3 * W.random_field(n)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_RESTRICT_PYR", "1")
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt")
+    monkeypatch.setenv("SR_FMG_RESTRICT_PYR", "0")
+    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt")
+    assert rel_l2(u, b) <= 1e-13, rel_l2(u, b)
+    ref = O.solve(f, O.Config(n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt"))
+    assert rel_l2(u, ref) <= TOL64, rel_l2(u, ref)
