@@ -347,7 +347,8 @@ bool dispatch27(const Lvl& L, const C27Args<T>& a, const FusedRhs<T>& b, int nst
                 cudaStream_t st, bool launch) {
   return try27<T, 72, 10, 4>(L, a, b, nst, fin, st, launch) ||
          try27<T, 40, 10, 4>(L, a, b, nst, fin, st, launch) ||
-         try27<T, 24, 11, 4>(L, a, b, nst, fin, st, launch);
+         try27<T, 24, 11, 4>(L, a, b, nst, fin, st, launch) ||
+         try27<T, 16, 14, 2>(L, a, b, nst, fin, st, launch);  // E = 14 (8^3 segments)
 }
 
 }  // namespace
