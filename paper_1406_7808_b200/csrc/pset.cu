@@ -327,6 +327,8 @@ bool pset_geom(int alt, const Lvl& L, const Lvl& Lc, const T* w, T* uout, const 
                double c0, cudaStream_t st, bool launch) {
   constexpr int NB = sizeof(T) == 4 ? 3 : 2;
   if (alt == 1 && try_pset<T, 72, 14, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch)) return true;
+  // (also measured at C3 fp64: 6-row bands at 3 CTAs/SM 0.68 ms, 10-row bands of 6 cells
+  // 0.71 ms, against 0.60 ms for the default below)
   // fp32: 14-row bands of 8 cells per thread (0.365 vs 0.414 ms at C3's finest level)
   if (sizeof(T) == 4 && alt != 1 &&
       try_pset<T, 72, 14, 8, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch))
