@@ -335,6 +335,7 @@ bool pset_geom(int alt, const Lvl& L, const Lvl& Lc, const T* w, T* uout, const 
     return true;
   if (alt == 3 && try_pset<T, 40, 14, 4, ZQ, 3>(L, Lc, w, uout, b, c0, st, launch)) return true;
   return try_pset<T, 72, 10, 4, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch) ||
+         // E = 134: 10-row bands at one CTA per SM (4.9 ms at C5; 6-row bands at two: 6.7 ms)
          try_pset<T, 136, 10, 4, ZQ, 1>(L, Lc, w, uout, b, c0, st, launch) ||
          try_pset<T, 40, 10, 4, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch) ||
          try_pset<T, 40, 12, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch);
