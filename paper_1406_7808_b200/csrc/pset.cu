@@ -338,6 +338,10 @@ bool pset_geom(int alt, const Lvl& L, const Lvl& Lc, const T* w, T* uout, const 
          // E = 134: 10-row bands at one CTA per SM (4.9 ms at C5; 6-row bands at two: 6.7 ms)
          try_pset<T, 136, 10, 4, ZQ, 1>(L, Lc, w, uout, b, c0, st, launch) ||
          try_pset<T, 40, 10, 4, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch) ||
+         // E = 22 / 14 (levels 6 and 5 of C3): 47 / 22 us against 60 / 32 us for the
+         // separate prolongation and degree-1 pass (SR_FMG_PSET_ALT=8: off)
+         (alt != 8 && try_pset<T, 24, 10, 4, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch)) ||
+         (alt != 8 && try_pset<T, 16, 6, 2, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch)) ||
          try_pset<T, 40, 12, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch);
 }
 
