@@ -34,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     hdr_t = max([_mtime(os.path.join(CSRC, h)) for h in HEADERS] +
                 [_mtime(os.path.join(ROOT, "include", "sr_fmg.h")), _mtime(__file__)])
-    objs = []
+    objs, jobs = [], []
     for s in srcs:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
@@ -45,12 +45,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 cmd += ["-Xptxas", "-v"] if verbose else []
             else:
                 cmd += ["-x", "cu"]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed on {s}")
-            if verbose:
-                sys.stderr.write(r.stderr)
+            jobs.append((s, cmd))
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    workers = max(1, min(len(jobs), os.cpu_count() or 1))
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        results = list(ex.map(lambda j: (j[0], subprocess.run(j[1], capture_output=True, text=True)),
+                              jobs))
+    for s, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {s}")
+        if verbose:
+            sys.stderr.write(r.stderr)
     if force or _mtime(LIB) < max(_mtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"]
         r = subprocess.run(cmd, capture_output=True, text=True)
