@@ -11,8 +11,9 @@ transcribes.  Pins: tests/test_oracle_*.py.  Parity status p
   fill_bc_ghosts, apply_A, cheb, restrict_avg8, prolong, exact_solve  -> pinned
   Oracle.vconv / fmg_conventional / vsolve                            -> pinned
   Oracle.vsr / solve (SR)                                             -> pinned by
-      equivalences (huge buffer, one segment), region brute force, symmetry, O(h^2) and
-      GSR-freeze invariants; the paper's e_r table values are for a different stencil,
+      equivalences (huge buffer, one segment), region brute force, symmetry, O(h^2),
+      GSR-freeze invariants, the FASMGVSR fixed point at u_h*, the GSR increment by
+      every correction (R17) and the tau's zero residual on C \ F (R18); the paper's e_r table values are for a different stencil,
       so the e_r VALUES are "parity unpinned" (context only).
 """
 from .grid import Box, Field

@@ -7,7 +7,12 @@ What fixes SR independently of the oracle's own arithmetic:
   * symmetry: a symmetric f on a symmetric segment grid gives a symmetric u;
   * the paper's trends: e_r decreases with the buffer and with larger
     transition subdomains pN0V (PAPER.md:333, 351);
-  * frozen GSR cells: never changed by a smoother.
+  * frozen GSR cells: never changed by a smoother (PAPER.md:206-209);
+  * the SR V-cycle: u_h* (DST, tests/pins.py) in every segment is a fixed point of
+    FASMGVSR; every correction increments the GSR cells by exactly
+    P(w - t) (R17); the tau leaves a zero residual on C \ F and R on F (R18).  Mutations
+    checked by hand to fail these: GSR corrected on C only (k = 1 or k >= 2), b = 0 on
+    C \ F, b = R - A u on F, R dropped from b.
 The e_r VALUES of Tables 1-3 belong to a 27-point stencil on [0,2]x[0,1]^2: parity unpinned.
 """
 import itertools
@@ -271,3 +276,157 @@ def test_nl_sr_huge_buffer_and_one_segment_equal_fmg():
     assert np.array_equal(O.solve(f, Config(n=n, M=4, seg=32, buffer=2, K=2, nl_gamma=g)), ref)
     sr = O.solve(f, Config(n=n, M=4, seg=16, buffer=2, K=2, nl_gamma=g))
     assert np.abs(sr - u).max() < 5 * np.abs(ref - u).max()
+
+
+# ---- the SR V-cycle itself (fig:mgvsr) ---------------------------------
+def _load_exact(o, f):
+    """Every level and every segment holds (a restriction of) the exact discrete solution
+    u_h* = A_M^{-1} f (DST, tests/pins.py -- independent of the oracle); b_M^p = f on C."""
+    from tests import pins
+    M = o.M
+    ustar = pins.dst_solve(f, o.h[M])
+    pyr = {M: ustar}
+    for l in range(M, 0, -1):
+        a = pyr[l]
+        pyr[l - 1] = 0.125 * sum(a[i::2, j::2, k::2] for i in (0, 1) for j in (0, 1) for k in (0, 1))
+    for l in range(o.T + 1):
+        o.u[l][o.dom[l]] = pyr[l]
+    for l in range(o.T + 1, M + 1):
+        for p in o.segs:
+            u = O.Field(o.storage(l, p))
+            CG = o.CG(l, p)
+            u[CG] = pyr[l][tuple(slice(a, b) for a, b in zip(CG.lo, CG.hi))]
+            o.us[l][p] = u
+            b = O.Field(o.storage(l, p))       # coarse SR levels: set by the tau (L234-236)
+            if l == M:
+                C = o.C(l, p)
+                b[C] = f[tuple(slice(a, c) for a, c in zip(C.lo, C.hi))]
+            o.bs[l][p] = b
+    return ustar
+
+
+@pytest.mark.parametrize("K,S", [(2, 8), (3, 16)])
+def test_sr_vcycle_fixed_point_at_exact_discrete_solution(K, S):
+    # SURVEY §8(c)(iii): with u = u_h* in every segment the fine residual vanishes, so the
+    # FAS coarse problems (Eq. 4, fig:mgvsr L234-236: b = R + A u on F, A u on C \ F) have
+    # zero residual on every level and the correction w - t is zero: FASMGVSR(M) leaves u
+    # unchanged.  A wrong sign or a dropped term in the tau (e.g. b = 0 on C \ F, or
+    # b = R - A u) makes the coarse smoothers move u, and the fixed point breaks.
+    n = (32, 32, 32)
+    f = W.make_rhs("manufactured+noise", n)
+    o = Oracle(Config(n=n, M=4, seg=S, buffer=2, K=K))
+    ustar = _load_exact(o, f)
+    before = {p: o.us[o.M][p].copy() for p in o.segs}
+    o.vsr(o.M)
+    sc = np.abs(ustar).max()
+    worst = 0.0
+    for p in o.segs:
+        CG = o.CG(o.M, p)
+        worst = max(worst, np.abs(o.us[o.M][p][CG] - before[p][CG]).max())
+    assert worst <= 1e-12 * sc, worst / sc
+    # the coarse SR levels saw the consistent tau right-hand sides (a visit happened)
+    assert all(o.counters["vsr_visits"][l] == 1 for l in range(o.T + 1, o.M + 1))
+
+
+def _spy_vsr(o, on_cheb):
+    """Wrap Oracle.vsr / vconv / _cheb: on_cheb(phase, l, p, u, b, X) runs before each SR
+    smoothing, phase 'pre' (L232) or 'post' (L242); state['tT'] holds t_T at the k = 1
+    hand-off (the level-T values right after the restriction, L234)."""
+    state = {"active": {}, "tT": None}
+    orig_vsr, orig_vconv, orig_cheb = o.vsr, o.vconv, o._cheb
+
+    def vsr(l):
+        state["active"][l] = {}
+        orig_vsr(l)
+        del state["active"][l]
+
+    def vconv(l, b):
+        if l == o.T and (o.T + 1) in state["active"]:
+            state["tT"] = o.u[o.T][o.dom[o.T]].copy()
+        orig_vconv(l, b)
+
+    def cheb(deg, u, b, X, l):
+        if l in state["active"]:
+            p = next(q for q in o.segs if o.us[l][q] is u)
+            seen = state["active"][l]
+            phase = "post" if p in seen else "pre"
+            seen[p] = True
+            on_cheb(phase, l, p, u, b, X)
+        orig_cheb(deg, u, b, X, l)
+
+    o.vsr, o.vconv, o._cheb = vsr, vconv, cheb
+    return state
+
+
+def _gsr_mask(o, l, p):
+    st = o.storage(l, p)
+    m = np.zeros(st.shape, bool)
+    for box, val in ((st.intersect(o.dom[l]), True), (o.C(l, p), False)):
+        m[tuple(slice(a - s, b - s) for a, b, s in zip(box.lo, box.hi, st.lo))] = val
+    return m
+
+
+def test_corrections_increment_gsr_cells():
+    # R17 (PAPER.md:206-209, 221, 241): the correction u += P(w - t) acts on C u GSR, so
+    # between the pre- and post-smoothing of an SR visit every GSR cell changes by exactly
+    # P(w - t) (the smoother never touches GSR).  K = 3 covers the k = 1 hand-off (w - t
+    # from the conventional level T) and k >= 2 (w - t from the segment's own coarse level).
+    n = (32, 32, 32)
+    f = W.make_rhs("manufactured+noise", n)
+    o = Oracle(Config(n=n, M=4, seg=16, buffer=2, K=3))
+    saved, checked, moved = {}, [], [0.0]
+
+    def on_cheb(phase, l, p, u, b, X):
+        m = _gsr_mask(o, l, p)
+        if phase == "pre":
+            saved[(l, p)] = u.a.copy()      # GSR values: unchanged by this smoothing
+            return
+        lc = l - 1
+        if lc == o.T:
+            w = o.u[o.T]
+            e = O.Field(w.box, fill=0.0)
+            e[o.dom[o.T]] = w[o.dom[o.T]] - st["tT"]
+        else:
+            e = O.Field(o.us[lc][p].box, array=o.us[lc][p].a - o.ts[lc][p].a)
+        O.fill_bc_ghosts(e, o.dom[lc])
+        stb = o.storage(l, p)
+        inc = np.zeros(stb.shape)
+        CG = o.CG(l, p)
+        inc[tuple(slice(a - s, c - s) for a, c, s in zip(CG.lo, CG.hi, stb.lo))] = O.prolong(e, CG)
+        got = u.a[m] - saved[(l, p)][m]
+        np.testing.assert_allclose(got, inc[m], rtol=0, atol=1e-13 * np.abs(u.a[m]).max())
+        moved[0] = max(moved[0], np.abs(inc[m]).max() / np.abs(u.a[m]).max())
+        checked.append((l, p))
+
+    st = _spy_vsr(o, on_cheb)
+    o.solve(f)
+    # every SR level and segment, over all the FMG visits, was checked
+    assert {l for l, _ in checked} == set(range(o.T + 1, o.M + 1))
+    assert moved[0] > 1e-6, moved        # the increments are not trivially zero
+
+
+def test_tau_gives_zero_residual_on_c_minus_f():
+    # R18 (PAPER.md:213, 236): on C_{l-1} \ F the coarse rhs is A u (the coarse cells keep
+    # their value, zero effective residual); on F it is R + A(I u), so b - A u = R there.
+    n = (32, 32, 32)
+    f = W.make_rhs("manufactured+noise", n)
+    o = Oracle(Config(n=n, M=4, seg=8, buffer=4, K=3))
+    seen = []
+
+    def on_cheb(phase, l, p, u, b, X):
+        if phase != "pre" or (l + 1) not in st["active"]:
+            return        # (FMG visits of level l smooth against b = f_l)
+        Cc, Fb = o.C(l, p), o.F(l + 1, p)
+        ug = u.copy()
+        r = O.residual(ug, b, Cc, o.h[l], o.dom[l])
+        inF = np.zeros(Cc.shape, bool)
+        inF[tuple(slice(a - s, c - s) for a, c, s in zip(Fb.lo, Fb.hi, Cc.lo))] = True
+        assert (~inF).any() and inF.any()
+        scale = np.abs(O.apply_A(ug, Cc, o.h[l])).max()
+        assert np.abs(r[~inF]).max() <= 1e-13 * scale
+        assert np.abs(r[inF]).max() > 1e-8 * scale      # R itself, not zero
+        seen.append(l)
+
+    st = _spy_vsr(o, on_cheb)
+    o.solve(f)
+    assert set(seen) == set(range(o.T + 1, o.M))
