@@ -1,4 +1,4 @@
-"""CPU oracle for segmental-refinement FAS-FMG (arXiv 1406.7808).
+r"""CPU oracle for segmental-refinement FAS-FMG (arXiv 1406.7808).
 
 TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
 `cpu_baseline` / `--impl reference` legs may import this package.  The product path
@@ -13,8 +13,9 @@ transcribes.  Pins: tests/test_oracle_*.py.  Parity status p
   Oracle.vsr / solve (SR)                                             -> pinned by
       equivalences (huge buffer, one segment), region brute force, symmetry, O(h^2),
       GSR-freeze invariants, the FASMGVSR fixed point at u_h*, the GSR increment by
-      every correction (R17) and the tau's zero residual on C \ F (R18); the paper's e_r table values are for a different stencil,
-      so the e_r VALUES are "parity unpinned" (context only).
+      every correction (R17) and the tau's zero residual on C \ F (R18); the paper's e_r
+      table values are for a different stencil, so the e_r VALUES are "parity unpinned"
+      (context only).
 """
 from .grid import Box, Field
 from .ops import (apply_A, cheb, cheb_constants, dense_operator, exact_solve, fill_bc_ghosts,

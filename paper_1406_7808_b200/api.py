@@ -288,10 +288,10 @@ class Solver:
         (u, cycles, relative residual)."""
         import torch
         want = torch.float64 if self.dtype == "f64" else torch.float32
-        if not f.is_cuda or f.dtype != want or not f.is_contiguous():
-            raise ValueError("f must be a contiguous CUDA tensor of the solver's dtype")
+        self._check_tensor(f, "f", self.f_shape)
         if out is None:
             out = torch.empty(self.shape, dtype=want, device=f.device)
+        self._check_tensor(out, "out", self.shape)
         check(lib.sr_fmg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
               self._h)
         cyc, rel = ctypes.c_int32(0), ctypes.c_double(0.0)

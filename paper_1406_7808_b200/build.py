@@ -17,9 +17,8 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libsrfmg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["kernels.cu", "fused.cu", "fused27.cu", "prolong.cu", "pset.cu", "up.cu", "pass.cu", "coarse.cu",
-           "solver.cpp"]
-HEADERS = ["kernels.cuh", "fused.cuh", "tma.cuh", "pass.cuh", "coarse.cuh"]
+SOURCES = ["kernels.cu", "fused.cu", "fused27.cu", "prolong.cu", "pset.cu", "coarse.cu", "solver.cpp"]
+HEADERS = ["kernels.cuh", "fused.cuh", "tma.cuh", "coarse.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", CSRC,
          "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]

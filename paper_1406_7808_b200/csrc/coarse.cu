@@ -327,11 +327,8 @@ bool coarse_level_tiny(const Lvl& L) {
 template <class T>
 void launch_coarse_exec(const COpList<T>& ops, cudaStream_t st) {
   if (ops.n <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_coarse_exec<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
-  }
+  // (per launch: the attribute is per device, and a process may drive several)
+  cudaFuncSetAttribute(k_coarse_exec<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kCluster);
   cfg.blockDim = dim3(kThreadsC);

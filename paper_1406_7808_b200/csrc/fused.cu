@@ -552,24 +552,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// kernel variants (cells per thread, max threads): picked by SR_FMG_CHEB2_VARIANT
+// generic kernel (levels without a geometry-specialised instantiation): cells per thread
+// and the thread cap
 struct Variant {
   int maxs, nt;
 };
 template <class T>
 Variant variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SR_FMG_CHEB2_VARIANT");
-    v = e ? std::atoi(e) : 0;
-    if (v < 0 || v > 2) v = 0;
-  }
-  if (sizeof(T) == 8) {
-    const Variant t[3] = {{6, 512}, {3, 1024}, {4, 768}};
-    return t[v];
-  }
-  const Variant t[3] = {{8, 512}, {4, 1024}, {6, 768}};
-  return t[v];
+  return sizeof(T) == 8 ? Variant{6, 512} : Variant{8, 512};
 }
 
 struct Plan {
@@ -622,15 +612,6 @@ bool cheb2_fused_ok(const Lvl& L) {
 }
 
 namespace {
-
-bool spec_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SR_FMG_CHEB2_SPEC");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
 
 template <class T>
 bool encode_rhs_map(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows) {
@@ -687,58 +668,20 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
 
 template <class T>
 bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
-  if (!spec_enabled()) return false;
-  static int alt = -1;
-  if (alt < 0) {
-    const char* e = std::getenv("SR_FMG_CHEB2_ALT");
-    alt = e ? std::atoi(e) : 1;
-  }
-  // E = 70 (64^3 segments, J = 2): 5 bands of 14 rows, 2+ CTAs per SM by default (fp64:
-  // 0.77 vs 0.85 ms for 2 bands of 35 at C3's finest level); SR_FMG_CHEB2_ALT picks others
-  // fp32: 14-row bands of 8 cells per thread (C3 finest pair 0.991 vs 1.032 ms for 10-row
-  // bands of 4, measured)
-  if (alt == 1 && sizeof(T) == 4 && try_spec<T, 72, 14, 8>(L, a, b, nst, st)) return true;
-  if (alt == 1 && try_spec<T, 72, 14, 4>(L, a, b, nst, st)) return true;
-  if (alt == 2 && try_spec<T, 72, 18, 4>(L, a, b, nst, st)) return true;
-  if (alt == 3 && try_spec<T, 72, 24, 4>(L, a, b, nst, st)) return true;
-  if (alt == 4 && try_spec<T, 72, 14, 8>(L, a, b, nst, st)) return true;
-  if (alt == 5 && try_spec<T, 72, 22, 6>(L, a, b, nst, st)) return true;
-  if (alt == 6 && try_spec<T, 72, 10, 4>(L, a, b, nst, st)) return true;
-  if (alt == 7 && try_spec<T, 72, 14, 3>(L, a, b, nst, st)) return true;
-  if (alt == 8 && try_spec<T, 72, 14, 2>(L, a, b, nst, st)) return true;
-  if (alt == 9 && try_spec<T, 72, 16, 6>(L, a, b, nst, st)) return true;
-  // E = 38 / 22 boxes (32^3 / 16^3 segments): SR_FMG_CHEB2_ALT40 / _ALT24 pick band shapes
-  static int a40 = -1, a24 = -1;
-  if (a40 < 0) {
-    const char* e = std::getenv("SR_FMG_CHEB2_ALT40");
-    a40 = e ? std::atoi(e) : 0;
-    const char* f = std::getenv("SR_FMG_CHEB2_ALT24");
-    a24 = f ? std::atoi(f) : 0;
-  }
-  if (a40 == 1 && try_spec<T, 40, 13, 4>(L, a, b, nst, st)) return true;
-  if (a40 == 2 && try_spec<T, 40, 10, 4>(L, a, b, nst, st)) return true;
-  // (measured at C3 level 7, fp64: 19-row bands of 3 cells 0.60 ms; 22-row bands of 6
-  // cells 0.71, 16 of 6 0.73, 22 of 8 0.76; fp32: 22 of 8 0.38, 14 of 8 0.45, 38 of 8 0.57)
-  if (a40 == 4 && try_spec<T, 40, 22, 8>(L, a, b, nst, st)) return true;
-  // fp32 at E = 38: 22-row bands of 8 cells per thread (C3 level 7: 0.38 vs 0.51 ms)
-  if (sizeof(T) == 4 && a40 == 0 && try_spec<T, 40, 22, 8>(L, a, b, nst, st)) return true;
-  if (a24 == 1 && try_spec<T, 24, 11, 4>(L, a, b, nst, st)) return true;
-  if (a24 == 2 && try_spec<T, 24, 8, 3>(L, a, b, nst, st)) return true;
-  // E = 134 (128^3 segments, C5): 14-row bands of 544 threads, one CTA per SM
-  // (SR_FMG_CHEB2_ALT136=1: 6-row bands, two CTAs per SM)
-  static int a136 = -1;
-  if (a136 < 0) {
-    const char* e = std::getenv("SR_FMG_CHEB2_ALT136");
-    a136 = e ? std::atoi(e) : 0;
-  }
-  if (a136 == 1 && try_spec<T, 136, 6, 4>(L, a, b, nst, st)) return true;
-  if (try_spec<T, 136, 14, 4>(L, a, b, nst, st)) return true;
+  // Band shapes per row pitch, measured (C3, DESIGN.md §9 keeps the losing ones):
+  //  E = 70 (64^3 segments): 14-row bands; fp64 4 cells per thread (0.77 vs 0.85 ms for 2
+  //    bands of 35), fp32 8 cells per thread (finest pair 0.991 vs 1.032 ms for 10 of 4);
+  //  E = 38 (32^3): fp64 19-row bands of 3 cells (0.60 ms; 22 of 6: 0.71, 16 of 6: 0.73,
+  //    22 of 8: 0.76), fp32 22 of 8 (0.38; 14 of 8: 0.45, 38 of 8: 0.57);
+  //  E = 134 (128^3, C5): 14-row bands of 544 threads, one CTA per SM (6-row bands slower).
   if constexpr (sizeof(T) == 8)
-    return try_spec<T, 72, 35, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
-           try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);
+    return try_spec<T, 72, 14, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
+           try_spec<T, 136, 14, 4>(L, a, b, nst, st) || try_spec<T, 24, 22, 3>(L, a, b, nst, st) ||
+           try_spec<T, 16, 14, 2>(L, a, b, nst, st);
   else
-    return try_spec<T, 72, 70, 6>(L, a, b, nst, st) || try_spec<T, 40, 38, 4>(L, a, b, nst, st) ||
-           try_spec<T, 24, 22, 3>(L, a, b, nst, st) || try_spec<T, 16, 14, 2>(L, a, b, nst, st);
+    return try_spec<T, 72, 14, 8>(L, a, b, nst, st) || try_spec<T, 40, 22, 8>(L, a, b, nst, st) ||
+           try_spec<T, 136, 14, 4>(L, a, b, nst, st) || try_spec<T, 24, 22, 3>(L, a, b, nst, st) ||
+           try_spec<T, 16, 14, 2>(L, a, b, nst, st);
 }
 
 }  // namespace
@@ -826,15 +769,12 @@ void launch_cheb2_fused(const Lvl& L, const T* u_in, T* u_out, FusedRhs<T> b, do
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     kern<<<grid, pl.NT, pl.smem, st>>>(map, a);
   };
-  constexpr bool D = sizeof(T) == 8;
-  if (v.nt == 512) go(k_cheb2<T, D ? 6 : 8, 512>);
-  else if (v.nt == 1024) go(k_cheb2<T, D ? 3 : 4, 1024>);
-  else go(k_cheb2<T, D ? 4 : 6, 768>);
+  go(k_cheb2<T, sizeof(T) == 8 ? 6 : 8, 512>);
 }
 
 template <class T>
 bool cheb_spec_ok(const Lvl& L) {
-  if (!spec_enabled() || !get_encode() || ((long long)L.N[0] * sizeof(T)) % 16) return false;
+  if (!get_encode() || ((long long)L.N[0] * sizeof(T)) % 16) return false;
   const int pys[5] = {136, 72, 40, 24, 16};
   for (int p : pys)
     if (L.py == p && L.E[0] <= p) return true;

@@ -95,13 +95,4 @@ template <class T>
 bool launch_pset1_fused(const Lvl& L, const Lvl& Lc, const T* w, T* uout, FusedRhs<T> b,
                         double c0, cudaStream_t st);
 
-// Up half of an SR V-cycle visit in one pass (up.cu): u += P(w - t) (R10) on C u GSR, then
-// the degree-2 Chebyshev smoothing (R8); fin.p: last pass, genuine cells -> user u.
-template <class T>
-bool up2_fused_ok(const Lvl& L, const Lvl& Lc);
-template <class T>
-bool launch_up2_fused(const Lvl& L, const Lvl& Lc, const T* u_in, T* u_out, const T* w,
-                      const T* t, FusedRhs<T> b, double c0, double cm, double cr,
-                      cudaStream_t st, FinalOut<T> fin);
-
 }  // namespace srfmg

@@ -211,20 +211,20 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
 template <class T>
 bool prolong_tma_ok(const Lvl& Lf, const Lvl& Lc) {
   (void)Lc;
-  return (long long)Lf.nsegs * ((Lf.E[1] + 17) / 18) >= 148;
+  // enough bands to fill the GPU, counted over the GLOBAL segment grid so that every world
+  // size picks the same kernel (R25)
+  long long g = 1;
+  for (int i = 0; i < 3; ++i) g *= Lf.N[i] / Lf.S[i];
+  return g * ((Lf.E[1] + 17) / 18) >= 148;
 }
 
 template <class T>
 void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
                         cudaStream_t st) {
   constexpr int MAXS = 3;
-  static const int tgt_env = [] {  // target band height (SR_FMG_PROLONG_BH, tuning)
-    const char* e = std::getenv("SR_FMG_PROLONG_BH");
-    return e ? std::max(3, std::atoi(e)) : 0;
-  }();
   // measured at C3: 18-row bands at E = 70 (0.55 ms; 10: 0.61, 24: 0.66), two 19-row bands at
   // E = 38 (0.22 ms for the level's two launches; three of 13: 0.24)
-  const int tgt = tgt_env ? tgt_env : (Lf.E[1] <= 40 ? 24 : 18);
+  const int tgt = Lf.E[1] <= 40 ? 24 : 18;
   const int nb = (Lf.E[1] + tgt - 1) / tgt;
   const int BH = (Lf.E[1] + nb - 1) / nb;
   ProlongArgs<T> a{};

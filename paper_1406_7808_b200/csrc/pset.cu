@@ -309,40 +309,31 @@ bool try_pset(const Lvl& L, const Lvl& Lc, const T* w, T* uout, const FusedRhs<T
   std::memset(&map, 0, sizeof(map));
   if (!encode_dense_tmap<T>(&map, b, G::FP, G::TR)) return false;
   auto kern = k_pset1s<T, PY, BH, MAXS, ZQ, NB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-    attr = true;
-  }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);  // per device
   kern<<<dim3((L.E[1] + BH - 1) / BH, L.nsegs), G::NT, smem, st>>>(map, a);
   return true;
 }
 
 // band geometries (PY, BH, MAXS[, CTAs/SM]).  BH = 10 (three row groups, 216 threads) keeps
 // the fp64 kernel at 2 CTAs/SM within 128 registers (BH = 14, 288 threads, caps it at 96 and
-// it spills: 0.77 vs 0.67 ms at C3); fp32 fits 3 CTAs/SM.  At E = 38 (PY = 40) BH = 10 at
-// 4 CTAs/SM: 0.115 ms vs 0.172 ms for BH = 12 at 3.  SR_FMG_PSET_ALT=1|3: BH = 14 variants.
+// it spills: 0.77 vs 0.67 ms at C3; 6-row bands at 3 CTAs/SM 0.68 ms, 10-row bands of 6
+// cells 0.71 ms); fp32: 14-row bands of 8 cells per thread (0.365 vs 0.414 ms at C3's
+// finest level).  At E = 38 (PY = 40) BH = 10 at 4 CTAs/SM: 0.115 ms vs 0.172 ms for BH = 12
+// at 3 (BH = 14: slower).
 template <class T, int ZQ>
-bool pset_geom(int alt, const Lvl& L, const Lvl& Lc, const T* w, T* uout, const FusedRhs<T>& b,
+bool pset_geom(const Lvl& L, const Lvl& Lc, const T* w, T* uout, const FusedRhs<T>& b,
                double c0, cudaStream_t st, bool launch) {
   constexpr int NB = sizeof(T) == 4 ? 3 : 2;
-  if (alt == 1 && try_pset<T, 72, 14, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch)) return true;
-  // (also measured at C3 fp64: 6-row bands at 3 CTAs/SM 0.68 ms, 10-row bands of 6 cells
-  // 0.71 ms, against 0.60 ms for the default below)
-  // fp32: 14-row bands of 8 cells per thread (0.365 vs 0.414 ms at C3's finest level)
-  if (sizeof(T) == 4 && alt != 1 &&
-      try_pset<T, 72, 14, 8, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch))
+  if (sizeof(T) == 4 && try_pset<T, 72, 14, 8, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch))
     return true;
-  if (alt == 3 && try_pset<T, 40, 14, 4, ZQ, 3>(L, Lc, w, uout, b, c0, st, launch)) return true;
   return try_pset<T, 72, 10, 4, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch) ||
          // E = 134: 10-row bands at one CTA per SM (4.9 ms at C5; 6-row bands at two: 6.7 ms)
          try_pset<T, 136, 10, 4, ZQ, 1>(L, Lc, w, uout, b, c0, st, launch) ||
          try_pset<T, 40, 10, 4, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch) ||
          // E = 22 / 14 (levels 6 and 5 of C3): 47 / 22 us against 60 / 32 us for the
-         // separate prolongation and degree-1 pass (SR_FMG_PSET_ALT=8: off)
-         (alt != 8 && try_pset<T, 24, 10, 4, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch)) ||
-         (alt != 8 && try_pset<T, 16, 6, 2, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch)) ||
-         try_pset<T, 40, 12, 4, ZQ>(L, Lc, w, uout, b, c0, st, launch);
+         // separate prolongation and degree-1 pass
+         try_pset<T, 24, 10, 4, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch) ||
+         try_pset<T, 16, 6, 2, ZQ, 4>(L, Lc, w, uout, b, c0, st, launch);
 }
 
 template <class T>
@@ -350,15 +341,11 @@ bool pset_dispatch(const Lvl& L, const Lvl& Lc, const T* w, T* uout, const Fused
                    double c0, cudaStream_t st, bool launch) {
   // S_z % 4: the segment origins oz = p S - (J+1) all share one residue mod 4
   if (L.st27 || L.nlg != 0.0 || (L.S[0] | L.S[1]) & 1 || L.S[2] & 3) return false;
-  static const int alt = [] {
-    const char* e = std::getenv("SR_FMG_PSET_ALT");
-    return e ? std::atoi(e) : 0;
-  }();
   switch ((L.J + 1) & 3) {
-    case 0: return pset_geom<T, 0>(alt, L, Lc, w, uout, b, c0, st, launch);
-    case 1: return pset_geom<T, 1>(alt, L, Lc, w, uout, b, c0, st, launch);
-    case 2: return pset_geom<T, 2>(alt, L, Lc, w, uout, b, c0, st, launch);
-    default: return pset_geom<T, 3>(alt, L, Lc, w, uout, b, c0, st, launch);
+    case 0: return pset_geom<T, 0>(L, Lc, w, uout, b, c0, st, launch);
+    case 1: return pset_geom<T, 1>(L, Lc, w, uout, b, c0, st, launch);
+    case 2: return pset_geom<T, 2>(L, Lc, w, uout, b, c0, st, launch);
+    default: return pset_geom<T, 3>(L, Lc, w, uout, b, c0, st, launch);
   }
 }
 

@@ -18,7 +18,6 @@
 #include "fused.cuh"
 #include "kernels.cuh"
 #include "coarse.cuh"
-#include "pass.cuh"
 #include "sr_fmg.h"
 
 using srfmg::Lvl;
@@ -104,19 +103,9 @@ struct sr_fmg {
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
   bool force = false; // SR_FMG_FORCE_FUSED=1: use them even on levels too small to fill the GPU
   int fused_min_e = 0; // SR_FMG_FUSED_MIN_E: smallest storage extent given to the TMA kernels
-  // fused multi-stage SR passes (pass.cu), SR_FMG_PASS=1|3|4.  pass_entry picks the
-  // FMG-entry chain: 4 = Pi+S1+S2+restrict, 3 = Pi+S1+S2 then restrict, 1 = Pi+S1
-  bool pass = false;
-  int pass_entry = 0;      // 0: unfused entry
-  bool pass_down = false;  // (LOAD, 2, RESTRICT)
-  bool pass_up = false;    // (PADD, 2, STORE|FINAL)
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
   bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
   bool tau_fuse = true;      // tau inside the next pre-smoothing pass; SR_FMG_TAU_FUSE=0 off
-  bool up_fuse = false;      // correction + post-smoothing in one pass (up.cu), opt-in
-                             // (SR_FMG_UP_FUSE=1): slower in fp64, DESIGN.md §9
-  bool pass_restrict = false;  // (LOAD, 0, RESTRICT) for the restriction (SR_FMG_PASS_RESTRICT=1;
-                              // measured equal to k_restrict in fp64, slower in fp32)
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
   // disables it.  flush_fn: enqueue the recorded operations (called before every launch)
   bool cexec = true;
@@ -193,7 +182,9 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
   if (d->stencil != 7 && d->stencil != 27) return bad("stencil must be 7 or 27");
   if (!(d->nl_gamma >= 0) || !std::isfinite(d->nl_gamma)) return bad("nl_gamma must be >= 0");
   if (d->world < 1) return bad("world must be >= 1");
-  if (d->world != d->pgrid[0] * d->pgrid[1] * d->pgrid[2]) return bad("world != prod(pgrid)");
+  for (int i = 0; i < 3; ++i)
+    if (d->pgrid[i] < 1 || d->pgrid[i] > d->world) return bad("need 1 <= pgrid[d] <= world");
+  if ((long long)d->pgrid[0] * d->pgrid[1] * d->pgrid[2] != d->world) return bad("world != prod(pgrid)");
   if (d->rank < 0 || d->rank >= d->world) return bad("rank out of range");
   if (d->world > 1) {
     for (int i = 0; i < 3; ++i)
@@ -204,6 +195,14 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
   if (d->world > 1 && d->comm != 0 && d->comm != 1) {
     msg = "comm must be 0 (NCCL) or 1 (replay store)";
     return SR_ERR_UNSUPPORTED_CONFIG;
+  }
+  if (d->sr_levels > 0) {  // every launch puts a rank's segments in gridDim.y (<= 65535)
+    long long ns = 1;
+    for (int i = 0; i < 3; ++i) ns *= (d->n[i] / d->seg) / d->pgrid[i];
+    if (ns > 65535) {
+      msg = "more than 65535 segments per rank; use larger segments or more ranks";
+      return SR_ERR_UNSUPPORTED_CONFIG;
+    }
   }
   long long n0 = 1;
   for (int i = 0; i < 3; ++i) n0 *= d->n[i] >> d->M;
@@ -566,6 +565,16 @@ struct Schedule {
     return o;
   }
 
+  // The fused kernels march z inside a CTA: they are used when segments x bands of `rows`
+  // fill the GPU; tiny levels are latency-bound and run faster as z-chunked step kernels.
+  // The count is over the GLOBAL segment grid, so every world size picks the same kernels
+  // and the result does not depend on the partition (R25, bitwise).
+  bool fills(const Lvl& L, int rows) const {
+    long long g = 1;
+    for (int i = 0; i < 3; ++i) g *= L.N[i] / L.S[i];
+    return h->force || g * ((L.E[1] + rows - 1) / rows) >= 148;
+  }
+
   // S^deg(L_l, u_l, b) on C_l of every segment (R8): ping-pong between the two buffers
   T* final_out = nullptr;  // user u: the last level-M smoothing writes it directly (R19)
   bool pyr = false;        // the f pyramid f_l (R6) of this solve is built
@@ -585,7 +594,7 @@ struct Schedule {
     // the fused pass marches z inside a CTA: use it only when segments x bands fill the
     // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
     if (deg == 2 && h->fused && !L.st27 && L.nlg == 0.0 &&
-        (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 && L.E[1] >= h->fused_min_e)) &&
+        (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
         tma_rhs_ok(b) && srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
       const double rho0 = 1.0 / h->sigma[l];
@@ -626,7 +635,7 @@ struct Schedule {
       return;
     }
     if (deg == 1 && h->fused && !L.st27 && L.nlg == 0.0 &&
-        (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 && L.E[1] >= h->fused_min_e)) &&
+        (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
         tma_rhs_ok(b) && srfmg::cheb_spec_ok<T>(L)) {
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb1_fused<T>(L, (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b),
@@ -635,7 +644,7 @@ struct Schedule {
       return;
     }
     if ((deg == 1 || deg == 2) && h->fused && L.st27 && L.nlg == 0.0 && tma_rhs_ok(b) &&
-        (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148) &&
+        fills(L, 10) &&
         srfmg::cheb27_fused_ok<T>(L)) {
       // 27-point operator: the whole polynomial in one TMA-fed pass (fused27.cu)
       const double rho0 = 1.0 / h->sigma[l];
@@ -766,8 +775,7 @@ struct Schedule {
     const Lvl& L = h->L[l];
     return h->pset1 && h->fused && h->d.alpha == 1 && !cx(l) && !L.st27 && L.nlg == 0.0 &&
            b.global && tma_rhs_ok(b) &&
-           (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
-                         L.E[1] >= h->fused_min_e)) &&
+           (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
            srfmg::pset1_fused_ok<T>(L, h->L[l - 1], 1);
   }
   void pset1(int l, const View<T>& b) {
@@ -839,87 +847,8 @@ struct Schedule {
     exchange(2, base, sy, sz, h->blkT_lo);
   }
 
-  // ---- fused multi-stage passes (pass.cu) on SR levels
-  bool pass_on(int l, int src, int nstep, int sink, const View<T>& b) {
-    if (!h->pass || l <= h->T || l < 1 || h->L[l].st27 || h->L[l].nlg != 0.0) return false;
-    if (h->d.alpha != 1 || h->d.nu1 != 2 || h->d.nu2 != 2) return false;
-    const Lvl& L = h->L[l];
-    if (!h->force && (long long)L.nsegs * ((L.E[1] + 13) / 14) < 148) return false;
-    if (!tma_rhs_ok(b)) return false;
-    return srfmg::pass_ok<T>(src, nstep, sink, L, h->L[l - 1], b.global);
-  }
-  // run one pass: steps = the Chebyshev steps of the chain (R8), u ping-pongs on level l
-  void run_pass(int l, int src, int nstep, int sink, const View<T>& b) {
-    const Lvl& L = h->L[l];
-    LevelBufs& bb = h->B[l];
-    srfmg::PassSpec<T> ps{};
-    ps.src = src;
-    ps.nstep = nstep;
-    ps.sink = sink;
-    ps.L = L;
-    ps.Lc = h->L[l - 1];
-    ps.uin = (const T*)bb.u[bb.cur];
-    ps.uout = (T*)bb.u[1 - bb.cur];
-    ps.rhs = frhs(b);
-    ps.w = U(l - 1);
-    ps.t = (const T*)h->B[l - 1].t;
-    // PSET + RESTRICT reads the coarse u (Pi) while restricting: restrict into t and
-    // merge afterwards (the coarse t is rewritten by the tau step that follows anyway)
-    const bool merge = src == srfmg::kSrcPset && sink == srfmg::kSinkRestrict;
-    ps.uc = merge ? (T*)h->B[l - 1].t : U(l - 1);
-    ps.rc = (T*)h->B[l - 1].rhs;
-    ps.jr = jr_for(l);
-    const double c0 = 1.0 / h->theta[l];
-    const double rho0 = 1.0 / h->sigma[l];
-    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
-    for (int i = 0; i < nstep; ++i) ps.cr[i] = c0;  // degree-1 steps / first step of degree 2
-    if (nstep >= 2) {                               // second step of the degree-2 polynomial
-      ps.cr[nstep - 1] = 2.0 * rho1 / h->delta[l];
-      ps.cm[nstep - 1] = rho1 * rho0;
-    }
-    const CellCounts& c = h->cells[l];
-    const double cgc = (double)c.cg / 8.0;  // coarse footprint (about 1/8 of C ∪ GSR)
-    double words = 0;
-    int cls = KC_PASS_ENTRY;
-    if (src == srfmg::kSrcPset) words = cgc + c.compute + c.cg;
-    if (src == srfmg::kSrcLoad) { words = 2.0 * c.cg + c.compute; cls = KC_PASS_DOWN; }
-    if (src == srfmg::kSrcPadd) { words = 2.0 * cgc + c.cg + c.compute; cls = KC_PASS_UP; }
-    if (sink == srfmg::kSinkRestrict) words += c.compute / 4.0;
-    if (nstep == 0) {  // plain residual + restriction: reads u over C and b, writes coarse
-      words = c.compute * (2.0 + 0.25);
-      cls = KC_RESTRICT;
-    }
-    if (sink == srfmg::kSinkFinal) {
-      ps.fin.p = final_out;
-      for (int i = 0; i < 3; ++i) ps.fin.bo[i] = h->blk_lo[i];
-      ps.fin.sy = h->blk_n[0];
-      ps.fin.sz = (long long)h->blk_n[0] * h->blk_n[1];
-      words += (double)h->blk_n[0] * h->blk_n[1] * h->blk_n[2];
-    } else if (nstep > 0) {
-      words += c.cg;
-    }
-    {
-      Launch g(h, st, cls, l, w * words);
-      srfmg::launch_pass<T>(ps, st);
-    }
-    if (merge) {
-      Launch g(h, st, KC_TAU, l - 1, w * 2.0 * c.compute / 8.0);
-      srfmg::launch_merge_f<T>(L, h->L[l - 1], (const T*)h->B[l - 1].t, U(l - 1), ps.jr, st);
-    }
-    if (sink == srfmg::kSinkFinal) final_done = true;
-    else if (nstep > 0) bb.cur = 1 - bb.cur;  // (no steps: u unchanged, not written)
-  }
-
   void restrict_std(int l, View<T> b) {
     const int jr = jr_for(l);
-    if (h->fused && h->pass_restrict && l > h->T && !h->L[l].st27 && h->L[l].nlg == 0.0 &&
-        tma_rhs_ok(b) &&
-        (h->force || (long long)h->L[l].nsegs * ((h->L[l].E[1] + 13) / 14) >= 148) &&
-        srfmg::pass_ok<T>(srfmg::kSrcLoad, 0, srfmg::kSinkRestrict, h->L[l], h->L[l - 1],
-                          b.global)) {
-      run_pass(l, srfmg::kSrcLoad, 0, srfmg::kSinkRestrict, b);  // TMA-fed residual+restrict
-      return;
-    }
     if (cx(l) && cx(l - 1)) {
       srfmg::COp<T> o = cop(srfmg::kCopRestrict, l, l - 1);
       o.a = U(l);
@@ -941,7 +870,7 @@ struct Schedule {
     // writes rhs while neighbouring bands still read R)
     T* rc = tau_fuse_ok(l - 1) ? (T*)h->B[l - 1].rres : (T*)h->B[l - 1].rhs;
     if (L.st27 && L.nlg == 0.0 && h->fused && tma_rhs_ok(b) && srfmg::cheb27_fused_ok<T>(L) &&
-        (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148)) {
+        fills(L, 10)) {
       // 27-point: TMA-fed residual pass into the free ping-pong buffer, then the averages
       T* scratch = (T*)h->B[l].u[1 - h->B[l].cur];
       // f-visit: R = f_{l-1} - avg8(A u) from the R6 pyramid, f_l not streamed
@@ -955,40 +884,6 @@ struct Schedule {
     srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), rc, jr, st,
                               (T*)h->B[l].u[1 - h->B[l].cur],
                               use_pyr ? fview(l - 1) : View<T>{});  // L113-115 / L233, L235
-  }
-
-  // correction + degree-2 post-smoothing in one pass (up.cu), on the levels the fused
-  // Chebyshev pass takes
-  bool up_on(int l, const View<T>& b) const {
-    const Lvl& L = h->L[l];
-    return h->up_fuse && h->fused && !h->pass && !cx(l) && h->d.nu2 == 2 && !L.st27 &&
-           L.nlg == 0.0 && tma_rhs_ok(b) &&
-           (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
-                         L.E[1] >= h->fused_min_e)) &&
-           srfmg::up2_fused_ok<T>(L, h->L[l - 1]);
-  }
-  void up2(int l, const View<T>& b, bool last) {
-    const Lvl& L = h->L[l];
-    LevelBufs& bb = h->B[l];
-    const CellCounts& c = h->cells[l];
-    const double rho0 = 1.0 / h->sigma[l];
-    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
-    const bool fin = last && final_out != nullptr;
-    srfmg::FinalOut<T> fo{};
-    const double nv = (double)h->blk_n[0] * h->blk_n[1] * h->blk_n[2];
-    if (fin) {
-      fo.p = final_out;
-      for (int i = 0; i < 3; ++i) fo.bo[i] = h->blk_lo[i];
-      fo.sy = h->blk_n[0];
-      fo.sz = (long long)h->blk_n[0] * h->blk_n[1];
-    }
-    // algorithmic words: u read (C u GSR), rhs (C), w and t (1/8 each), u or user u written
-    Launch g(h, st, KC_PASS_UP, l, w * (c.cg + c.compute + c.cg / 4.0 + (fin ? nv : c.cg)));
-    srfmg::launch_up2_fused<T>(L, h->L[l - 1], (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
-                               U(l - 1), (const T*)h->B[l - 1].t, frhs(b), 1.0 / h->theta[l],
-                               rho1 * rho0, 2.0 * rho1 / h->delta[l], st, fo);
-    bb.cur = 1 - bb.cur;
-    if (fin) final_done = true;
   }
 
   void tau_from_rres(int lc, int jr) {  // the separate tau on R parked in rres
@@ -1007,14 +902,13 @@ struct Schedule {
   // as the fused degree-2 pre-smoothing with the segment-storage rhs
   bool tau_fuse_ok(int lc) const {
     const Lvl& L = h->L[lc];
-    const bool base = h->tau_fuse && h->B[lc].rres && lc > h->T && h->fused && !h->pass &&
-                      !h->pass_restrict && h->d.nu1 == 2 && L.nlg == 0.0;
+    const bool base = h->tau_fuse && h->B[lc].rres && lc > h->T && h->fused &&
+                      h->d.nu1 == 2 && L.nlg == 0.0;
     if (L.st27)  // the 27-point pass (fused27.cu) under the conditions cheb() uses
-      return base && (h->force || (long long)L.nsegs * ((L.E[1] + 9) / 10) >= 148) &&
+      return base && fills(L, 10) &&
              srfmg::cheb27_fused_ok<T>(L);
     return base &&
-           (h->force || ((long long)L.nsegs * ((L.E[1] + 39) / 40) >= 148 &&
-                         L.E[1] >= h->fused_min_e)) &&
+           (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
            srfmg::cheb2_fused_ok<T>(L) && srfmg::cheb_spec_ok<T>(L);
   }
 
@@ -1026,34 +920,16 @@ struct Schedule {
       coarsest(b);
       return;
     }
-    using namespace srfmg;
-    bool restricted = false;
     if (entry) {
-      if (h->pass_entry == 4 && pass_on(l, kSrcPset, 3, kSinkRestrict, b)) {
-        // (the merge into u_{l-1} precedes the level-T exchange below)
-        run_pass(l, kSrcPset, 3, kSinkRestrict, b);  // Pi, S^1, S^2, r, restrict
-        restricted = true;
-      } else if (h->pass_entry == 3 && pass_on(l, kSrcPset, 3, kSinkStore, b)) {
-        run_pass(l, kSrcPset, 3, kSinkStore, b);  // Pi, S^1, S^2
-        restrict_std(l, b);
-        restricted = true;
-      } else if (h->pass_entry == 1 && pass_on(l, kSrcPset, 1, kSinkStore, b)) {
-        run_pass(l, kSrcPset, 1, kSinkStore, b);  // Pi, S^1
-      } else if (pset1_on(l, b)) {
+      if (pset1_on(l, b)) {
         pset1(l, b);                 // Pi onto C ∪ GSR and S^1, one pass
       } else {
         prolong(l, 0);               // Pi onto C ∪ GSR
         cheb(l, h->d.alpha, b);      // S^alpha
       }
     }
-    if (!restricted) {
-      if (h->pass_down && pass_on(l, kSrcLoad, 2, kSinkRestrict, b)) {
-        run_pass(l, kSrcLoad, 2, kSinkRestrict, b);  // L112-115 / L232-235 in one pass
-      } else {
-        cheb(l, h->d.nu1, b);  // L112 / L232
-        restrict_std(l, b);
-      }
-    }
+    cheb(l, h->d.nu1, b);  // L112 / L232
+    restrict_std(l, b);
     const int jr = jr_for(l);
     if (h->world > 1 && l - 1 == h->T) exchange_uT();  // a8: level-T hand-off (R16)
     if (cx(l - 1)) {  // conventional level: F = V = Omega (jr = 0)
@@ -1069,17 +945,8 @@ struct Schedule {
       tau_std(l - 1, jr);  // L116-117 / L234-236
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
-    const bool last = l == h->M && final_out != nullptr;
-    if (h->pass_up && last && pass_on(l, kSrcPadd, 2, kSinkFinal, b)) {
-      run_pass(l, kSrcPadd, 2, kSinkFinal, b);  // L241-242, genuine cells -> user u (R19)
-    } else if (h->pass_up && !last && pass_on(l, kSrcPadd, 2, kSinkStore, b)) {
-      run_pass(l, kSrcPadd, 2, kSinkStore, b);  // L241-242 in one pass
-    } else if (up_on(l, b)) {
-      up2(l, b, last);  // L241-242 in one pass (at l = M: the solve's last pass)
-    } else {
-      prolong(l, 1);                    // L118 / L241
-      cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
-    }
+    prolong(l, 1);                    // L118 / L241
+    cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
   }
 
   void run(T* uout) {
@@ -1371,25 +1238,12 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->fused = !(fu && fu[0] == '0');
   const char* ff = std::getenv("SR_FMG_FORCE_FUSED");
   h->force = ff && ff[0] == '1';
-  // fused passes: opt-in until they beat the separate kernels.  SR_FMG_PASS=1|3|4 turns on
-  // all three kinds with that entry chain; SR_FMG_PASS_{ENTRY,DOWN,UP} override per kind
   if (const char* e = std::getenv("SR_FMG_FUSED_MIN_E")) h->fused_min_e = std::atoi(e);
   const char* ce = std::getenv("SR_FMG_CEXEC");
   h->cexec = !(ce && ce[0] == '0');
-  const char* fp = std::getenv("SR_FMG_PASS");
-  const bool all = fp && (fp[0] == '1' || fp[0] == '3' || fp[0] == '4');
-  h->pass_entry = all ? fp[0] - '0' : 0;
-  h->pass_down = all;
-  h->pass_up = all;
-  if (const char* e = std::getenv("SR_FMG_PASS_ENTRY")) h->pass_entry = std::atoi(e);
-  if (const char* e = std::getenv("SR_FMG_PASS_DOWN")) h->pass_down = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SR_FMG_PASS_UP")) h->pass_up = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SR_FMG_PASS_RESTRICT")) h->pass_restrict = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_TAU_FUSE")) h->tau_fuse = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SR_FMG_UP_FUSE")) h->up_fuse = std::atoi(e) != 0;
-  h->pass = h->fused && (h->pass_entry || h->pass_down || h->pass_up);
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {
@@ -1645,7 +1499,11 @@ sr_status_t sr_fmg_solve_host(sr_fmg_t* h, const void* f_host, void* u_host) {
 
 void sr_fmg_destroy(sr_fmg_t* h) {
   if (!h) return;
+  // every stream of the handle: a copy of the host pipeline may still read a staging slot,
+  // which an allocator hook could hand out again as soon as it is freed
   cudaStreamSynchronize(h->stream);
+  if (h->s_h2d) cudaStreamSynchronize(h->s_h2d);
+  if (h->s_d2h) cudaStreamSynchronize(h->s_d2h);
   free_all(h);
   delete h;
 }

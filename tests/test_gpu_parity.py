@@ -363,37 +363,6 @@ def test_fused_and_step_kernels_agree(dtype, force, monkeypatch):
     assert rel_l2(a, b) <= (1e-13 if dtype == "f64" else 1e-5)
 
 
-# ---- fused multi-stage SR passes (pass.cu): every FMG-entry variant, forced onto levels
-# that are too small to fill the GPU, against the oracle and against the unfused schedule
-PASS_CASES = [
-    # (name, n, M, seg, J, K, rhs): E = S_l + 2J + 2 in {70, 38} on the SR levels
-    ("K2-S64", (128, 128, 128), 6, 64, 2, 2, "manufactured+noise"),
-    ("K1-S64", (128, 128, 128), 6, 64, 2, 1, "bumps"),
-    ("K3-S64", (128, 128, 128), 6, 64, 2, 3, "manufactured+noise"),
-    ("noncubic-S64", (128, 64, 64), 5, 64, 2, 2, "random"),
-]
-
-
-@pytest.mark.parametrize("cl", ["1", "0"], ids=["cluster", "recompute"])
-@pytest.mark.parametrize("mode", ["0", "1", "3", "4"])
-@pytest.mark.parametrize("case", PASS_CASES, ids=[c[0] for c in PASS_CASES])
-def test_fused_passes_match_oracle(case, mode, cl, monkeypatch):
-    # cl: bands of a segment as one thread-block cluster exchanging halo rows through DSMEM,
-    # or independent bands that recompute their halo rows
-    name, n, M, seg, J, K, rhs = case
-    f = W.make_rhs(rhs, n)
-    ref = _oracle(rhs, f, n, M, seg, J, K)
-    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
-    monkeypatch.setenv("SR_FMG_PASS_CL", cl)
-    monkeypatch.setenv("SR_FMG_PASS", mode)
-    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
-    assert rel_l2(u, ref) <= TOL64, (name, mode, rel_l2(u, ref))
-    monkeypatch.setenv("SR_FMG_PASS", "0")
-    monkeypatch.setenv("SR_FMG_FUSED", "0")
-    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
-    assert rel_l2(u, b) <= 1e-13, (name, mode, rel_l2(u, b))
-
-
 # FMG entry Pi + S^1 in one TMA pass (pset.cu) vs prolongation + degree-1 step: the buffer
 # widths J = 0..3 give every residue of the storage origin mod 4 (fine row pairs vs coarse
 # rows in y, fine plane pairs vs coarse planes in z)
@@ -417,24 +386,6 @@ def test_fused_fmg_entry_matches_oracle(case, dtype, monkeypatch):
     monkeypatch.setenv("SR_FMG_PSET1", "1")
     u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
     monkeypatch.setenv("SR_FMG_PSET1", "0")
-    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
-    assert rel_l2(u, b) <= (1e-13 if dtype == "f64" else 1e-5), (name, rel_l2(u, b))
-    if dtype == "f64":
-        ref = _oracle(rhs, f, n, M, seg, J, K)
-        assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
-
-
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("case", PSET_CASES, ids=[c[0] for c in PSET_CASES])
-def test_up_pass_correction_and_smoothing(case, dtype, monkeypatch):
-    # u += P(w - t) and the degree-2 post-smoothing in one pass (up.cu) vs the correction
-    # kernel followed by the fused Chebyshev pass: equal up to rounding; oracle parity
-    name, n, M, seg, J, K, rhs = case
-    f = W.make_rhs(rhs, n)
-    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
-    monkeypatch.setenv("SR_FMG_UP_FUSE", "1")
-    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
-    monkeypatch.setenv("SR_FMG_UP_FUSE", "0")
     b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
     assert rel_l2(u, b) <= (1e-13 if dtype == "f64" else 1e-5), (name, rel_l2(u, b))
     if dtype == "f64":
@@ -475,48 +426,6 @@ def test_restriction_via_pyramid(case, dtype, monkeypatch):
     if dtype == "f64":
         ref = _oracle(rhs, f, n, M, seg, J, K)
         assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
-
-
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_restriction_pass_matches_oracle(dtype, monkeypatch):
-    # the TMA-fed residual + restriction pass (pass.cu with no Chebyshev steps) on the E = 70
-    # and E = 38 boxes, forced onto these small levels
-    n, M, seg, J, K, rhs = (128, 128, 128), 6, 64, 2, 3, "manufactured+noise"
-    f = W.make_rhs(rhs, n)
-    ref = _oracle(rhs, f, n, M, seg, J, K)
-    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
-    monkeypatch.setenv("SR_FMG_PASS_RESTRICT", "1")
-    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
-    assert rel_l2(u, ref) <= (TOL64 if dtype == "f64" else TOL32), rel_l2(u, ref)
-
-
-@pytest.mark.parametrize("mode", ["1", "4"])
-def test_fused_passes_fp32(mode, monkeypatch):
-    n, M, seg, J, K, rhs = (128, 128, 128), 6, 64, 2, 2, "manufactured+noise"
-    f = W.make_rhs(rhs, n)
-    ref = _oracle(rhs, f, n, M, seg, J, K)
-    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
-    monkeypatch.setenv("SR_FMG_PASS", mode)
-    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype="f32")
-    assert rel_l2(u, ref) <= TOL32, rel_l2(u, ref)
-
-
-def test_fused_pass_launch_count(monkeypatch):
-    # C2-like level plan with passes on both SR levels: per SR level the FMG entry is one
-    # launch and every later visit two (down, up) instead of 2 + 2 + 2 (+prolong)
-    n = (128, 128, 128)
-    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
-    monkeypatch.setenv("SR_FMG_PASS", "4")
-    with Solver(n, 6, seg=64, buffer=2, K=2) as s:
-        s.solve(torch.from_numpy(W.make_rhs("manufactured", n)).cuda())
-        fused = s.launches_per_solve
-    monkeypatch.setenv("SR_FMG_PASS", "0")
-    for k in ("SR_FMG_UP_FUSE", "SR_FMG_TAU_FUSE", "SR_FMG_PSET1"):  # the unfused schedule
-        monkeypatch.setenv(k, "0")
-    with Solver(n, 6, seg=64, buffer=2, K=2) as s:
-        s.solve(torch.from_numpy(W.make_rhs("manufactured", n)).cuda())
-        unfused = s.launches_per_solve
-    assert fused < unfused, (fused, unfused)
 
 
 def test_host_async_pipeline_matches_device_solves():
@@ -584,8 +493,7 @@ def test_c4_two_ranks_full_size_equal_single_gpu():
     for r, s in enumerate(ranks):
         lo, nb = s.block_lo, s.block_n
         blk = single[lo[2]:lo[2] + nb[2], lo[1]:lo[1] + nb[1], lo[0]:lo[0] + nb[0]]
-        d = float(torch.linalg.vector_norm(outs[r] - blk) / torch.linalg.vector_norm(blk))
-        assert d <= 1e-13, (r, d)
+        assert torch.equal(outs[r], blk), r      # bitwise (R25)
     for s in ranks:
         s.close()
 

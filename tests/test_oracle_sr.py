@@ -1,4 +1,4 @@
-"""Pins of the oracle's segmental refinement (fig:fmgsr / fig:mgvsr).
+r"""Pins of the oracle's segmental refinement (fig:fmgsr / fig:mgvsr).
 
 What fixes SR independently of the oracle's own arithmetic:
   * the region definitions of PAPER.md:187-214, evaluated by brute force on cell sets;
