@@ -46,7 +46,7 @@ ORACLE_SAMPLE = dict(n=(128, 128, 128), M=6, seg=16, buffer=2, K=4, rhs="manufac
 PGRID = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 # kernel classes (sr_fmg_kernel_name) that can dominate the finest level: the roofline line
 # reports the one with the largest device time per solve
-KC_CANDIDATES = (1, 3, 7, 8, 9, 10)  # k_restrict, k_prolong, k_cheb2, k_pass_entry/down/up
+KC_CANDIDATES = (1, 3, 7, 8)  # k_restrict, k_prolong, k_cheb2, k_pass_entry (Pi + S^1)
 
 
 def parse():
@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--stencil", default="7pt", choices=["7pt", "27pt"],
                     help="27pt: the paper's operator (SURVEY f1; unfused kernels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
     return ap.parse_args()
 
 
@@ -137,6 +138,68 @@ def sample_desc():
     return (f"oracle (numpy fp64) FMG+SR solve of {s['n'][0]}^3 cells, M={s['M']}, "
             f"seg={s['seg']} (8^3 segments), buffer={s['buffer']}, K={s['K']}, "
             f"{s['rhs']} rhs: the C3 segment grid/K/J at 1/64 of the cells")
+
+
+def mem_available_gb():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) / 1e6
+    except Exception:
+        pass
+    return 0.0
+
+
+def oracle_full_solve(n, M, seg, buf, K, rhs, h):
+    """The oracle, as it stands, on the bench workload itself: one solve of
+    the same f on the host; returns (seconds, cells, cores used = CPU time / wall time)."""
+    import resource
+
+    import oracle as O
+    f = W.make_rhs(rhs, n, h=h)
+    cfg = O.Config(n=n, M=M, seg=seg, buffer=buf, K=K, h=h)
+    r0 = resource.getrusage(resource.RUSAGE_SELF)
+    t0 = time.perf_counter()
+    O.solve(f, cfg)
+    t = time.perf_counter() - t0
+    r1 = resource.getrusage(resource.RUSAGE_SELF)
+    cpu = (r1.ru_utime - r0.ru_utime) + (r1.ru_stime - r0.ru_stime)
+    return t, float(np.prod(n)), max(1, round(cpu / t))
+
+
+def accuracy(solver_args, n, M, seg, buf, K, h, dtype, f_bench, u_bench):
+    """Accuracy of the measured configuration (north_star: the GPU must match the error-to-
+    discretisation-error ratios; PAPER.md:262-264 defines e_r = ||e_SR||_inf/||e_FMG||_inf).
+    * the manufactured f alone (no noise): e_SR = ||u_SR - u||_inf and e_FMG (K = 0) against the
+      exact u, e_disc = ||u_h* - u||_inf with u_h* = A^-1 f by DST (tests/pins.py), e_r;
+    * the bench's own f: the algebraic error ||u - u_h*||_inf against u_h* of that f."""
+    import torch
+
+    from paper_1406_7808_b200 import Solver
+    from tests import pins
+    npd = np.float64 if dtype == "f64" else np.float32
+    fm = W.manufactured_f(n, h)
+    ue = W.manufactured_u(n, h)
+    out = {"rhs": "manufactured f (no noise) for e_r; the bench f for e_alg",
+           "norm": "max norm over the fine grid"}
+    ft = torch.from_numpy(fm.astype(npd)).cuda()
+    u_sr = solver_args["solver"].solve(ft).double().cpu().numpy()
+    with Solver(n, M, seg=seg, buffer=buf, K=0, dtype=dtype, h=h) as s0:
+        u_fmg = s0.solve(ft).double().cpu().numpy()
+    del ft
+    ustar = pins.dst_solve(fm, h)
+    e_sr = float(np.abs(u_sr - ue).max())
+    e_fmg = float(np.abs(u_fmg - ue).max())
+    e_disc = float(np.abs(ustar - ue).max())
+    out.update({"e_sr_inf": e_sr, "e_fmg_inf": e_fmg, "e_disc_inf": e_disc,
+                "e_r": e_sr / e_fmg,
+                "e_sr_alg_over_disc": float(np.abs(u_sr - ustar).max()) / e_disc,
+                "e_fmg_alg_over_disc": float(np.abs(u_fmg - ustar).max()) / e_disc})
+    if f_bench is not None:
+        ub = pins.dst_solve(np.asarray(f_bench, dtype=np.float64), h)
+        out["bench_f_e_alg_inf"] = float(np.abs(np.asarray(u_bench, np.float64) - ub).max())
+        out["bench_f_e_alg_rel_l2"] = float(np.linalg.norm(u_bench - ub) / np.linalg.norm(ub))
+    return out
 
 
 def run_reference(args):
@@ -331,11 +394,28 @@ def main():
         "solve_roofline_frac": (solver.alg_bytes_per_solve / (ms / 1e3)) / (peak * 1e9),
         "clocks": clk,
     }
+    if rank == 0 and world == 1 and args.stencil == "7pt" and max(n) <= 512 and not args.no_accuracy:
+        try:
+            line["accuracy"] = accuracy({"solver": solver}, n, M, seg, buf, K, h, args.dtype,
+                                        f_host, u.double().cpu().numpy())
+        except Exception as e:  # reported, never fatal for the bench line
+            line["accuracy"] = {"error": repr(e)[:200]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t1, c1 = oracle_sample_solve()
-        t2, c2 = oracle_sample_solve()
-        line["cpu_baseline"] = {"value": (c1 + c2) / (t1 + t2), "unit": "cells/s", "cores": 1,
-                                "kind": "oracle", "sample": sample_desc() + " (2 solves)"}
+        cpus = len(os.sched_getaffinity(0))
+        if config == "C3" and args.stencil == "7pt" and mem_available_gb() >= 24:
+            # the oracle on the bench workload itself: one full-size 512^3 C3 solve (~75 s)
+            t1, c1, used = oracle_full_solve(n, M, seg, buf, K, rhs, h)
+            line["cpu_baseline"] = {
+                "value": c1 / t1, "unit": "cells/s", "cores": used, "kind": "oracle",
+                "host_cpus": cpus, "seconds": t1,
+                "sample": f"the full C3 workload: one oracle (numpy fp64) solve of the same "
+                          f"512^3 manufactured+noise f, M=8, seg=64, buffer=2, K=4"}
+        else:
+            t1, c1 = oracle_sample_solve()
+            t2, c2 = oracle_sample_solve()
+            line["cpu_baseline"] = {"value": (c1 + c2) / (t1 + t2), "unit": "cells/s",
+                                    "cores": 1, "kind": "oracle", "host_cpus": cpus,
+                                    "sample": sample_desc() + " (2 solves)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     solver.close()

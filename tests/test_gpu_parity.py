@@ -344,6 +344,12 @@ def test_full_size_c3_matches_oracle():
         s.solve(ft)
         u = s.solve(ft).cpu().numpy()
     assert rel_l2(u, ref) <= TOL64, rel_l2(u, ref)
+    # fp32 (C3's second dtype) against the same fp64 oracle solve (R20, R23: <= 1e-4)
+    with Solver(n, 8, seg=64, buffer=2, K=4, dtype="f32") as s:
+        ft = torch.from_numpy(f.astype(np.float32)).cuda()
+        s.solve(ft)
+        u32 = s.solve(ft).double().cpu().numpy()
+    assert rel_l2(u32, ref) <= TOL32, rel_l2(u32, ref)
 
 
 @pytest.mark.parametrize("force", ["0", "1"])
