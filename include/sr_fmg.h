@@ -84,7 +84,7 @@ typedef struct {
   int32_t device;     /* CUDA device ordinal; -1 = current device                        */
   void *stream;       /* cudaStream_t; NULL = legacy default stream                      */
   int32_t use_graph;  /* 1 (default): capture a solve into a CUDA graph and replay it    */
-  int32_t comm;       /* world > 1: 0 = NCCL (default), 1 = test replay store (see below) */
+  int32_t comm;       /* world > 1: 0 = NCCL (default), 1 = test host store (see below)   */
   int32_t stencil;    /* 7 (default): 7-point FD, A = -Lap_h (BASELINE); 27: the paper's    */
                       /*   27-point operator (weights centre 8/3, edges     */
                       /*   -1/6, corners -1/12, faces 0, /h^2), lambda_max = 4/h^2; runs  */
@@ -99,6 +99,13 @@ typedef struct {
   void *(*alloc)(size_t bytes, void *ctx);
   void (*free)(void *p, void *ctx);
   void *alloc_ctx;
+  /* world > 1: the conventional levels l <= T stay domain-decomposed (each rank holds its  */
+  /* block, a halo exchange of grouped ncclSend/ncclRecv before every operator application, */
+  /* PAPER.md:157-168) while every dimension of the rank's block has at least dd_min cells; */
+  /* the first level below is all-gathered once per visit and it and the coarser levels    */
+  /* are solved redundantly on every rank.  0 = default (32); a value    */
+  /* larger than the level-T block agglomerates at T (no decomposed coarse levels).         */
+  int32_t dd_min;
 } sr_fmg_desc_t;
 
 typedef struct {
@@ -120,15 +127,22 @@ typedef struct {
   int64_t block_lo[3], block_n[3];         /* fine cells owned (output block of u)        */
   int32_t f_halo;                          /* halo width of the local f block             */
   int64_t f_dims[3];                       /* local f array dims = block_n + 2 f_halo     */
-  int64_t exchanges_per_solve;             /* collective (all-gather) calls per solve     */
+  int64_t exchanges_per_solve;             /* collective calls of the last solve (all-    */
+                                           /* gathers + halo phases; 0 before a solve)    */
+  int32_t level_A;                         /* levels <= A gathered / redundant; levels    */
+                                           /* A < l <= T decomposed (A = T: none)         */
+  int32_t dd[SR_FMG_MAX_LEVELS];           /* 1 if level l is domain-decomposed           */
+  int64_t comm_calls[SR_FMG_MAX_LEVELS];   /* collective calls (NCCL groups / all-gathers) */
+                                           /* per level in the last solve: 0 on SR levels */
 } sr_fmg_info_t;
 
 /* Multi-GPU partition of a descriptor (pure host arithmetic, no GPU needed).  The
  * segment grid (n_d/seg per dimension) is split into pgrid blocks; rank r has block
  * coordinates (r % P1, (r / P1) % P2, r / (P1 P2)).  Each rank solves the SR levels of its
- * own segments with no communication; the transition level and below are
- * solved redundantly on every rank (the paper's "redundant coarse grid")
- * after one all-gather of the level-T blocks per SR V-cycle. */
+ * own segments with no communication.  The conventional levels A < l <= T
+ * are domain-decomposed: rank r owns block (its fine block) / 2^(M-l) of Omega_l and
+ * exchanges halos with its face neighbours; the levels <= A are
+ * all-gathered and solved redundantly on every rank. */
 typedef struct {
   int32_t world, rank, coord[3];
   int32_t segs_per_rank[3];          /* SR segments per dimension owned by this rank     */
@@ -136,6 +150,7 @@ typedef struct {
   int32_t f_halo;                    /* f must be given on [lo - halo, lo + n + halo)     */
   int64_t f_dims[3];                 /* = block_n + 2 f_halo (x1 fastest)                 */
   int64_t level_T_lo[3], level_T_n[3]; /* this rank's block of the transition level T     */
+  int32_t level_A;                   /* levels A < l <= T decomposed, l <= A redundant      */
 } sr_fmg_partition_t;
 
 /* Fill *d with defaults: cube 0, M 0, seg 0, buffer 2, K 0, sched (-1,-1), fp64,
@@ -221,14 +236,15 @@ sr_status_t sr_fmg_debug_level_io(sr_fmg_t *h, int32_t level, int32_t field, int
 sr_status_t sr_fmg_debug_op(sr_fmg_t *h, int32_t op, int32_t level, int32_t deg,
                             const void *f_dev);
 
-/* Test-only comm backend (desc.comm = 1): instead of NCCL, every all-gather records this
- * rank's block into a host-side store shared by the handles of all ranks in one process
- * and fills the other ranks' blocks from it.  Running every rank's solve repeatedly
- * (exchanges_per_solve + 1 rounds) reproduces the distributed solve on ONE GPU, so the
- * rank-local logic is validated without NCCL.  Forces eager (non-graph) execution. */
-void *sr_fmg_replay_store_create(int32_t world);
-void sr_fmg_replay_store_destroy(void *store);
-sr_status_t sr_fmg_set_replay(sr_fmg_t *h, void *store);
+/* Test-only comm backend (desc.comm = 1): instead of NCCL, the handles of all ranks live in
+ * one process, one host thread each (all on one GPU), and pass every all-gather block and
+ * halo slab through a host-side store (device -> host copy, mailbox, host -> device copy;
+ * a receive blocks until the sending rank has posted, at most 30 s, then SR_ERR_NCCL).
+ * The rank threads must call sr_fmg_solve concurrently.  No kernel waits for another rank.
+ * Forces eager (non-graph) execution. */
+void *sr_fmg_host_store_create(int32_t world);
+void sr_fmg_host_store_destroy(void *store);
+sr_status_t sr_fmg_set_host_store(sr_fmg_t *h, void *store);
 
 /* Profiling hooks used by bench.py: select one kernel class (index into
  * sr_fmg_kernel_name) at one level; later solves record a CUDA event pair around every

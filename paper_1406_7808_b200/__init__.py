@@ -6,7 +6,7 @@ The product is the C-ABI shared library `libsrfmg.so` (include/sr_fmg.h) built f
 library has not been built -- there is no CPU fallback.
 """
 from ._lib import LIB_PATH, SrError, kernel_names  # noqa: F401  (raises if .so missing)
-from .api import LevelInfo, ReplayStore, Solver, nccl_unique_id, partition  # noqa: F401
+from .api import HostStore, LevelInfo, Solver, nccl_unique_id, partition  # noqa: F401
 
 __all__ = ["Solver", "LevelInfo", "SrError", "kernel_names", "LIB_PATH", "partition",
-           "nccl_unique_id", "ReplayStore"]
+           "nccl_unique_id", "HostStore"]

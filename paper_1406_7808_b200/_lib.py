@@ -24,8 +24,8 @@ EXPORTED = [
     "sr_fmg_solve_host", "sr_fmg_set_stream", "sr_fmg_destroy", "sr_fmg_get_info",
     "sr_fmg_last_error", "sr_fmg_kernel_count", "sr_fmg_kernel_name",
     "sr_fmg_debug_level_io", "sr_fmg_debug_op", "sr_fmg_profile_select", "sr_fmg_profile_read",
-    "sr_fmg_partition", "sr_fmg_nccl_unique_id", "sr_fmg_replay_store_create",
-    "sr_fmg_replay_store_destroy", "sr_fmg_set_replay", "sr_fmg_solve_host_async",
+    "sr_fmg_partition", "sr_fmg_nccl_unique_id", "sr_fmg_host_store_create",
+    "sr_fmg_host_store_destroy", "sr_fmg_set_host_store", "sr_fmg_solve_host_async",
     "sr_fmg_synchronize", "sr_fmg_vsolve", "sr_fmg_desc_size",
 ]
 
@@ -48,6 +48,7 @@ class Desc(ctypes.Structure):
         ("use_graph", ctypes.c_int32), ("comm", ctypes.c_int32), ("stencil", ctypes.c_int32),
         ("nl_gamma", ctypes.c_double),
         ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
+        ("dd_min", ctypes.c_int32),
     ]
 
 
@@ -71,6 +72,9 @@ class Info(ctypes.Structure):
         ("block_lo", ctypes.c_int64 * 3), ("block_n", ctypes.c_int64 * 3),
         ("f_halo", ctypes.c_int32), ("f_dims", ctypes.c_int64 * 3),
         ("exchanges_per_solve", ctypes.c_int64),
+        ("level_A", ctypes.c_int32),
+        ("dd", ctypes.c_int32 * MAX_LEVELS),
+        ("comm_calls", ctypes.c_int64 * MAX_LEVELS),
     ]
 
 
@@ -81,6 +85,7 @@ class Partition(ctypes.Structure):
         ("block_lo", ctypes.c_int64 * 3), ("block_n", ctypes.c_int64 * 3),
         ("f_halo", ctypes.c_int32), ("f_dims", ctypes.c_int64 * 3),
         ("level_T_lo", ctypes.c_int64 * 3), ("level_T_n", ctypes.c_int64 * 3),
+        ("level_A", ctypes.c_int32),
     ]
 
 
@@ -114,9 +119,9 @@ def _load():
                                       ctypes.POINTER(I32)]),
         "sr_fmg_partition": (I32, [ctypes.POINTER(Desc), ctypes.POINTER(Partition)]),
         "sr_fmg_nccl_unique_id": (I32, [P]),
-        "sr_fmg_replay_store_create": (P, [I32]),
-        "sr_fmg_replay_store_destroy": (None, [P]),
-        "sr_fmg_set_replay": (I32, [P, P]),
+        "sr_fmg_host_store_create": (P, [I32]),
+        "sr_fmg_host_store_destroy": (None, [P]),
+        "sr_fmg_set_host_store": (I32, [P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -31,7 +31,7 @@ class LevelInfo:
 
 def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha=1, nu1=2,
               nu2=2, cheb=None, device=None, use_graph=True, world=1, rank=0,
-              pgrid=(1, 1, 1), stencil="7pt", nl_gamma=0.0) -> Desc:
+              pgrid=(1, 1, 1), stencil="7pt", nl_gamma=0.0, dd_min=0) -> Desc:
     if isinstance(n, int):
         n = (n, n, n)
     d = Desc()
@@ -55,18 +55,21 @@ def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha
     d.device = -1 if device is None else int(device)
     d.use_graph = 1 if use_graph else 0
     d.world, d.rank = int(world), int(rank)
+    d.dd_min = int(dd_min)
     return d
 
 
-def partition(n, M, seg, buffer, K, world, rank, pgrid, sched=None) -> dict:
+def partition(n, M, seg, buffer, K, world, rank, pgrid, sched=None, dd_min=0) -> dict:
     """This rank's block of a multi-GPU descriptor (host arithmetic, no GPU)."""
-    d = make_desc(n, M, seg, buffer, K, sched=sched, world=world, rank=rank, pgrid=pgrid)
+    d = make_desc(n, M, seg, buffer, K, sched=sched, world=world, rank=rank, pgrid=pgrid,
+                  dd_min=dd_min)
     p = Partition()
     check(lib.sr_fmg_partition(ctypes.byref(d), ctypes.byref(p)))
     return dict(world=p.world, rank=p.rank, coord=tuple(p.coord),
                 segs_per_rank=tuple(p.segs_per_rank), block_lo=tuple(p.block_lo),
                 block_n=tuple(p.block_n), f_halo=p.f_halo, f_dims=tuple(p.f_dims),
-                level_T_lo=tuple(p.level_T_lo), level_T_n=tuple(p.level_T_n))
+                level_T_lo=tuple(p.level_T_lo), level_T_n=tuple(p.level_T_n),
+                level_A=p.level_A)
 
 
 def nccl_unique_id() -> bytes:
@@ -76,15 +79,16 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-class ReplayStore:
-    """Test-only in-process stand-in for the all-gathers of a multi-rank solve."""
+class HostStore:
+    """Test-only in-process stand-in for NCCL: the ranks' handles (one host thread each, all
+    on one GPU) pass their all-gather blocks and halo slabs through host memory."""
 
     def __init__(self, world):
-        self.ptr = ctypes.c_void_p(lib.sr_fmg_replay_store_create(int(world)))
+        self.ptr = ctypes.c_void_p(lib.sr_fmg_host_store_create(int(world)))
 
     def __del__(self):
         if getattr(self, "ptr", None) and self.ptr.value:
-            lib.sr_fmg_replay_store_destroy(self.ptr)
+            lib.sr_fmg_host_store_destroy(self.ptr)
             self.ptr = ctypes.c_void_p()
 
 
@@ -98,12 +102,12 @@ class Solver:
 
     def __init__(self, n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None,
                  alpha=1, nu1=2, nu2=2, cheb=None, device=None, use_graph=True,
-                 world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, replay_store=None,
-                 stencil="7pt", nl_gamma=0.0, allocator=None):
+                 world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, host_store=None,
+                 stencil="7pt", nl_gamma=0.0, allocator=None, dd_min=0):
         if isinstance(n, int):
             n = (n, n, n)
         d = make_desc(n, M, seg, buffer, K, dtype, h, sched, alpha, nu1, nu2, cheb, device,
-                      use_graph, world, rank, pgrid, stencil, nl_gamma)
+                      use_graph, world, rank, pgrid, stencil, nl_gamma, dd_min)
         if allocator == "torch":
             # the workspace comes from PyTorch's caching allocator (desc.alloc / desc.free);
             # the callbacks must outlive the handle
@@ -123,19 +127,19 @@ class Solver:
             d.alloc, d.free = self._alloc_cb, self._free_cb
         elif allocator is not None:
             raise ValueError("allocator must be None (cudaMalloc) or 'torch'")
-        if world > 1 and replay_store is None:
+        if world > 1 and host_store is None:
             import torch  # noqa: F401  (PyTorch's NCCL is the one the library will reuse)
             if nccl_id is None:
-                raise ValueError("world > 1 needs nccl_id (see nccl_unique_id) or replay_store")
+                raise ValueError("world > 1 needs nccl_id (see nccl_unique_id) or host_store")
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
             d.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
-        if replay_store is not None:
+        if host_store is not None:
             d.comm = 1
         self._h = ctypes.c_void_p()
         check(lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(self._h)))
-        if replay_store is not None:
-            check(lib.sr_fmg_set_replay(self._h, replay_store.ptr), self._h)
-            self._store = replay_store
+        if host_store is not None:
+            check(lib.sr_fmg_set_host_store(self._h, host_store.ptr), self._h)
+            self._store = host_store
         self.n = tuple(int(v) for v in n)
         self.dtype = dtype
         self.np_dtype = np.float64 if dtype == "f64" else np.float32
@@ -206,7 +210,21 @@ class Solver:
 
     @property
     def exchanges_per_solve(self) -> int:
-        return self._info.exchanges_per_solve
+        """Collective calls of the last solve (all-gathers and halo phases)."""
+        return self._get_info().exchanges_per_solve
+
+    @property
+    def level_A(self) -> int:
+        """Levels <= A are gathered and redundant; A < l <= T are domain-decomposed."""
+        return self._info.level_A
+
+    def comm_calls(self):
+        """Collective calls per level in the last solve (index = level)."""
+        i = self._get_info()
+        return [int(i.comm_calls[l]) for l in range(i.M + 1)]
+
+    def dd_levels(self):
+        return [l for l in range(self._info.M + 1) if self._info.dd[l]]
 
     def local_f(self, f_global):
         """This rank's haloed block of a global f (numpy, shape (n3, n2, n1)); cells of the

@@ -11,6 +11,11 @@
 //   PYRAMID   f_c = avg8(f_f) on dense arrays                                 (R6)
 //
 // A = -Lap_h with 7 points; a neighbour outside Omega is the reflected ghost -u_i (R3).
+// A level may be a rank's BLOCK of a domain-decomposed conventional level (multi-GPU,
+// DESIGN.md §8): the operations run over the block's cells (L.S, global offset L.so*L.S),
+// read neighbours in other ranks' blocks from the ghost ring (filled by the halo exchange
+// before the operation) and test the domain boundary in global coordinates -- with one
+// block (S = N, so = 0) this is exactly the single-GPU operation, cell for cell.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -30,13 +35,20 @@ __device__ __forceinline__ long long soff(const Lvl& L, int x, int y, int z) {
   return (long long)(z + 1) * L.pz + (long long)(y + 1) * L.py + (x + 1);
 }
 
+// global index of the block's first cell in dimension d (0 with one block)
+__device__ __forceinline__ int goff(const Lvl& L, int d) { return L.so[d] * L.S[d]; }
+
+// rhs at local cell (x, y, z) / global cell (gx, gy, gz): dense views (f pyramid, user f)
+// are indexed globally (virtual origin), segment-storage views locally
 template <class T>
-__device__ __forceinline__ T rhs_at(const View<T>& v, int x, int y, int z) {
-  if (v.global) return v.p[(long long)z * v.sz + (long long)y * v.sy + x];
+__device__ __forceinline__ T rhs_at(const View<T>& v, int x, int y, int z, int gx, int gy,
+                                    int gz) {
+  if (v.global) return v.p[(long long)gz * v.sz + (long long)gy * v.sy + gx];
   return v.p[(long long)(z + 1) * v.sz + (long long)(y + 1) * v.sy + (x + 1)];
 }
 
-// (A u) at cell (x, y, z) of a conventional level; neighbour order z-, z+, y-, y+, x-, x+
+// (A u) at global cell (x, y, z) of a conventional level (storage offset o); neighbour
+// order z-, z+, y-, y+, x-, x+
 template <class T>
 __device__ __forceinline__ T apply_A(const Lvl& L, const T* __restrict__ u, long long o, int x,
                                      int y, int z) {
@@ -84,18 +96,19 @@ constexpr int kZC = 4;  // planes per register batch (longer chunks loop; 64 reg
 // storage ghosts are zero, so the reflected ghost -u_i is +1 on the diagonal (R3)
 template <class T, bool TAU>
 __device__ void op_column(const Lvl& L, const COp<T>& o, int tid, int nth) {
-  const ColMap m = col_map(L.N[0], L.N[1], L.N[2], tid, nth);
+  const ColMap m = col_map(L.S[0], L.S[1], L.S[2], tid, nth);
   if (!m.ok) return;
   const T cm = T(o.c0), cr = T(o.c1);
-  const bool xm = m.x > 0, xp = m.x < L.N[0] - 1, ym = m.y > 0, yp = m.y < L.N[1] - 1;
+  const int gx = m.x + goff(L, 0), gy = m.y + goff(L, 1), gz0 = goff(L, 2);
+  const bool xm = gx > 0, xp = gx < L.N[0] - 1, ym = gy > 0, yp = gy < L.N[1] - 1;
   const T dxy = T(6 + !xm + !xp + !ym + !yp);
   for (int zb = m.z0; zb < m.z1; zb += kZC) {
     const int ze = min(m.z1, zb + kZC);
     T q[kZC + 2], nb[kZC], bv[kZC], pv[kZC];
     const long long c0 = soff<T>(L, m.x, m.y, zb);
 #pragma unroll
-    for (int k = 0; k < kZC + 2; ++k)  // planes zb-1 .. zb+kZC (ghost planes are zero)
-      q[k] = (zb - 1 + k <= ze) ? o.a[c0 + (long long)(k - 1) * L.pz] : T(0);
+    for (int k = 0; k < kZC + 2; ++k)  // planes zb-1 .. zb+kZC (ghost planes: zero at the
+      q[k] = (zb - 1 + k <= ze) ? o.a[c0 + (long long)(k - 1) * L.pz] : T(0);  // domain face)
 #pragma unroll
     for (int k = 0; k < kZC; ++k) {
       if (zb + k >= ze) break;
@@ -105,7 +118,7 @@ __device__ void op_column(const Lvl& L, const COp<T>& o, int tid, int nth) {
       if constexpr (TAU) {
         bv[k] = o.c[off];
       } else {
-        bv[k] = rhs_at(o.v, m.x, m.y, zb + k);
+        bv[k] = rhs_at(o.v, m.x, m.y, zb + k, gx, gy, gz0 + zb + k);
         pv[k] = o.b ? o.b[off] : T(0);
       }
     }
@@ -113,7 +126,7 @@ __device__ void op_column(const Lvl& L, const COp<T>& o, int tid, int nth) {
     for (int k = 0; k < kZC; ++k) {
       const int z = zb + k;
       if (z >= ze) break;
-      const T d = dxy + T((z == 0 ? 1 : 0) + (z == L.N[2] - 1 ? 1 : 0));
+      const T d = dxy + T((gz0 + z == 0 ? 1 : 0) + (gz0 + z == L.N[2] - 1 ? 1 : 0));
       const T c = q[k + 1];
       const T Au = (d * c - ((q[k] + q[k + 2]) + nb[k])) * T(L.inv_h2) + T(L.nlg) * c * c * c;
       const long long off = c0 + (long long)k * L.pz;
@@ -130,27 +143,34 @@ __device__ void op_column(const Lvl& L, const COp<T>& o, int tid, int nth) {
 
 // RESTRICT: eight lanes per coarse cell, one fine child each (residual of the child with all
 // its loads in flight at once), reduced with three butterfly shuffles
+// (the coarse cells are those of the fine block: local X of the fine block's coarsening,
+// global X + goff(Lf)/2, written at their local index in the coarse array -- a block of a
+// decomposed level, or the rank's part of a global one)
 template <class T>
 __device__ void op_restrict(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int tid, int nth) {
-  const int n = Lc.N[0] * Lc.N[1] * Lc.N[2];
+  const int nc[3] = {Lf.S[0] / 2, Lf.S[1] / 2, Lf.S[2] / 2};
+  const int n = nc[0] * nc[1] * nc[2];
   const int ch = tid & 7;
   const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
+  const int fo[3] = {goff(Lf, 0), goff(Lf, 1), goff(Lf, 2)};
   for (int base = tid - ch; base < 8 * n; base += nth) {  // warp-uniform trip count
     const int c = base >> 3;
     const bool ok = c < n;
     int X, Y, Z;
-    cell_of(ok ? c : n - 1, Lc.N, X, Y, Z);
+    cell_of(ok ? c : n - 1, nc, X, Y, Z);
     const int x = 2 * X + dx, y = 2 * Y + dy, z = 2 * Z + dz;
     const long long off = soff<T>(Lf, x, y, z);
     T su = o.a[off];
-    T sr = rhs_at(o.v, x, y, z) - apply_A(Lf, o.a, off, x, y, z);
+    T sr = rhs_at(o.v, x, y, z, x + fo[0], y + fo[1], z + fo[2]) -
+           apply_A(Lf, o.a, off, x + fo[0], y + fo[1], z + fo[2]);
 #pragma unroll
     for (int m = 1; m < 8; m <<= 1) {
       su += __shfl_xor_sync(0xffffffffu, su, m);
       sr += __shfl_xor_sync(0xffffffffu, sr, m);
     }
     if (ok && ch == 0) {
-      const long long co = soff<T>(Lc, X, Y, Z);
+      const long long co = soff<T>(Lc, X + fo[0] / 2 - goff(Lc, 0), Y + fo[1] / 2 - goff(Lc, 1),
+                                   Z + fo[2] / 2 - goff(Lc, 2));
       o.c[co] = su * T(0.125);
       o.d[co] = sr * T(0.125);
     }
@@ -159,10 +179,11 @@ __device__ void op_restrict(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int t
 
 template <class T>
 __device__ void op_prolong(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int tid, int nth) {
-  const ColMap m = col_map(Lf.N[0], Lf.N[1], Lf.N[2], tid, nth);
+  const ColMap m = col_map(Lf.S[0], Lf.S[1], Lf.S[2], tid, nth);
   if (!m.ok) return;
   const T W0 = T(0.75), W1 = T(0.25);
-  const int g[2] = {m.x, m.y};
+  const int g[2] = {m.x + goff(Lf, 0), m.y + goff(Lf, 1)};
+  const int co[3] = {goff(Lc, 0), goff(Lc, 1), goff(Lc, 2)};
   int P[2], Q[2];
   T sg[2];
 #pragma unroll
@@ -172,12 +193,16 @@ __device__ void op_prolong(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int ti
     sg[d] = T(1);
     if (Q[d] < 0) { Q[d] = 0; sg[d] = T(-1); }
     if (Q[d] >= Lc.N[d]) { Q[d] = Lc.N[d] - 1; sg[d] = T(-1); }
+    P[d] -= co[d];  // local coarse index (-1 or S_c: the ghost ring of a block)
+    Q[d] -= co[d];
   }
-  // xy-interpolant of coarse plane cz (weights 3/4 parent, 1/4 neighbour, signed ghosts)
+  // xy-interpolant of coarse plane cz (global; weights 3/4 parent, 1/4 neighbour, signed
+  // ghosts)
   auto ixy = [&](int cz) {
     T sgz = T(1);
     if (cz < 0) { cz = 0; sgz = T(-1); }
     if (cz >= Lc.N[2]) { cz = Lc.N[2] - 1; sgz = T(-1); }
+    cz -= co[2];
     T py[2];
 #pragma unroll
     for (int ky = 0; ky < 2; ++ky) {
@@ -190,7 +215,8 @@ __device__ void op_prolong(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int ti
     return sgz * (W0 * py[0] + (W1 * sg[1]) * py[1]);
   };
   for (int z = m.z0; z < m.z1; ++z) {
-    const int Pz = z >> 1, Qz = Pz + ((z & 1) ? 1 : -1);
+    const int gz = z + goff(Lf, 2);
+    const int Pz = gz >> 1, Qz = Pz + ((gz & 1) ? 1 : -1);
     const T acc = W0 * ixy(Pz) + W1 * ixy(Qz);
     const long long off = soff<T>(Lf, m.x, m.y, z);
     o.c[off] = o.flag ? o.c[off] + acc : acc;
@@ -227,6 +253,9 @@ __global__ void __launch_bounds__(kThreadsC, 1)
   // indexed kernel-parameter reads go through the constant cache and miss (~1 us per op)
   __shared__ COp<T> sop[kCoarseMaxOps];
   __shared__ Lvl sL[kCoarseMaxLevels];
+  extern __shared__ __align__(16) unsigned char dyn[];
+  T* dres = reinterpret_cast<T*>(dyn);  // resident buffers (used in CTA 0 only)
+  const int rank = (int)cl.block_rank();
   {
     const int* src = reinterpret_cast<const int*>(ol.op);
     int* dst = reinterpret_cast<int*>(sop);
@@ -235,9 +264,32 @@ __global__ void __launch_bounds__(kThreadsC, 1)
     const int* ls = reinterpret_cast<const int*>(ol.L);
     int* ld = reinterpret_cast<int*>(sL);
     for (int k = threadIdx.x; k < (int)(sizeof(sL) / sizeof(int)); k += blockDim.x) ld[k] = ls[k];
+    if (rank == 0)  // the tiny levels' arrays into shared memory
+      for (int r = 0; r < ol.nres; ++r)
+        for (int e = threadIdx.x; e < ol.res_n[r]; e += blockDim.x)
+          dres[ol.res_off[r] + e] = ol.res_g[r][e];
   }
   __syncthreads();
-  const int rank = (int)cl.block_rank();
+  if (ol.nres > 0) {
+    // redirect every operation's pointers into a resident buffer to CTA 0's copy (a
+    // distributed-shared-memory address on the other CTAs)
+    auto rm = [&](const T* p) -> T* {
+      for (int r = 0; r < ol.nres; ++r)
+        if (p >= ol.res_g[r] && p < ol.res_g[r] + ol.res_n[r])
+          return cl.map_shared_rank(dres + ol.res_off[r], 0) + (p - ol.res_g[r]);
+      return const_cast<T*>(p);
+    };
+    for (int i = threadIdx.x; i < ol.n; i += blockDim.x) {
+      COp<T>& o = sop[i];
+      o.a = rm(o.a);
+      o.b = rm(o.b);
+      o.c = rm(o.c);
+      o.d = rm(o.d);
+      if (!o.v.global) o.v.p = rm(o.v.p);
+    }
+    __syncthreads();
+  }
+  cl.sync();  // CTA 0's copies are in place before any operation reads them
   if (ol.prof && rank == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -268,7 +320,7 @@ __global__ void __launch_bounds__(kThreadsC, 1)
           for (int j = threadIdx.x; j < n0; j += kThreadsC) {
             int x, y, z;
             cell_of(j, L.N, x, y, z);
-            bs[j] = rhs_at(o.v, x, y, z);
+            bs[j] = rhs_at(o.v, x, y, z, x, y, z);
           }
           __syncthreads();
           // nonlinear (R29): Picard sweeps u <- A_lin^-1 (b - nlg u^3), as k_coarsest
@@ -284,7 +336,7 @@ __global__ void __launch_bounds__(kThreadsC, 1)
               for (int j = threadIdx.x; j < n0; j += kThreadsC) {
                 int x, y, z;
                 cell_of(j, L.N, x, y, z);
-                bs[j] = rhs_at(o.v, x, y, z) - T(L.nlg) * us[j] * us[j] * us[j];
+                bs[j] = rhs_at(o.v, x, y, z, x, y, z) - T(L.nlg) * us[j] * us[j] * us[j];
               }
               __syncthreads();
             }
@@ -308,6 +360,11 @@ __global__ void __launch_bounds__(kThreadsC, 1)
       ol.prof[i + 1] = t;
     }
   }
+  // (the last operation ended with a cluster barrier: every write to CTA 0's copies is done)
+  if (rank == 0)
+    for (int r = 0; r < ol.nres; ++r)
+      for (int e = threadIdx.x; e < ol.res_n[r]; e += blockDim.x)
+        const_cast<T*>(ol.res_g[r])[e] = dres[ol.res_off[r] + e];
 }
 
 }  // namespace
@@ -329,9 +386,13 @@ void launch_coarse_exec(const COpList<T>& ops, cudaStream_t st) {
   if (ops.n <= 0) return;
   // (per launch: the attribute is per device, and a process may drive several)
   cudaFuncSetAttribute(k_coarse_exec<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  const size_t dyn = (size_t)ops.res_total * sizeof(T);
+  cudaFuncSetAttribute(k_coarse_exec<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(dyn, 16));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kCluster);
   cfg.blockDim = dim3(kThreadsC);
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;

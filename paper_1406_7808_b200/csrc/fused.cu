@@ -538,6 +538,216 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, NST>::NT,
   }
 }
 
+// =====================================================================================
+// Lean degree-2 pass (same geometry, rings and arithmetic plan as k_cheb2s; FIN = 0 / 1):
+// the per-cell region masks are folded into per-slot coefficients, so a plane step is
+// branch- and select-free.  A slot that is not a C cell (GSR ring, out-of-domain row or
+// column, padding) gets c0 = cr = 0: u1 = fma(0, r, u0) = u0 and u2 = c1 + cm (c1 - u0) + 0
+// = u0 exactly, provided r is finite -- so every shared-memory word a dead slot reads is
+// zeroed once at the start (margin rows, rows beyond the loaded range).  Planes outside
+// C in z are uniform per CTA (a uniform branch copies them).  The diagonal (6 + reflected
+// neighbours, R3) is kept per slot, pre-multiplied by 1/h^2:
+//   r = f - (d u - sum) / h^2 = fma(1/h^2, sum, fma(-d/h^2, u, f)).
+// =====================================================================================
+template <class T, int PY, int BH, int MAXS, int RG, int FIN = 0>
+__global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, 2>::NT,
+                                  SpecGeom<T, PY, BH, MAXS, RG, 2>::MINB)
+    k_cheb2l(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<T> a) {
+  using G = SpecGeom<T, PY, BH, MAXS, RG, 2>;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const Lvl& L = a.L;
+  const int Ex = L.E[0], Ey = L.E[1], Ez = L.E[2];
+  const long long pz = L.pz;
+  const int s = blockIdx.y;
+  const int r0 = blockIdx.x * BH, r1 = min(Ey, r0 + BH);
+  const int s0 = max(0, r0 - 1), s1 = min(Ey, r1 + 1);
+  const int q0 = max(0, r0 - 2), q1 = min(Ey, r1 + 2);
+  T* u0s = reinterpret_cast<T*>(sm);
+  T* fs = u0s + G::RU * G::U0S;
+  T* u1s = fs + G::RF * G::FS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + G::NU1 * G::U1S);
+
+  const int px = s % L.ns[0] + L.so[0];
+  const int pyy = (s / L.ns[0]) % L.ns[1] + L.so[1];
+  const int pzz = s / (L.ns[0] * L.ns[1]) + L.so[2];
+  const int ox = px * L.S[0] - (L.J + 1);
+  const int oy = pyy * L.S[1] - (L.J + 1);
+  const int oz = pzz * L.S[2] - (L.J + 1);
+  const T* useg = a.uin + (long long)s * L.ss;
+  T* oseg = a.uout + (long long)s * L.ss;
+  const T* rseg = RG ? nullptr : a.rhs_seg + (long long)s * L.ss;
+  const uint32_t u0_bytes = (uint32_t)((q1 - q0) * PY * sizeof(T));
+  const int oxt = ox - a.foff[0];
+  const int oxa = oxt & ~(G::kAl - 1);
+  const int fsh = RG ? oxt - oxa : 0;
+  const uint32_t f_bytes = RG ? (uint32_t)((BH + 2) * G::FP * sizeof(T))
+                              : (uint32_t)((s1 - s0) * PY * sizeof(T));
+  // zero every buffer once: dead slots read margin rows and rows no copy fills
+  {
+    const int nw = (int)((G::RU * G::U0S + G::RF * G::FS + G::NU1 * G::U1S) * sizeof(T) / 16);
+    uint4* z4 = reinterpret_cast<uint4*>(sm);
+    for (int i = threadIdx.x; i < nw; i += G::NT) z4[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < G::RU + G::RF; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // generic-proxy zero stores before the async-proxy (TMA) writes into the same buffers
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  auto issue_u0 = [=](int z) {
+    const int sl = z % G::RU;
+    mbar_expect_tx(&bars[sl], u0_bytes);
+    bulk_g2s(u0s + sl * G::U0S + (q0 - s0 + 1) * PY, useg + (long long)z * pz + (long long)q0 * PY,
+             u0_bytes, &bars[sl]);
+  };
+  auto issue_f = [=, &fmap](int z) {
+    const int sl = z % G::RF;
+    mbar_expect_tx(&bars[G::RU + sl], f_bytes);
+    if (RG)
+      tma_3d(fs + sl * G::FS, &fmap, oxa, oy + s0 - a.foff[1], oz + z - a.foff[2],
+             &bars[G::RU + sl]);
+    else
+      bulk_g2s(fs + sl * G::FS, rseg + (long long)z * pz + (long long)s0 * PY, f_bytes,
+               &bars[G::RU + sl]);
+  };
+  if (threadIdx.x == 0) {
+    for (int z = 0; z < min(G::RU, Ez); ++z) issue_u0(z);
+    for (int z = 0; z < min(3, Ez); ++z) issue_f(z);
+  }
+
+  const int tx = threadIdx.x % PY, g = threadIdx.x / PY;
+  const int y0 = s0 + g * MAXS;
+  const int gxv = ox + tx;
+  const bool tin = tx < Ex && gxv >= 0 && gxv < L.N[0];
+  const bool tcx = tx >= 1 && tx <= Ex - 2;
+  const T ih2 = T(L.inv_h2);
+  // per slot: the two step coefficients (0 on dead slots), the scaled diagonal, and the
+  // rows of the band's output (written whole, padding and dead cells unchanged)
+  T c0k[MAXS], crk[MAXS], dkh[MAXS];
+  bool wr[MAXS];
+  unsigned gen_mask = 0;
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    const int y = y0 + k;
+    const int gy = oy + y;
+    const bool c = tin && tcx && y < s1 && y >= 1 && y <= Ey - 2 && gy >= 0 && gy < L.N[1];
+    c0k[k] = c ? a.c0 : T(0);
+    crk[k] = c ? a.cr : T(0);
+    const int nb = 6 + (gxv == 0) + (gxv == L.N[0] - 1) + (gy == 0) + (gy == L.N[1] - 1);
+    dkh[k] = T(nb) * ih2;
+    wr[k] = y >= r0 && y < r1 && y0 < s1;
+    if constexpr (FIN == 1) {
+      const int vlo = L.J + 1;
+      if (wr[k] && tin && gy >= 0 && gy < L.N[1] && tx >= vlo && tx < vlo + L.S[0] && y >= vlo &&
+          y < vlo + L.S[1])
+        gen_mask |= 1u << k;
+    }
+  }
+  T* fbase = nullptr;
+  if constexpr (FIN == 1)
+    fbase = a.fin.p + (long long)(oy + y0 - a.fin.bo[1]) * a.fin.sy + (gxv - a.fin.bo[0]);
+  const T* const u0b = u0s + (y0 - s0 + 1) * PY + tx;
+  const T* const fb = fs + (y0 - s0) * G::FP + tx + fsh;
+  T* const u1b = u1s + (y0 - s0 + 1) * PY + tx;
+  T* const ob = oseg + (long long)y0 * PY + tx;
+  T u0q[MAXS][3], u1q[MAXS][3];
+  mbar_wait(&bars[0], 0);
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    u0q[k][0] = u0b[k * PY];
+    u0q[k][1] = u0q[k][2] = T(0);
+    u1q[k][0] = u1q[k][1] = u1q[k][2] = T(0);
+  }
+  const T cm = a.cm;
+
+  auto step = [&](auto RR, int z) {
+    constexpr int R = decltype(RR)::value;  // z % 3: u0 ring slot, u1 buffer, queue slot
+    constexpr int IM = (R + 2) % 3, I0 = R, IP = (R + 1) % 3;
+    if (z < Ez) {
+      if (z + 1 < Ez) mbar_wait(&bars[(z + 1) % G::RU], ((z + 1) / G::RU) & 1);
+      mbar_wait(&bars[G::RU + z % G::RF], (z / G::RF) & 1);
+      const T* pl = u0b + (z % G::RU) * G::U0S;
+      const T* pn = u0b + ((z + 1) % G::RU) * G::U0S;
+      const T* fp = fb + (z % G::RF) * G::FS;
+      T* u1w = u1b + R * G::U1S;
+      const int gz = oz + z;
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) u0q[k][IP] = (z + 1 < Ez) ? pn[k * PY] : T(0);
+      if (gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2) {  // uniform: C planes
+        const T dzh = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0)) * ih2;
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) {
+          const T v0 = u0q[k][I0];
+          const T ym = (k == 0) ? pl[-PY] : u0q[k > 0 ? k - 1 : 0][I0];
+          const T yp = (k == MAXS - 1) ? pl[MAXS * PY] : u0q[k + 1 < MAXS ? k + 1 : k][I0];
+          const T sum = ((u0q[k][IM] + u0q[k][IP]) + (ym + yp)) + (pl[k * PY - 1] + pl[k * PY + 1]);
+          const T r = fma(ih2, sum, fma(-(dkh[k] + dzh), v0, fp[k * G::FP]));
+          const T v1 = fma(c0k[k], r, v0);
+          u1q[k][I0] = v1;
+          u1w[k * PY] = v1;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) {
+          u1q[k][I0] = u0q[k][I0];
+          u1w[k * PY] = u0q[k][I0];
+        }
+      }
+    }
+    __syncthreads();  // the only barrier of the plane step
+    if (threadIdx.x == 0) {
+      if (z + G::RU < Ez) issue_u0(z + G::RU);  // u0 slot of plane z is free
+      if (z >= 1 && z + 2 < Ez) issue_f(z + 2);  // rhs slot of plane z-2 is free
+    }
+    if (z >= 1) {
+      const int zz = z - 1;
+      const int gz = oz + zz;
+      if (gz >= 0 && gz < L.N[2]) {
+        constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
+        T v2[MAXS];
+        if (zz >= 1 && zz <= Ez - 2) {  // uniform: C planes
+          const T dzh = T((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0)) * ih2;
+          const T* u1r = u1b + J1 * G::U1S;
+          const T* fp = fb + (zz % G::RF) * G::FS;
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k) {
+            const T u0v = u0q[k][J1];
+            const T c1 = u1q[k][J1];
+            const T ym = (k == 0) ? u1r[-PY] : u1q[k > 0 ? k - 1 : 0][J1];
+            const T yp = (k == MAXS - 1) ? u1r[MAXS * PY] : u1q[k + 1 < MAXS ? k + 1 : k][J1];
+            const T sum = ((u1q[k][J2] + u1q[k][J0]) + (ym + yp)) + (u1r[k * PY - 1] + u1r[k * PY + 1]);
+            const T r = fma(ih2, sum, fma(-(dkh[k] + dzh), c1, fp[k * G::FP]));
+            v2[k] = fma(crk[k], r, fma(cm, c1 - u0v, c1));
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k) v2[k] = u0q[k][J1];
+        }
+        if constexpr (FIN != 1) {
+          T* orow = ob + (long long)zz * pz;
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k)
+            if (wr[k]) orow[k * PY] = v2[k];
+        } else {
+          // last pass: genuine cells of a genuine plane go to the user's u (R19)
+          if (zz >= L.J + 1 && zz < L.J + 1 + L.S[2]) {
+            T* frow = fbase + (long long)(gz - a.fin.bo[2]) * a.fin.sz;
+#pragma unroll
+            for (int k = 0; k < MAXS; ++k)
+              if ((gen_mask >> k) & 1u) frow[k * a.fin.sy] = v2[k];
+          }
+        }
+      }
+    }
+  };
+  for (int zb = 0; zb <= Ez; zb += 3) {
+    step(std::integral_constant<int, 0>{}, zb);
+    if (zb + 1 <= Ez) step(std::integral_constant<int, 1>{}, zb + 1);
+    if (zb + 2 <= Ez) step(std::integral_constant<int, 2>{}, zb + 2);
+  }
+}
+
 // ---- host side ---------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -632,6 +842,19 @@ bool encode_rhs_map(CUtensorMap* map, const FusedRhs<T>& rb, int bw, int rows) {
   return r == CUDA_SUCCESS;
 }
 
+// lean plane steps (k_cheb2l) for the plain and last degree-2 passes.  Measured at C3's
+// finest level (ncu, one pass): fp32 0.45 vs 0.50 ms (lean faster); fp64 0.752 vs 0.720 ms
+// (the masked k_cheb2s faster: 414 vs 437 M instructions, but 96 registers and more
+// short-scoreboard stalls).  SR_FMG_CHEB_LEAN=0/1 forces one for both (A/B).
+template <class T>
+bool lean() {
+  static const int v = [] {
+    const char* e = std::getenv("SR_FMG_CHEB_LEAN");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return v < 0 ? sizeof(T) == 4 : v == 1;
+}
+
 // geometry-specialised launch if (T, row pitch) has an instantiation
 template <class T, int PY, int BH, int MAXS>
 bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
@@ -650,7 +873,9 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
     using G2 = SpecGeom<T, PY, BH, MAXS, 1, 2>;
     using G1 = SpecGeom<T, PY, BH, MAXS, 1, 1>;
     if (!encode_rhs_map<T>(&map, b, G2::FP, BH + 2)) return false;
-    if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 1, 2, 1>, G2::SMEM, G2::NT);
+    if (nst == 2 && fin && lean<T>()) go(k_cheb2l<T, PY, BH, MAXS, 1, 1>, G2::SMEM, G2::NT);
+    else if (nst == 2 && lean<T>()) go(k_cheb2l<T, PY, BH, MAXS, 1, 0>, G2::SMEM, G2::NT);
+    else if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 1, 2, 1>, G2::SMEM, G2::NT);
     else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 1, 2>, G2::SMEM, G2::NT);
     else go(k_cheb2s<T, PY, BH, MAXS, 1, 1>, G1::SMEM, G1::NT);
   } else {
@@ -659,7 +884,9 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
     if (a.tout) {  // tau fused in front (FIN = 2)
       if (nst != 2 || fin) return false;
       go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 2>, G2::SMEM, G2::NT);
-    } else if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 1>, G2::SMEM, G2::NT);
+    } else if (nst == 2 && fin && lean<T>()) go(k_cheb2l<T, PY, BH, MAXS, 0, 1>, G2::SMEM, G2::NT);
+    else if (nst == 2 && lean<T>()) go(k_cheb2l<T, PY, BH, MAXS, 0, 0>, G2::SMEM, G2::NT);
+    else if (nst == 2 && fin) go(k_cheb2s<T, PY, BH, MAXS, 0, 2, 1>, G2::SMEM, G2::NT);
     else if (nst == 2) go(k_cheb2s<T, PY, BH, MAXS, 0, 2>, G2::SMEM, G2::NT);
     else go(k_cheb2s<T, PY, BH, MAXS, 0, 1>, G1::SMEM, G1::NT);
   }

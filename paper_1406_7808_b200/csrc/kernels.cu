@@ -894,6 +894,52 @@ __global__ void __launch_bounds__(kThreads) k_box_copy(T* __restrict__ base, lon
   }
 }
 
+// f_{l-1} = avg8(f_l) (R6) over a box of coarse cells [lo, lo + n) (global indices) between
+// two dense views indexed globally (virtual origins): a rank's block of a domain-decomposed
+// level, read from its (haloed) local f_l, written into its local f_{l-1} block or into its
+// part of a global array (multi-GPU pyramid below level T)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_pyramid_box(View<T> f, View<T> c, int lx, int ly,
+                                                          int lz, int nx, int ny, int nz) {
+  const long long n = (long long)nx * ny * nz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int X = lx + (int)(i % nx);
+    const int Y = ly + (int)((i / nx) % ny);
+    const int Z = lz + (int)(i / ((long long)nx * ny));
+    T s = T(0);
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx)
+          s += f.p[(long long)(2 * Z + dz) * f.sz + (long long)(2 * Y + dy) * f.sy + (2 * X + dx)];
+    const_cast<T*>(c.p)[(long long)Z * c.sz + (long long)Y * c.sy + X] = s * T(0.125);
+  }
+}
+
+// dst = a - b (b != null) or dst = a on the S^3 block cells of two storage layouts (local
+// cell (x, y, z) at (z + ga) pz + (y + ga) py + x + ga): the correction footprint of the
+// k = 1 hand-off, w - t (or u for the FMG interpolation), moved into the wider-ghosted
+// level-T array of a domain-decomposed run
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_block_diff(Lvl La, const T* __restrict__ a,
+                                                         const T* __restrict__ b, Lvl Ld,
+                                                         T* __restrict__ dst) {
+  const long long n = (long long)La.S[0] * La.S[1] * La.S[2];
+  const int ga = La.J + 1, gd = Ld.J + 1;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % La.S[0]);
+    const int y = (int)((i / La.S[0]) % La.S[1]);
+    const int z = (int)(i / ((long long)La.S[0] * La.S[1]));
+    const long long oa = (long long)(z + ga) * La.pz + (long long)(y + ga) * La.py + (x + ga);
+    const long long od = (long long)(z + gd) * Ld.pz + (long long)(y + gd) * Ld.py + (x + gd);
+    dst[od] = b ? a[oa] - b[oa] : a[oa];
+  }
+}
+
 }  // namespace
 
 // column-layout launch geometry: (bx, by) tile over an (ex, ey) plane, z split into
@@ -1024,6 +1070,23 @@ void launch_gather(const Lvl& L, const T* useg, T* out, const int bo[3], long lo
 }
 
 template <class T>
+void launch_pyramid_box(View<T> f, View<T> c, const int lo[3], const int n[3], cudaStream_t st) {
+  const long long cnt = (long long)n[0] * n[1] * n[2];
+  if (cnt <= 0) return;
+  const unsigned g = (unsigned)std::min<long long>(148LL * 8, (cnt + kThreads - 1) / kThreads);
+  k_pyramid_box<T><<<std::max(g, 1u), kThreads, 0, st>>>(f, c, lo[0], lo[1], lo[2], n[0], n[1],
+                                                         n[2]);
+}
+
+template <class T>
+void launch_block_diff(const Lvl& La, const T* a, const T* b, const Lvl& Ld, T* dst,
+                       cudaStream_t st) {
+  const long long cnt = (long long)La.S[0] * La.S[1] * La.S[2];
+  const unsigned g = (unsigned)std::min<long long>(148LL * 8, (cnt + kThreads - 1) / kThreads);
+  k_block_diff<T><<<std::max(g, 1u), kThreads, 0, st>>>(La, a, b, Ld, dst);
+}
+
+template <class T>
 void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const int n[3], T* buf,
                      int to_buf, cudaStream_t st) {
   const long long cnt = (long long)n[0] * n[1] * n[2];
@@ -1049,7 +1112,9 @@ void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const
   template void launch_gather<T>(const Lvl&, const T*, T*, const int*, long long, long long,      \
                                  cudaStream_t);                                                  \
   template void launch_box_copy<T>(T*, long long, long long, const int*, const int*, T*, int,    \
-                                   cudaStream_t);
+                                   cudaStream_t);                                                  \
+  template void launch_pyramid_box<T>(View<T>, View<T>, const int*, const int*, cudaStream_t);    \
+  template void launch_block_diff<T>(const Lvl&, const T*, const T*, const Lvl&, T*, cudaStream_t);
 SRFMG_INST(double)
 SRFMG_INST(float)
 

@@ -80,6 +80,16 @@ template <class T>
 void launch_box_copy(T* base, long long sy, long long sz, const int lo[3], const int n[3], T* buf,
                      int to_buf, cudaStream_t st);
 
+// f_{l-1} = avg8(f_l) over the coarse box [lo, lo + n) (global indices) of two globally
+// indexed dense views (virtual origins): the pyramid of a rank's block below level T
+template <class T>
+void launch_pyramid_box(View<T> f, View<T> c, const int lo[3], const int n[3], cudaStream_t st);
+// dst = a - b (or a when b == null) on the S^3 block cells of two storage layouts La, Ld
+// (ghost widths La.J + 1, Ld.J + 1): the k = 1 footprint array of a decomposed level T
+template <class T>
+void launch_block_diff(const Lvl& La, const T* a, const T* b, const Lvl& Ld, T* dst,
+                       cudaStream_t st);
+
 extern const char* const kKernelNames[];
 extern const int kNumKernelNames;
 

@@ -7,7 +7,11 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -41,13 +45,23 @@ struct LevelBufs {
   void* floc = nullptr;             // multi-GPU: this rank's haloed block of f_l, T <= l < M
   void* rres = nullptr;             // SR levels T < l < M: restricted residual R when the tau
                                     // is fused into the next pass (read there, rhs written)
+  void* dwt = nullptr;              // decomposed levels < T: w - t with exchanged ghosts
 };
 
 // collectives of the multi-GPU path: all-gather of equal per-rank blocks
+// (agglomeration of a coarse level), and groups of point-to-point transfers (one phase of a
+// halo exchange on a domain-decomposed level)
+struct Xfer {
+  int peer;      // rank
+  int recv;      // 0: send buf to peer, 1: receive buf from peer
+  void* buf;     // device
+  size_t bytes;
+};
 struct Comm {
   virtual ~Comm() {}
   virtual sr_status_t allgather(sr_fmg* h, const void* send, void* recv, size_t bytes,
                                 cudaStream_t st) = 0;
+  virtual sr_status_t group(sr_fmg* h, const Xfer* xs, int n, cudaStream_t st) = 0;
 };
 
 struct ProfRec {
@@ -100,15 +114,20 @@ struct sr_fmg {
   long long hcalls = 0;
   long long launches = 0;
   bool sync_debug = false;
+  bool trace = false;  // SR_FMG_TRACE=1: print every collective (multi-rank debugging)
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
   bool force = false; // SR_FMG_FORCE_FUSED=1: use them even on levels too small to fill the GPU
   int fused_min_e = 0; // SR_FMG_FUSED_MIN_E: smallest storage extent given to the TMA kernels
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
+  bool seg = true;    // segment-resident half visits on the small SR levels (seg.cu);
+                      // SR_FMG_SEG=0 off
   bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
   bool tau_fuse = true;      // tau inside the next pre-smoothing pass; SR_FMG_TAU_FUSE=0 off
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
   // disables it.  flush_fn: enqueue the recorded operations (called before every launch)
   bool cexec = true;
+  bool cexec_res = true;  // tiny levels resident in the executor's shared memory
+                          // (SR_FMG_CEXEC_RES=0 off)
   void (*flush_fn)(void*) = nullptr;
   void* flush_ctx = nullptr;
   int prof_cls = -1, prof_level = -1;
@@ -129,6 +148,20 @@ struct sr_fmg {
   size_t xbytes = 0;                        // bytes per rank of the largest exchange
   long long exch = 0;                       // exchanges in the current solve
   long long exch_per_solve = 0;
+  // domain decomposition of the conventional levels: levels A < l <= T are
+  // held as this rank's block (Omega_l block + one ghost ring, refreshed by a halo exchange
+  // before every operator application); levels l <= A are gathered once and solved
+  // redundantly on every rank (the paper's redundant coarse grid)
+  int A = 0;
+  int dd_min = 0;                           // a level stays decomposed while every block
+                                            // dimension has at least dd_min cells
+  srfmg::Lvl LT2{};                         // level T block with the k = 1 footprint ghosts
+  void* wT2 = nullptr;                      // w - t (or u) of level T on LT2 storage
+  void* zT2 = nullptr;                      // zeros on LT2 storage (the correction's t)
+  void* hsend = nullptr;                    // halo staging buffers (device)
+  void* hrecv = nullptr;
+  size_t hbytes = 0;
+  std::vector<long long> comm_calls;        // collective calls per level, last solve
 };
 
 namespace {
@@ -181,6 +214,7 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
     return bad("need 0 <= cheb_lo < cheb_hi (cheb_lo = 0: the stencil's default)");
   if (d->stencil != 7 && d->stencil != 27) return bad("stencil must be 7 or 27");
   if (!(d->nl_gamma >= 0) || !std::isfinite(d->nl_gamma)) return bad("nl_gamma must be >= 0");
+  if (d->dd_min < 0 || d->dd_min == 1) return bad("dd_min must be 0 (default) or >= 2");
   if (d->world < 1) return bad("world must be >= 1");
   for (int i = 0; i < 3; ++i)
     if (d->pgrid[i] < 1 || d->pgrid[i] > d->world) return bad("need 1 <= pgrid[d] <= world");
@@ -193,7 +227,7 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
   }
   // supported-config checks
   if (d->world > 1 && d->comm != 0 && d->comm != 1) {
-    msg = "comm must be 0 (NCCL) or 1 (replay store)";
+    msg = "comm must be 0 (NCCL) or 1 (host store, tests)";
     return SR_ERR_UNSUPPORTED_CONFIG;
   }
   if (d->sr_levels > 0) {  // every launch puts a rank's segments in gridDim.y (<= 65535)
@@ -274,15 +308,32 @@ void make_plan(sr_fmg* h) {
       h->flo[l][i] = (h->blk_lo[i] >> (h->M - l)) - h->H[l];
       h->fdim[l][i] = (h->blk_n[i] >> (h->M - l)) + 2 * h->H[l];
     }
+  // domain decomposition below the SR levels: level l <= T stays decomposed while every
+  // dimension of the rank's block has at least dd_min cells (and the block coarsens evenly
+  // onto level l-1); the first level that does not is gathered (A), and every level <= A is
+  // solved redundantly
+  h->dd_min = d->dd_min > 0 ? d->dd_min : 32;
+  h->A = h->T;
+  if (h->world > 1) {
+    while (h->A >= 1) {
+      bool ok = true;
+      for (int i = 0; i < 3; ++i)
+        ok = ok && (h->blk_n[i] >> (h->M - h->A)) >= h->dd_min &&
+             h->blk_n[i] % (1LL << (h->M - h->A + 1)) == 0;
+      if (!ok) break;
+      --h->A;
+    }
+  }
   for (int l = 0; l <= h->M; ++l) {
     Lvl& L = h->L[l];
     const bool sr = l > h->T;
+    const bool ddl = h->world > 1 && l > h->A && l <= h->T;  // this rank's block of Omega_l
     for (int i = 0; i < 3; ++i) L.N[i] = (int)(d->n[i] >> (h->M - l));
     L.J = sr ? buffer_of(d, l - h->T) : 0;
     for (int i = 0; i < 3; ++i) {
-      L.S[i] = sr ? (d->seg >> (h->M - l)) : L.N[i];
+      L.S[i] = sr ? (d->seg >> (h->M - l)) : ddl ? (h->blk_n[i] >> (h->M - l)) : L.N[i];
       L.ns[i] = sr ? h->nsr[i] : 1;
-      L.so[i] = sr ? h->coord[i] * h->nsr[i] : 0;
+      L.so[i] = sr ? h->coord[i] * h->nsr[i] : ddl ? h->coord[i] : 0;
       L.E[i] = L.S[i] + 2 * L.J + 2;
     }
     L.nsegs = L.ns[0] * L.ns[1] * L.ns[2];
@@ -318,6 +369,19 @@ void make_plan(sr_fmg* h) {
   }
   h->visits.assign(h->M + 1, 0);
   for (int l = 0; l <= h->M; ++l) h->visits[l] = h->M - l + 1;
+  h->comm_calls.assign(h->M + 1, 0);
+  // a decomposed level T also keeps a copy of its block with the ghost width of the k = 1
+  // footprint, grow(V_T^p, ceil(J/2) + 1) (R15): the interpolation and the correction of the
+  // first SR level read up to that far into the neighbouring ranks' blocks
+  h->LT2 = h->L[h->T];
+  if (h->world > 1 && h->A < h->T && h->K > 0) {
+    Lvl& L2 = h->LT2;
+    L2.J = std::max(0, (h->L[h->T + 1].J + 1) / 2);  // ghost width J + 1 = ceil(J_{T+1}/2) + 1
+    for (int i = 0; i < 3; ++i) L2.E[i] = L2.S[i] + 2 * L2.J + 2;
+    L2.py = (int)round_up(L2.E[0], pitch_mult);
+    L2.pz = (long long)L2.py * L2.E[1];
+    L2.ss = round_up(L2.pz * L2.E[2], 32);
+  }
 }
 
 // dense inverse of A_0 (7-point, reflected ghosts) by Gauss-Jordan in fp64 (R7)
@@ -450,12 +514,18 @@ struct Schedule {
   View<T> fview(int l) {
     View<T> v{};
     v.global = 1;
-    const bool local = l > h->T || (l == h->M);
-    if (local) {
+    const bool local = l > h->T || (l == h->M) || (h->world > 1 && l > h->A);
+    if (local && (l == h->M || l >= h->T)) {
       v.base = (l == h->M) ? f : (const T*)(h->world > 1 ? h->B[l].floc : h->B[l].fpyr);
       for (int i = 0; i < 3; ++i) {
         v.dims[i] = h->fdim[l][i];
         v.off[i] = h->flo[l][i];
+      }
+    } else if (local) {  // decomposed level below T: the rank's block of f_l, no halo
+      v.base = (const T*)h->B[l].fpyr;
+      for (int i = 0; i < 3; ++i) {
+        v.dims[i] = h->L[l].S[i];
+        v.off[i] = h->blk_lo[i] >> (h->M - l);
       }
     } else {
       v.base = (const T*)h->B[l].fpyr;
@@ -510,6 +580,28 @@ struct Schedule {
       for (int i = 0; i <= std::min(h->M, srfmg::kCoarseMaxLevels - 1); ++i) cops.L[i] = h->L[i];
       cops_top = 0;
       cops_bytes = 0;
+      // resident buffers: the arrays of the tiny (CTA-0) levels, smallest first, within the
+      // shared-memory budget
+      cops.nres = 0;
+      cops.res_total = 0;
+      if (h->cexec_res)
+        for (int l = 0; l <= std::min(h->M, srfmg::kCoarseMaxLevels - 1); ++l) {
+          const Lvl& L = h->L[l];
+          if (dd(l) || !srfmg::coarse_level_tiny(L)) continue;
+          const LevelBufs& bb = h->B[l];
+          const void* bufs[4] = {bb.u[0], bb.u[1], bb.rhs, bb.t};
+          for (const void* b : bufs) {
+            const int ne = (int)((L.ss * L.nsegs + 31) / 32 * 32);
+            if (!b || cops.nres == srfmg::kCoarseMaxRes ||
+                cops.res_total + ne > srfmg::kCoarseMaxResElems * 8 / (int)sizeof(T))
+              continue;
+            cops.res_g[cops.nres] = (const T*)b;
+            cops.res_n[cops.nres] = (int)(L.ss * L.nsegs);
+            cops.res_off[cops.nres] = cops.res_total;
+            cops.res_total += ne;
+            cops.nres++;
+          }
+        }
     }
     cops.op[cops.n] = o;
     // tiny: every level the operation touches fits one CTA
@@ -593,7 +685,7 @@ struct Schedule {
     const CellCounts& c = h->cells[l];
     // the fused pass marches z inside a CTA: use it only when segments x bands fill the
     // GPU; tiny levels are latency-bound and run faster as z-chunked step kernels
-    if (deg == 2 && h->fused && !L.st27 && L.nlg == 0.0 &&
+    if (deg == 2 && l > h->T && h->fused && !L.st27 && L.nlg == 0.0 &&
         (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
         tma_rhs_ok(b) && srfmg::cheb2_fused_ok<T>(L)) {
       // both sweeps in one HBM pass: read u, b; write u (C) and copy GSR
@@ -634,7 +726,7 @@ struct Schedule {
       if (fin) final_done = true;
       return;
     }
-    if (deg == 1 && h->fused && !L.st27 && L.nlg == 0.0 &&
+    if (deg == 1 && l > h->T && h->fused && !L.st27 && L.nlg == 0.0 &&
         (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
         tma_rhs_ok(b) && srfmg::cheb_spec_ok<T>(L)) {
       Launch g(h, st, KC_CHEB_FUSED, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
@@ -643,7 +735,7 @@ struct Schedule {
       bb.cur = 1 - bb.cur;
       return;
     }
-    if ((deg == 1 || deg == 2) && h->fused && L.st27 && L.nlg == 0.0 && tma_rhs_ok(b) &&
+    if ((deg == 1 || deg == 2) && l > h->T && h->fused && L.st27 && L.nlg == 0.0 && tma_rhs_ok(b) &&
         fills(L, 10) &&
         srfmg::cheb27_fused_ok<T>(L)) {
       // 27-point operator: the whole polynomial in one TMA-fed pass (fused27.cu)
@@ -689,6 +781,7 @@ struct Schedule {
     if (cx(l)) {  // recorded for the coarse-level executor (same steps, same ping-pong)
       double rho_prev = 1.0 / h->sigma[l];
       for (int k = 0; k < deg; ++k) {
+        if (dd(l)) halo(l, L, (T*)bb.u[lat]);  // every step reads the neighbours' cells
         srfmg::COp<T> o = cop(srfmg::kCopCheb, l, l);
         o.a = (const T*)bb.u[lat];
         o.b = k == 0 ? nullptr : (const T*)bb.u[oth];
@@ -709,6 +802,7 @@ struct Schedule {
       bb.cur = lat;
       return;
     }
+    if (dd(l)) halo(l, L, (T*)bb.u[lat]);
     {
       Launch g(h, st, KC_CHEB, l, w * (3.0 * c.compute + 2.0 * (c.cg - c.compute)));
       srfmg::launch_cheb_step<T>(L, (const T*)bb.u[lat], nullptr, b, (T*)bb.u[oth], 0.0,
@@ -718,6 +812,7 @@ struct Schedule {
     double rho_prev = 1.0 / h->sigma[l];
     for (int k = 1; k < deg; ++k) {
       const double rho = 1.0 / (2.0 * h->sigma[l] - rho_prev);
+      if (dd(l)) halo(l, L, (T*)bb.u[lat]);
       {
         Launch g(h, st, KC_CHEB, l, w * 4.0 * c.compute);
         srfmg::launch_cheb_step<T>(L, (const T*)bb.u[lat], (const T*)bb.u[oth], b,
@@ -749,106 +844,239 @@ struct Schedule {
 
   void prolong(int l, int add) {
     const CellCounts& c = h->cells[l];
+    // a decomposed coarse level: the interpolation reads one ghost layer of the source (the
+    // neighbours' cells).  The correction's source is w - t, formed on the block and then
+    // exchanged (t is snapshotted on the block only); P(d - 0) == P(w - t) cell for cell
+    const bool dwt = dd(l - 1) && add && l - 1 < h->T;
+    if (dd(l - 1)) {
+      if (l - 1 == h->T) {
+        footprint_T(add != 0);  // k = 1: w - t (or u) with the footprint ghosts
+      } else if (dwt) {
+        const Lvl& Lc = h->L[l - 1];
+        {
+          Launch g(h, st, KC_PROLONG, l - 1, 0.0);
+          srfmg::launch_block_diff<T>(Lc, U(l - 1), (const T*)h->B[l - 1].t, Lc,
+                                      (T*)h->B[l - 1].dwt, st);
+        }
+        halo(l - 1, Lc, (T*)h->B[l - 1].dwt);
+      } else {
+        halo_u(l - 1);  // Pi reads u
+      }
+    }
+    const T* wsrc = dwt ? (const T*)h->B[l - 1].dwt : U(l - 1);
+    const T* tsrc = dwt ? (const T*)h->zT2 : (const T*)h->B[l - 1].t;
+    // the k = 1 source of a decomposed level T: the footprint copy, P(d - 0) == P(w - t)
+    const bool fp = dd(l - 1) && l - 1 == h->T;
     if (cx(l) && cx(l - 1)) {
       srfmg::COp<T> o = cop(srfmg::kCopProlong, l, l - 1);
       o.flag = add;
-      o.a = U(l - 1);
-      o.b = (const T*)h->B[l - 1].t;
+      o.a = wsrc;
+      o.b = tsrc;
       o.c = U(l);
+      if (fp) {  // (an SR level is never an executor level; kept for completeness)
+        h->sticky = SR_ERR_UNSUPPORTED_CONFIG;
+        h->err = "executor interpolation from the footprint copy";
+      }
       emit(o, w * (add ? 2.0 : 1.0) * c.cg);
       return;
     }
+    const Lvl& Lc = fp ? h->LT2 : h->L[l - 1];
+    const T* wc = fp ? (const T*)h->wT2 : wsrc;
+    const T* tc = fp ? (const T*)h->zT2 : tsrc;
     Launch g(h, st, KC_PROLONG, l,
              w * (add ? 2.0 : 1.0) * c.cg + w * (add ? 2.0 : 1.0) * h->cells[l - 1].cg / 8.0);
     if (h->fused && (h->force || (srfmg::prolong_tma_ok<T>(h->L[l], h->L[l - 1]) &&
                                   h->L[l].E[1] >= h->fused_min_e)))
-      srfmg::launch_prolong_tma<T>(h->L[l], U(l), h->L[l - 1], U(l - 1), (const T*)h->B[l - 1].t,
-                                   add, st);
+      srfmg::launch_prolong_tma<T>(h->L[l], U(l), Lc, wc, tc, add, st);
     else
-      srfmg::launch_prolong<T>(h->L[l], U(l), h->L[l - 1], U(l - 1), (const T*)h->B[l - 1].t, add,
-                               st);
+      srfmg::launch_prolong<T>(h->L[l], U(l), Lc, wc, tc, add, st);
   }
 
   // FMG entry Pi + S^1 (alpha = 1) in one TMA pass (pset.cu), on the levels the fused
-  // Chebyshev pass takes (enough segments x bands to fill the GPU)
+  // Chebyshev pass takes (enough segments x bands to fill the GPU).  The choice uses the
+  // single-GPU shape of the coarse level, so every partition makes the same one.
   bool pset1_on(int l, const View<T>& b) {
     const Lvl& L = h->L[l];
-    return h->pset1 && h->fused && h->d.alpha == 1 && !cx(l) && !L.st27 && L.nlg == 0.0 &&
-           b.global && tma_rhs_ok(b) &&
+    return h->pset1 && h->fused && h->d.alpha == 1 && l > h->T && !cx(l) && !L.st27 &&
+           L.nlg == 0.0 && b.global && tma_rhs_ok(b) &&
            (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
-           srfmg::pset1_fused_ok<T>(L, h->L[l - 1], 1);
+           srfmg::pset1_fused_ok<T>(L, glob(l - 1), 1);
   }
   void pset1(int l, const View<T>& b) {
     const Lvl& L = h->L[l];
     const CellCounts& c = h->cells[l];
+    const bool fp = dd(l - 1) && l - 1 == h->T;
+    if (fp) footprint_T(false);
     // algorithmic words: u written (storage), rhs read (C), coarse u read (1/8 of storage)
     Launch g(h, st, KC_PASS_ENTRY, l, w * (c.cg + c.compute + h->cells[l - 1].cg / 8.0));
     LevelBufs& bb = h->B[l];
-    srfmg::launch_pset1_fused<T>(L, h->L[l - 1], U(l - 1), (T*)bb.u[bb.cur], frhs(b),
-                                 1.0 / h->theta[l], st);  // (pset1_on checked the fit)
+    const bool ok = srfmg::launch_pset1_fused<T>(L, fp ? h->LT2 : h->L[l - 1],
+                                                 fp ? (const T*)h->wT2 : U(l - 1),
+                                                 (T*)bb.u[bb.cur], frhs(b), 1.0 / h->theta[l], st);
+    if (!ok) {  // (pset1_on checked the single-GPU fit; a block never needs more)
+      h->sticky = SR_ERR_UNSUPPORTED_CONFIG;
+      h->err = "fused FMG entry: no instantiation for this rank's level-T block";
+    }
   }
 
-  // ---- multi-GPU exchanges: every rank owns a block of level T; an
-  // all-gather assembles the full level-T arrays on every rank
-  void rank_blockT(int r, int lo[3]) const {
-    const int c[3] = {r % h->d.pgrid[0], (r / h->d.pgrid[0]) % h->d.pgrid[1],
-                      r / (h->d.pgrid[0] * h->d.pgrid[1])};
-    for (int i = 0; i < 3; ++i) lo[i] = c[i] * h->blkT_n[i];
+  // ---- multi-GPU.  Levels A < l <= T are decomposed: the rank holds its
+  // block of Omega_l with a ghost ring that a halo exchange refreshes before every operator
+  // application.  Level A is agglomerated: its blocks are all-gathered into a global array on
+  // every rank, and the levels <= A are solved redundantly.
+  bool dd(int l) const { return h->world > 1 && l > h->A && l <= h->T; }
+  int rank_of(const int c[3]) const {
+    return c[0] + h->d.pgrid[0] * (c[1] + h->d.pgrid[1] * c[2]);
   }
-  // fields: (base, sy, sz) strided arrays holding level T (index = global cell)
-  void exchange(int nf, T* const* base, const long long* sy, const long long* sz,
-                const int* own_lo) {
+  // halo exchange of a decomposed level's array `base` (storage layout L, ghost width
+  // g = L.J + 1): three phases x, y, z; phase d sends the g boundary planes of the block to
+  // the two neighbours in d and receives their planes into the ghost ring.  A phase covers
+  // the ghost cells of the dimensions already exchanged, so edges and corners arrive too
+  // (the trilinear interpolation reads them).  One NCCL group per phase.
+  void halo(int lvl, const Lvl& L, T* base) {
     flush();
-    const long long nb = (long long)h->blkT_n[0] * h->blkT_n[1] * h->blkT_n[2];
+    if (h->trace) fprintf(stderr, "sr_fmg[rank %d]: halo level %d (width %d)\n", h->rank, lvl, L.J + 1);
+    const int g = L.J + 1;
+    T* snd = (T*)h->hsend;
+    T* rcv = (T*)h->hrecv;
+    for (int d = 0; d < 3; ++d) {
+      const bool lo_nb = h->coord[d] > 0, hi_nb = h->coord[d] < h->d.pgrid[d] - 1;
+      if (!lo_nb && !hi_nb) continue;
+      int lo[3], n[3];
+      for (int e = 0; e < 3; ++e) {
+        lo[e] = e < d ? 0 : g;
+        n[e] = e < d ? L.E[e] : L.S[e];
+      }
+      n[d] = g;
+      const long long cnt = (long long)n[0] * n[1] * n[2];
+      const size_t bytes = (size_t)cnt * sizeof(T);
+      Xfer xs[4];
+      int nx = 0;
+      int c[3] = {h->coord[0], h->coord[1], h->coord[2]};
+      if (lo_nb) {
+        lo[d] = g;
+        srfmg::launch_box_copy<T>(base, L.py, L.pz, lo, n, snd, 1, st);
+        c[d] = h->coord[d] - 1;
+        xs[nx++] = Xfer{rank_of(c), 0, snd, bytes};
+        xs[nx++] = Xfer{rank_of(c), 1, rcv, bytes};
+      }
+      if (hi_nb) {
+        lo[d] = L.S[d];
+        srfmg::launch_box_copy<T>(base, L.py, L.pz, lo, n, snd + cnt, 1, st);
+        c[d] = h->coord[d] + 1;
+        xs[nx++] = Xfer{rank_of(c), 0, snd + cnt, bytes};
+        xs[nx++] = Xfer{rank_of(c), 1, rcv + cnt, bytes};
+      }
+      const sr_status_t r = h->comm->group(h, xs, nx, st);
+      if (r != SR_OK) h->sticky = r;
+      h->comm_calls[lvl]++;
+      h->exch++;
+      if (lo_nb) {
+        lo[d] = 0;
+        srfmg::launch_box_copy<T>(base, L.py, L.pz, lo, n, rcv, 0, st);
+      }
+      if (hi_nb) {
+        lo[d] = g + L.S[d];
+        srfmg::launch_box_copy<T>(base, L.py, L.pz, lo, n, rcv + cnt, 0, st);
+      }
+      h->launches += 2 * ((lo_nb ? 1 : 0) + (hi_nb ? 1 : 0));
+    }
+  }
+  void halo_u(int l) { halo(l, h->L[l], U(l)); }
+
+  // all-gather of the rank blocks of level lvl: field k of this rank's block is read at
+  // slo[k] (local coordinates) of (sbase, ssy, ssz) and every rank's block is written at its
+  // global origin into the global array (dbase, dsy, dsz)
+  void gather(int lvl, int nf, T* const* sbase, const long long* ssy, const long long* ssz,
+              const int (*slo)[3], T* const* dbase, const long long* dsy, const long long* dsz) {
+    flush();
+    if (h->trace) fprintf(stderr, "sr_fmg[rank %d]: all-gather level %d\n", h->rank, lvl);
+    int nb3[3];
+    for (int i = 0; i < 3; ++i) nb3[i] = h->blk_n[i] >> (h->M - lvl);
+    const long long nb = (long long)nb3[0] * nb3[1] * nb3[2];
     T* snd = (T*)h->xsend;
     T* rcv = (T*)h->xrecv;
     for (int k = 0; k < nf; ++k)
-      srfmg::launch_box_copy<T>(base[k], sy[k], sz[k], own_lo, h->blkT_n, snd + k * nb, 1, st);
-    h->launches += nf;
+      srfmg::launch_box_copy<T>(sbase[k], ssy[k], ssz[k], slo[k], nb3, snd + k * nb, 1, st);
     const sr_status_t r = h->comm->allgather(h, snd, rcv, (size_t)nf * nb * sizeof(T), st);
     if (r != SR_OK) h->sticky = r;
+    h->comm_calls[lvl]++;
     h->exch++;
+    h->launches += nf;
     for (int q = 0; q < h->world; ++q) {
-      if (q == h->rank) continue;
+      const int c[3] = {q % h->d.pgrid[0], (q / h->d.pgrid[0]) % h->d.pgrid[1],
+                        q / (h->d.pgrid[0] * h->d.pgrid[1])};
       int lo[3];
-      rank_blockT(q, lo);
+      for (int i = 0; i < 3; ++i) lo[i] = c[i] * nb3[i];
+      if (q == h->rank && sbase[0] == dbase[0]) continue;  // already in place
       for (int k = 0; k < nf; ++k)
-        srfmg::launch_box_copy<T>(base[k], sy[k], sz[k], lo, h->blkT_n, rcv + (q * nf + k) * nb, 0,
+        srfmg::launch_box_copy<T>(dbase[k], dsy[k], dsz[k], lo, nb3, rcv + (q * nf + k) * nb, 0,
                                   st);
       h->launches += nf;
     }
   }
-  void exchange_fT() {  // the rank's block of f_T (interior of its haloed local f_T)
-    flush();
-    const int HT = h->H[h->T];
-    const auto& d = h->fdim[h->T];
-    const int own[3] = {HT, HT, HT};
-    const long long nb = (long long)h->blkT_n[0] * h->blkT_n[1] * h->blkT_n[2];
-    T* snd = (T*)h->xsend;
-    T* rcv = (T*)h->xrecv;
-    srfmg::launch_box_copy<T>((T*)h->B[h->T].floc, d[0], (long long)d[0] * d[1], own, h->blkT_n,
-                              snd, 1, st);
-    const sr_status_t r = h->comm->allgather(h, snd, rcv, (size_t)nb * sizeof(T), st);
-    if (r != SR_OK) h->sticky = r;
-    h->exch++;
-    const Lvl& LT = h->L[h->T];
-    for (int q = 0; q < h->world; ++q) {
-      int lo[3];
-      rank_blockT(q, lo);
-      srfmg::launch_box_copy<T>((T*)h->B[h->T].fpyr, LT.N[0], (long long)LT.N[0] * LT.N[1], lo,
-                                h->blkT_n, rcv + q * nb, 0, st);
-    }
-    h->launches += 1 + h->world;
+  // u_A and R_A: the blocks written by this rank's restriction into the global level-A
+  // arrays (k = 1 restriction when A = T, else the restriction from the decomposed A + 1)
+  void gather_uR() {
+    const int a = h->A;
+    const Lvl& LA = h->L[a];
+    T* base[2] = {U(a) + LA.pz + LA.py + 1, (T*)h->B[a].rhs + LA.pz + LA.py + 1};
+    const long long sy[2] = {LA.py, LA.py}, sz[2] = {LA.pz, LA.pz};
+    int lo[2][3];
+    for (int i = 0; i < 3; ++i) lo[0][i] = lo[1][i] = h->blk_lo[i] >> (h->M - a);
+    gather(a, 2, base, sy, sz, lo, base, sy, sz);
   }
-  void exchange_uT() {  // u_T and R_T blocks written by this rank's k = 1 restriction
-    const Lvl& LT = h->L[h->T];
-    T* base[2] = {U(h->T) + LT.pz + LT.py + 1, (T*)h->B[h->T].rhs + LT.pz + LT.py + 1};
-    const long long sy[2] = {LT.py, LT.py}, sz[2] = {LT.pz, LT.pz};
-    exchange(2, base, sy, sz, h->blkT_lo);
+  // f_A: this rank's block (the interior of the haloed local f_T when A = T, else the part of
+  // the global f_A its block pyramid wrote), all-gathered into the global f_A
+  void gather_f() {
+    const int a = h->A;
+    const Lvl& LA = h->L[a];
+    T* dst[1] = {(T*)h->B[a].fpyr};
+    const long long dsy[1] = {LA.N[0]}, dsz[1] = {(long long)LA.N[0] * LA.N[1]};
+    if (a == h->T) {
+      const int HT = h->H[h->T];
+      const auto& d = h->fdim[h->T];
+      T* src[1] = {(T*)h->B[h->T].floc};
+      const long long ssy[1] = {d[0]}, ssz[1] = {(long long)d[0] * d[1]};
+      const int lo[1][3] = {{HT, HT, HT}};
+      gather(a, 1, src, ssy, ssz, lo, dst, dsy, dsz);
+    } else {
+      int lo[1][3];
+      for (int i = 0; i < 3; ++i) lo[0][i] = h->blk_lo[i] >> (h->M - a);
+      gather(a, 1, dst, dsy, dsz, lo, dst, dsy, dsz);
+    }
+  }
+  // the k = 1 footprint of a decomposed level T (R15: grow(V_T^p, ceil(J/2) + 1)) on the
+  // wider-ghosted copy LT2: w - t for the correction (t = the zero array), u for the
+  // interpolation; the same values the single-GPU kernels read from the global level T
+  void footprint_T(bool diff) {
+    const int t = h->T;
+    {
+      Launch g(h, st, KC_PROLONG, t, 0.0);
+      srfmg::launch_block_diff<T>(h->L[t], U(t), diff ? (const T*)h->B[t].t : nullptr, h->LT2,
+                                  (T*)h->wT2, st);
+    }
+    halo(t, h->LT2, (T*)h->wT2);
+  }
+  // single-GPU shape of a conventional level: the kernel choices are made on it, so every
+  // partition runs the same kernels (R25)
+  Lvl glob(int l) const {
+    Lvl L = h->L[l];
+    if (l > h->T) return L;
+    for (int i = 0; i < 3; ++i) {
+      L.S[i] = L.N[i];
+      L.so[i] = 0;
+      L.E[i] = L.N[i] + 2;
+    }
+    const int pm = 32 / (int)sizeof(T);
+    L.py = (L.E[0] + pm - 1) / pm * pm;
+    L.pz = (long long)L.py * L.E[1];
+    L.ss = (L.pz * L.E[2] + 31) / 32 * 32;
+    return L;
   }
 
   void restrict_std(int l, View<T> b) {
     const int jr = jr_for(l);
+    if (dd(l)) halo_u(l);  // the residual reads the neighbours' cells
     if (cx(l) && cx(l - 1)) {
       srfmg::COp<T> o = cop(srfmg::kCopRestrict, l, l - 1);
       o.a = U(l);
@@ -869,8 +1097,8 @@ struct Schedule {
     // R goes to the level's rres buffer when its tau rides in the next pass (that pass
     // writes rhs while neighbouring bands still read R)
     T* rc = tau_fuse_ok(l - 1) ? (T*)h->B[l - 1].rres : (T*)h->B[l - 1].rhs;
-    if (L.st27 && L.nlg == 0.0 && h->fused && tma_rhs_ok(b) && srfmg::cheb27_fused_ok<T>(L) &&
-        fills(L, 10)) {
+    if (l > h->T && L.st27 && L.nlg == 0.0 && h->fused && tma_rhs_ok(b) &&
+        srfmg::cheb27_fused_ok<T>(L) && fills(L, 10)) {
       // 27-point: TMA-fed residual pass into the free ping-pong buffer, then the averages
       T* scratch = (T*)h->B[l].u[1 - h->B[l].cur];
       // f-visit: R = f_{l-1} - avg8(A u) from the R6 pyramid, f_l not streamed
@@ -907,6 +1135,7 @@ struct Schedule {
     if (L.st27)  // the 27-point pass (fused27.cu) under the conditions cheb() uses
       return base && fills(L, 10) &&
              srfmg::cheb27_fused_ok<T>(L);
+    if (seg_on(lc)) return base;  // the segment-resident down pass forms the tau
     return base &&
            (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
            srfmg::cheb2_fused_ok<T>(L) && srfmg::cheb_spec_ok<T>(L);
@@ -915,12 +1144,89 @@ struct Schedule {
   // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors.
   // entry = the FMG visit of level l (fig:fmg L139-141 / fig:fmgsr L221-223): Pi and S^alpha
   // run first, fused with the V-cycle's first half where a pass exists.
+  // segment-resident half visits (seg.cu) on the small SR levels below M, for F(1,2,2): the
+  // choice depends on the level's segment shape only (every partition makes it alike)
+  bool seg_on(int l) const {
+    const Lvl& L = h->L[l];
+    return h->seg && h->fused && l > h->T && l < h->M && h->d.alpha == 1 && h->d.nu1 == 2 &&
+           h->d.nu2 == 2 && srfmg::seg_ok<T>(L);
+  }
+  // the k = 1 coarse source of the segment passes: the level-T array, or the footprint
+  // copy of a decomposed level T (filled by the caller)
+  const Lvl& seg_coarse(int l) const {
+    return (dd(l - 1) && l - 1 == h->T) ? h->LT2 : h->L[l - 1];
+  }
+  void seg_down(int l, const View<T>& b, bool entry) {
+    const Lvl& L = h->L[l];
+    LevelBufs& bb = h->B[l];
+    const CellCounts& c = h->cells[l];
+    // FMG entry at k = 1: the interpolation source u_T is shared by all segments while the
+    // same launch restricts into it, so the pass reads a copy (the footprint copy, with the
+    // neighbours' ghosts when level T is decomposed)
+    const bool cp = entry && l - 1 == h->T;
+    if (cp) {
+      if (dd(l - 1)) {
+        footprint_T(false);
+      } else {
+        Launch g(h, st, KC_PROLONG, l - 1, 0.0);
+        srfmg::launch_block_diff<T>(h->L[l - 1], U(l - 1), nullptr, h->LT2, (T*)h->wT2, st);
+      }
+    }
+    const bool tau = pend_tau == l;
+    const int jt = pend_jr;
+    pend_tau = -1;
+    const double rho0 = 1.0 / h->sigma[l];
+    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
+    T* rc = tau_fuse_ok(l - 1) ? (T*)h->B[l - 1].rres : (T*)h->B[l - 1].rhs;
+    {
+      // words: u read (or coarse 1/8), b read, u written, rhs + t written (tau), coarse 2/8
+      Launch g(h, st, KC_CHEB_FUSED, l,
+               w * ((entry ? c.cg / 8.0 : c.storage) + c.storage + c.storage +
+                    (tau ? 2.0 * c.storage : 0.0) + c.compute / 4.0));
+      const bool ok = srfmg::launch_seg_down<T>(
+          L, h->L[l - 1], cp ? h->LT2 : h->L[l - 1], (const T*)bb.u[bb.cur],
+          (T*)bb.u[1 - bb.cur], frhs(b), tau ? (const T*)bb.rres : nullptr, (T*)bb.rhs, (T*)bb.t,
+          jt, cp ? (const T*)h->wT2 : U(l - 1), U(l - 1), rc, jr_for(l), entry ? 1 : 0,
+          1.0 / h->theta[l], 1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
+      if (!ok) {
+        h->sticky = SR_ERR_UNSUPPORTED_CONFIG;
+        h->err = "segment-resident pass: no instantiation for this level";
+      }
+    }
+    bb.cur = 1 - bb.cur;
+  }
+  void seg_up(int l, const View<T>& b) {
+    const Lvl& L = h->L[l];
+    LevelBufs& bb = h->B[l];
+    const CellCounts& c = h->cells[l];
+    const bool fp = dd(l - 1) && l - 1 == h->T;
+    if (fp) footprint_T(true);
+    else if (dd(l - 1)) halo_u(l - 1);
+    const double rho0 = 1.0 / h->sigma[l];
+    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
+    {
+      Launch g(h, st, KC_PROLONG, l, w * (c.storage + c.storage + c.storage + c.cg / 4.0));
+      const bool ok = srfmg::launch_seg_up<T>(
+          L, seg_coarse(l), (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b),
+          fp ? (const T*)h->wT2 : U(l - 1), fp ? (const T*)h->zT2 : (const T*)h->B[l - 1].t,
+          1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
+      if (!ok) {
+        h->sticky = SR_ERR_UNSUPPORTED_CONFIG;
+        h->err = "segment-resident pass: no instantiation for this level";
+      }
+    }
+    bb.cur = 1 - bb.cur;
+  }
+
   void vcycle(int l, View<T> b, bool entry = false) {
     if (l == 0) {  // L120-121: exact solve
       coarsest(b);
       return;
     }
-    if (entry) {
+    const bool sg = seg_on(l);
+    if (sg) {
+      seg_down(l, b, entry);  // [Pi, S^1,] [tau,] S^2, r, restriction: L221-222, L232-236
+    } else if (entry) {
       if (pset1_on(l, b)) {
         pset1(l, b);                 // Pi onto C ∪ GSR and S^1, one pass
       } else {
@@ -928,10 +1234,16 @@ struct Schedule {
         cheb(l, h->d.alpha, b);      // S^alpha
       }
     }
-    cheb(l, h->d.nu1, b);  // L112 / L232
-    restrict_std(l, b);
+    if (!sg) {
+      cheb(l, h->d.nu1, b);  // L112 / L232
+      restrict_std(l, b);
+    }
     const int jr = jr_for(l);
-    if (h->world > 1 && l - 1 == h->T) exchange_uT();  // a8: level-T hand-off (R16)
+    // a8: the level-T hand-off (R16).  Multi-GPU: the blocks of the agglomeration level A
+    // (T, or below a decomposed T) are all-gathered; a decomposed coarse level refreshes its
+    // ghost ring for the tau instead
+    if (h->world > 1 && l - 1 == h->A) gather_uR();
+    if (dd(l - 1)) halo_u(l - 1);
     if (cx(l - 1)) {  // conventional level: F = V = Omega (jr = 0)
       srfmg::COp<T> o = cop(srfmg::kCopTau, l - 1, l - 1);
       o.a = U(l - 1);
@@ -945,6 +1257,10 @@ struct Schedule {
       tau_std(l - 1, jr);  // L116-117 / L234-236
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
+    if (sg) {
+      seg_up(l, b);  // L241-242
+      return;
+    }
     prolong(l, 1);                    // L118 / L241
     cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
   }
@@ -967,8 +1283,22 @@ struct Schedule {
       Launch g(h, st, KC_PYRAMID, l, w * (double)d[0] * d[1] * d[2] * (1.0 + 1.0 / 8));
       srfmg::launch_pyramid<T>(src, d[0], d[1], d[2], dst, st);
     }
-    if (h->world > 1) exchange_fT();
-    for (int l = h->T; l >= 1; --l) {
+    if (h->world > 1) {
+      // decomposed levels: each rank averages its own block (f_T from the haloed local
+      // f_T) down to level A, whose blocks are then all-gathered (the rank's own part is
+      // written straight into the global f_A)
+      for (int l = h->T; l > h->A; --l) {
+        int lo[3], n[3];
+        for (int i = 0; i < 3; ++i) {
+          n[i] = h->blk_n[i] >> (M - l + 1);
+          lo[i] = h->blk_lo[i] >> (M - l + 1);
+        }
+        Launch g(h, st, KC_PYRAMID, l, w * (double)n[0] * n[1] * n[2] * 9.0);
+        srfmg::launch_pyramid_box<T>(fview(l), fview(l - 1), lo, n, st);
+      }
+      gather_f();
+    }
+    for (int l = h->A; l >= 1; --l) {
       const Lvl& L = h->L[l];
       if (l < M && cx(l)) {
         srfmg::COp<T> o = cop(srfmg::kCopPyramid, l, l - 1);
@@ -997,6 +1327,7 @@ struct Schedule {
 sr_status_t enqueue_solve(sr_fmg* h, const void* f, void* u, cudaStream_t st) {
   h->launches = 0;
   h->exch = 0;
+  std::fill(h->comm_calls.begin(), h->comm_calls.end(), 0LL);
   h->prof_used = 0;
   for (int l = 0; l <= h->M; ++l) h->B[l].cur = 0;
   if (h->esize == 8) {
@@ -1030,6 +1361,10 @@ struct NcclApi {
   int (*getUniqueId)(UniqueId*) = nullptr;
   int (*commInitRank)(CommT*, int, UniqueId, int) = nullptr;
   int (*allGather)(const void*, void*, size_t, int, CommT, cudaStream_t) = nullptr;
+  int (*send)(const void*, size_t, int, int, CommT, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, CommT, cudaStream_t) = nullptr;
+  int (*groupStart)() = nullptr;
+  int (*groupEnd)() = nullptr;
   int (*commDestroy)(CommT) = nullptr;
   const char* (*getErrorString)(int) = nullptr;
   bool ok = false;
@@ -1058,9 +1393,16 @@ NcclApi& nccl() {
         (int (*)(NcclApi::CommT*, int, NcclApi::UniqueId, int))dlsym(lib, "ncclCommInitRank");
     api.allGather = (int (*)(const void*, void*, size_t, int, NcclApi::CommT, cudaStream_t))dlsym(
         lib, "ncclAllGather");
+    api.send = (int (*)(const void*, size_t, int, int, NcclApi::CommT, cudaStream_t))dlsym(
+        lib, "ncclSend");
+    api.recv = (int (*)(void*, size_t, int, int, NcclApi::CommT, cudaStream_t))dlsym(
+        lib, "ncclRecv");
+    api.groupStart = (int (*)())dlsym(lib, "ncclGroupStart");
+    api.groupEnd = (int (*)())dlsym(lib, "ncclGroupEnd");
     api.commDestroy = (int (*)(NcclApi::CommT))dlsym(lib, "ncclCommDestroy");
     api.getErrorString = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
-    api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy;
+    api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.send && api.recv &&
+             api.groupStart && api.groupEnd && api.commDestroy;
     if (!api.ok) api.why = "libnccl.so.2 lacks the expected symbols";
   }
   return api;
@@ -1078,33 +1420,96 @@ struct NcclComm : Comm {
                                                 (nccl().getErrorString ? nccl().getErrorString(r) : "error"));
     return SR_OK;
   }
+  // one halo phase: the sends and receives with the (up to two) neighbours of one dimension
+  // in one NCCL group (matched per peer in issue order; one transfer per direction and pair)
+  sr_status_t group(sr_fmg* h, const Xfer* xs, int n, cudaStream_t st) override {
+    NcclApi& api = nccl();
+    int r = api.groupStart();
+    for (int i = 0; i < n && r == 0; ++i)
+      r = xs[i].recv ? api.recv(xs[i].buf, xs[i].bytes, /*ncclInt8*/ 0, xs[i].peer, comm, st)
+                     : api.send(xs[i].buf, xs[i].bytes, 0, xs[i].peer, comm, st);
+    const int e = api.groupEnd();
+    if (r == 0) r = e;
+    if (r != 0) return fail(h, SR_ERR_NCCL, std::string("ncclSend/ncclRecv: ") +
+                                                (api.getErrorString ? api.getErrorString(r) : "error"));
+    return SR_OK;
+  }
 };
 
-// ---- test replay store: the blocks of every rank, per exchange, shared in one process
-struct ReplayStore {
+// ---- test backend: the ranks of one process (one host thread each, all on one GPU) pass
+// their messages through host memory.  Every transfer is synchronous on the host (device ->
+// host copy, mailbox, host -> device copy); a receive blocks until its sender has posted, so
+// the ranks must run concurrently.  No kernel of one rank ever waits for another rank.
+struct HostStore {
   int world;
-  std::map<long long, std::vector<std::vector<char>>> blocks;  // exchange -> rank -> bytes
+  std::mutex mu;
+  std::condition_variable cv;
+  std::map<std::pair<int, int>, std::deque<std::vector<char>>> box;  // (src, dst) -> FIFO
+  bool aborted = false;
 };
 
-struct ReplayComm : Comm {
-  ReplayStore* store = nullptr;
+struct HostComm : Comm {
+  HostStore* store = nullptr;
+  sr_status_t post(sr_fmg* h, int peer, const void* buf, size_t bytes, cudaStream_t st) {
+    std::vector<char> msg(bytes);
+    CU(h, cudaMemcpyAsync(msg.data(), buf, bytes, cudaMemcpyDeviceToHost, st));
+    CU(h, cudaStreamSynchronize(st));
+    {
+      std::lock_guard<std::mutex> g(store->mu);
+      store->box[{h->rank, peer}].push_back(std::move(msg));
+    }
+    store->cv.notify_all();
+    return SR_OK;
+  }
+  sr_status_t take(sr_fmg* h, int peer, void* buf, size_t bytes, cudaStream_t st) {
+    std::vector<char> msg;
+    {
+      std::unique_lock<std::mutex> g(store->mu);
+      auto& q = store->box[{peer, h->rank}];
+      const bool got = store->cv.wait_for(g, std::chrono::seconds(30),
+                                          [&] { return !q.empty() || store->aborted; });
+      if (!got || q.empty()) {
+        store->aborted = true;
+        store->cv.notify_all();
+        return fail(h, SR_ERR_NCCL, "host store: no message from rank " + std::to_string(peer));
+      }
+      msg = std::move(q.front());
+      q.pop_front();
+    }
+    if (msg.size() != bytes) return fail(h, SR_ERR_NCCL, "host store: message size mismatch");
+    CU(h, cudaMemcpyAsync(buf, msg.data(), bytes, cudaMemcpyHostToDevice, st));
+    CU(h, cudaStreamSynchronize(st));
+    return SR_OK;
+  }
   sr_status_t allgather(sr_fmg* h, const void* send, void* recv, size_t bytes,
                         cudaStream_t st) override {
-    if (!store) return fail(h, SR_ERR_INVALID_ARGUMENT, "replay comm without a store");
-    auto& row = store->blocks[h->exch];
-    if ((int)row.size() != store->world) row.assign(store->world, std::vector<char>());
-    std::vector<char> mine(bytes);
-    CU(h, cudaMemcpyAsync(mine.data(), send, bytes, cudaMemcpyDeviceToHost, st));
-    CU(h, cudaStreamSynchronize(st));
-    row[h->rank] = mine;
-    for (int q = 0; q < store->world; ++q) {
-      char* dst = (char*)recv + (size_t)q * bytes;
-      if (row[q].size() == bytes)
-        CU(h, cudaMemcpyAsync(dst, row[q].data(), bytes, cudaMemcpyHostToDevice, st));
-      else
-        CU(h, cudaMemsetAsync(dst, 0, bytes, st));
-    }
-    CU(h, cudaStreamSynchronize(st));
+    if (!store) return fail(h, SR_ERR_INVALID_ARGUMENT, "host comm without a store");
+    for (int q = 0; q < store->world; ++q)
+      if (q != h->rank) {
+        sr_status_t r = post(h, q, send, bytes, st);
+        if (r != SR_OK) return r;
+      }
+    CU(h, cudaMemcpyAsync((char*)recv + (size_t)h->rank * bytes, send, bytes,
+                          cudaMemcpyDeviceToDevice, st));
+    for (int q = 0; q < store->world; ++q)
+      if (q != h->rank) {
+        sr_status_t r = take(h, q, (char*)recv + (size_t)q * bytes, bytes, st);
+        if (r != SR_OK) return r;
+      }
+    return SR_OK;
+  }
+  sr_status_t group(sr_fmg* h, const Xfer* xs, int n, cudaStream_t st) override {
+    if (!store) return fail(h, SR_ERR_INVALID_ARGUMENT, "host comm without a store");
+    for (int i = 0; i < n; ++i)  // all sends first: posting never blocks
+      if (!xs[i].recv) {
+        sr_status_t r = post(h, xs[i].peer, xs[i].buf, xs[i].bytes, st);
+        if (r != SR_OK) return r;
+      }
+    for (int i = 0; i < n; ++i)
+      if (xs[i].recv) {
+        sr_status_t r = take(h, xs[i].peer, xs[i].buf, xs[i].bytes, st);
+        if (r != SR_OK) return r;
+      }
     return SR_OK;
   }
 };
@@ -1141,9 +1546,14 @@ void free_all(sr_fmg* h) {
     dev_free(h, b.t);
     dev_free(h, b.fpyr);
     dev_free(h, b.floc);
+    dev_free(h, b.dwt);
   }
   dev_free(h, h->xsend);
   dev_free(h, h->xrecv);
+  dev_free(h, h->wT2);
+  dev_free(h, h->zT2);
+  dev_free(h, h->hsend);
+  dev_free(h, h->hrecv);
   delete h->comm;
   h->comm = nullptr;
   dev_free(h, h->ainv);
@@ -1234,6 +1644,8 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   }
   const char* sd = std::getenv("SR_FMG_SYNC");
   h->sync_debug = sd && sd[0] == '1';
+  const char* tr = std::getenv("SR_FMG_TRACE");
+  h->trace = tr && tr[0] == '1';
   const char* fu = std::getenv("SR_FMG_FUSED");
   h->fused = !(fu && fu[0] == '0');
   const char* ff = std::getenv("SR_FMG_FORCE_FUSED");
@@ -1241,7 +1653,9 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_FUSED_MIN_E")) h->fused_min_e = std::atoi(e);
   const char* ce = std::getenv("SR_FMG_CEXEC");
   h->cexec = !(ce && ce[0] == '0');
+  if (const char* e = std::getenv("SR_FMG_CEXEC_RES")) h->cexec_res = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_SEG")) h->seg = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_TAU_FUSE")) h->tau_fuse = std::atoi(e) != 0;
   if (d->device >= 0) {
@@ -1267,8 +1681,11 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
     if (l < h->M) {
       ok = ok && alloc(&h->B[l].rhs, bytes) && alloc(&h->B[l].t, bytes);
       if (l > h->T && h->tau_fuse) ok = ok && alloc(&h->B[l].rres, bytes);
-      if (h->world == 1 || l <= h->T)
+      if (h->world == 1 || l <= h->A)
         ok = ok && alloc(&h->B[l].fpyr, (size_t)L.N[0] * L.N[1] * L.N[2] * h->esize);
+      else if (l < h->T)  // decomposed level below T: the rank's block of f_l, and w - t
+        ok = ok && alloc(&h->B[l].fpyr, (size_t)L.S[0] * L.S[1] * L.S[2] * h->esize) &&
+             alloc(&h->B[l].dwt, bytes);
       if (h->world > 1 && l >= h->T) {
         const auto& fd = h->fdim[l];
         ok = ok && alloc(&h->B[l].floc, (size_t)fd[0] * fd[1] * fd[2] * h->esize);
@@ -1276,9 +1693,25 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
     }
   }
   if (h->world > 1) {
-    h->xbytes = (size_t)2 * h->blkT_n[0] * h->blkT_n[1] * h->blkT_n[2] * h->esize;
+    // all-gather of the agglomeration level's blocks (u and R), and halo staging for the
+    // decomposed levels: both sides of the largest face slab, ghost width deep
+    long long nbA = 1;
+    for (int i = 0; i < 3; ++i) nbA *= h->blk_n[i] >> (h->M - h->A);
+    h->xbytes = (size_t)2 * nbA * h->esize;
     ok = ok && alloc(&h->xsend, h->xbytes) && alloc(&h->xrecv, h->xbytes * h->world);
+    long long face = 0;
+    auto slab = [&](const Lvl& L) {
+      for (int i = 0; i < 3; ++i)
+        face = std::max(face, 2LL * (L.J + 1) * L.E[(i + 1) % 3] * L.E[(i + 2) % 3]);
+    };
+    for (int l = h->A + 1; l <= h->T; ++l) slab(h->L[l]);
+    if (h->A < h->T) slab(h->LT2);
+    h->hbytes = (size_t)std::max(face, 1LL) * h->esize;
+    if (h->A < h->T) ok = ok && alloc(&h->hsend, h->hbytes) && alloc(&h->hrecv, h->hbytes);
   }
+  if (h->K > 0)  // copy of level T for the first SR level (footprint / entry source)
+    ok = ok && alloc(&h->wT2, (size_t)h->LT2.ss * h->esize) &&
+         alloc(&h->zT2, (size_t)h->LT2.ss * h->esize);
   std::vector<double> inv = coarsest_inverse(h->L[0]);
   const size_t n0sq = inv.size();
   ok = ok && alloc(&h->ainv, n0sq * h->esize);
@@ -1299,7 +1732,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   }
   if (h->world > 1) {
     if (d->comm == 1) {
-      h->comm = new ReplayComm();
+      h->comm = new HostComm();
       h->d.use_graph = 0;  // host round trips inside the solve
     } else {
       NcclApi& api = nccl();
@@ -1529,6 +1962,7 @@ sr_status_t sr_fmg_partition(const sr_fmg_desc_t* d, sr_fmg_partition_t* out) {
     out->level_T_n[i] = tmp.blkT_n[i];
   }
   out->f_halo = tmp.H[tmp.M];
+  out->level_A = tmp.A;
   return SR_OK;
 }
 
@@ -1543,19 +1977,19 @@ sr_status_t sr_fmg_nccl_unique_id(void* out128) {
   return SR_OK;
 }
 
-void* sr_fmg_replay_store_create(int32_t world) {
-  ReplayStore* s = new ReplayStore();
+void* sr_fmg_host_store_create(int32_t world) {
+  HostStore* s = new HostStore();
   s->world = world;
   return s;
 }
 
-void sr_fmg_replay_store_destroy(void* store) { delete (ReplayStore*)store; }
+void sr_fmg_host_store_destroy(void* store) { delete (HostStore*)store; }
 
-sr_status_t sr_fmg_set_replay(sr_fmg_t* h, void* store) {
+sr_status_t sr_fmg_set_host_store(sr_fmg_t* h, void* store) {
   if (!h || !store) return fail(h, SR_ERR_INVALID_ARGUMENT, "NULL argument");
-  ReplayComm* c = dynamic_cast<ReplayComm*>(h->comm);
+  HostComm* c = dynamic_cast<HostComm*>(h->comm);
   if (!c) return fail(h, SR_ERR_INVALID_ARGUMENT, "handle was not created with comm = 1");
-  c->store = (ReplayStore*)store;
+  c->store = (HostStore*)store;
   return SR_OK;
 }
 
@@ -1605,7 +2039,12 @@ sr_status_t sr_fmg_get_info(const sr_fmg_t* h, sr_fmg_info_t* info) {
     info->f_dims[i] = h->fdim[h->M][i];
   }
   info->f_halo = h->H[h->M];
-  info->exchanges_per_solve = h->world > 1 ? 1 + h->K : 0;
+  info->exchanges_per_solve = h->exch_per_solve;
+  info->level_A = h->A;
+  for (int l = 0; l <= h->M; ++l) {
+    info->dd[l] = (h->world > 1 && l > h->A && l <= h->T) ? 1 : 0;
+    info->comm_calls[l] = h->comm_calls[l];
+  }
   info->alg_bytes_per_solve = alg_bytes(h);
   return SR_OK;
 }

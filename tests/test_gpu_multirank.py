@@ -1,11 +1,15 @@
 """The multi-GPU path of the library on ONE GPU (test comm backend, desc.comm = 1).
 
-Every rank's handle lives in this process; its all-gathers record / replay per-rank blocks
-through a shared host store, and solving all ranks exchanges_per_solve + 1 times makes every
-exchange consistent.  Each rank's output block must equal the single-GPU solve BITWISE (R25:
-SR segments are independent and the coarse levels are solved redundantly), and the oracle
-to the parity tolerance.  Only the NCCL call itself is not exercised here.
+Every rank's handle lives in this process and runs its solve in a thread of its own; the
+all-gathers and halo slabs go through a host store (sr_fmg_host_store_create), so no kernel
+of one rank ever waits for another.  Each rank's output block must equal the single-GPU
+solve BITWISE (R25: SR segments are independent, the decomposed coarse levels exchange
+their ghost rings before every operator application, the agglomerated levels are solved
+redundantly), and the oracle to the parity tolerance.  Only the NCCL call itself is not
+exercised here.
 """
+import threading
+
 import numpy as np
 import pytest
 
@@ -17,45 +21,86 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("needs CUDA", allow_module_level=True)
 
-from paper_1406_7808_b200 import ReplayStore, Solver  # noqa: E402
+from paper_1406_7808_b200 import HostStore, Solver  # noqa: E402
 from tests.gpu_helpers import rel_l2  # noqa: E402
 
+
+def run_ranks(n, M, seg, J, K, pgrid, f, dtype="f64", dd_min=0, solves=1, **kw):
+    """Solve f on every rank of pgrid concurrently (one thread per rank); returns the
+    handles (open) and each rank's output block of the last solve."""
+    world = int(np.prod(pgrid))
+    store = HostStore(world)
+    ranks = [Solver(n, M, seg=seg, buffer=J, K=K, dtype=dtype, world=world, rank=r, pgrid=pgrid,
+                    host_store=store, dd_min=dd_min, **kw) for r in range(world)]
+    fl = [torch.from_numpy(s.local_f(f)).cuda() for s in ranks]
+    outs, errs = [None] * world, []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(solves):
+                    u = ranks[r].solve(fl[r])
+                st.synchronize()
+            outs[r] = u.cpu().numpy()
+        except Exception as e:  # reported in the main thread
+            errs.append((r, e))
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    return ranks, outs, store
+
+
 CASES = [
-    ("2x1x1", (64, 64, 64), 5, 8, 2, 2, (2, 1, 1), "f64"),
-    ("2x2x1", (64, 64, 64), 5, 16, 2, 3, (2, 2, 1), "f64"),
-    ("2x2x2", (64, 64, 64), 5, 8, 2, 2, (2, 2, 2), "f64"),
-    ("4x1x2-f32", (128, 64, 64), 5, 16, 1, 2, (4, 1, 2), "f32"),
-    # 32^3 and 64^3 segments: the fused FMG entry (pset.cu), the tau inside the coarse
-    # pre-smoothing and the pyramid restriction run with nonzero segment / f offsets per rank
-    ("2x1x1-S32", (128, 64, 64), 5, 32, 2, 2, (2, 1, 1), "f64"),
-    ("1x2x2-S64", (128, 128, 128), 6, 64, 2, 2, (1, 2, 2), "f64"),
-    ("2x1x1-S64-f32", (128, 64, 64), 5, 64, 2, 2, (2, 1, 1), "f32"),
+    # name, n, M, seg, J, K, pgrid, dtype, dd_min
+    ("2x1x1", (64, 64, 64), 5, 8, 2, 2, (2, 1, 1), "f64", 0),
+    ("2x2x1", (64, 64, 64), 5, 16, 2, 3, (2, 2, 1), "f64", 0),
+    ("2x2x2", (64, 64, 64), 5, 8, 2, 2, (2, 2, 2), "f64", 0),
+    ("4x1x2-f32", (128, 64, 64), 5, 16, 1, 2, (4, 1, 2), "f32", 0),
+    ("2x1x1-S32", (128, 64, 64), 5, 32, 2, 2, (2, 1, 1), "f64", 0),
+    ("1x2x2-S64", (128, 128, 128), 6, 64, 2, 2, (1, 2, 2), "f64", 0),
+    ("2x1x1-S64-f32", (128, 64, 64), 5, 64, 2, 2, (2, 1, 1), "f32", 0),
+    # decomposed coarse levels (halo exchange) below T, agglomeration further down
+    ("dd-2x1x1", (64, 64, 64), 5, 16, 2, 2, (2, 1, 1), "f64", 4),
+    ("dd-2x2x2", (128, 128, 128), 6, 32, 2, 2, (2, 2, 2), "f64", 4),
+    ("dd-2x2x1-J1", (128, 128, 64), 5, 32, 1, 2, (2, 2, 1), "f64", 2),
+    ("dd-4x1x1-f32", (128, 32, 32), 5, 16, 2, 2, (4, 1, 1), "f32", 2),
+    ("dd-1x2x2-K1", (64, 128, 128), 6, 32, 2, 1, (1, 2, 2), "f64", 4),
+    ("dd-2x2x2-J3", (64, 64, 64), 5, 16, 3, 2, (2, 2, 2), "f64", 2),
 ]
 
 
+@pytest.mark.timeout(150)
 @pytest.mark.parametrize("force", ["0", "1"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_replayed_ranks_equal_single_gpu(case, force, monkeypatch):
-    name, n, M, seg, J, K, pgrid, dt = case
+def test_ranks_equal_single_gpu(case, force, monkeypatch):
+    name, n, M, seg, J, K, pgrid, dt, dd_min = case
     monkeypatch.setenv("SR_FMG_FORCE_FUSED", force)
     npd = np.float64 if dt == "f64" else np.float32
     f = W.make_rhs("manufactured+noise", n).astype(npd)
     with Solver(n, M, seg=seg, buffer=J, K=K, dtype=dt) as s1:
         single = s1.solve(torch.from_numpy(f).cuda()).cpu().numpy()
-    world = int(np.prod(pgrid))
-    store = ReplayStore(world)
-    ranks = [Solver(n, M, seg=seg, buffer=J, K=K, dtype=dt, world=world, rank=r, pgrid=pgrid,
-                    replay_store=store) for r in range(world)]
-    fl = [torch.from_numpy(s.local_f(f)).cuda() for s in ranks]
-    E = ranks[0].exchanges_per_solve
-    assert E == K + 1
-    outs = None
-    for _ in range(E + 1):
-        outs = [s.solve(fl[r]).cpu().numpy() for r, s in enumerate(ranks)]
+    ranks, outs, store = run_ranks(n, M, seg, J, K, pgrid, f, dt, dd_min, solves=2)
+    T, A = ranks[0].T, ranks[0].level_A
+    if dd_min:
+        assert A < T, (name, A, T)               # the case decomposes at least level T
+        assert ranks[0].dd_levels() == list(range(A + 1, T + 1))
     for r, s in enumerate(ranks):
         # kernel choices follow the global level shape, so every rank runs the single-GPU
-        # schedule on its segments: bitwise (R25)
+        # arithmetic on its segments and blocks: bitwise (R25)
         assert np.array_equal(outs[r], s.block_of(single)), (name, r)
+        calls = s.comm_calls()
+        # zero collectives on the SR levels (PAPER.md:44, 444-449); the decomposed levels
+        # exchange halos, the agglomeration level gathers
+        assert all(calls[l] == 0 for l in range(T + 1, s.M + 1)), calls
+        assert calls[A] >= 1 and all(calls[l] == 0 for l in range(A)), calls
+        assert all(calls[l] > 0 for l in range(A + 1, T + 1)), calls
+        assert s.exchanges_per_solve == sum(calls)
     if dt == "f64":
         ref = O.solve(f.astype(np.float64), O.Config(n=n, M=M, seg=seg, buffer=J, K=K))
         full = np.zeros_like(ref)
@@ -67,19 +112,17 @@ def test_replayed_ranks_equal_single_gpu(case, force, monkeypatch):
         s.close()
 
 
+@pytest.mark.timeout(150)
 def test_multirank_local_f_uses_halo_only():
     # f outside a rank's haloed block must not matter: perturb it and get the same block
-    n, M, seg, J, K, pgrid = (64, 64, 64), 5, 8, 2, 2, (2, 1, 1)
+    n, M, seg, J, K, pgrid = (64, 64, 64), 5, 16, 2, 2, (2, 1, 1)
     f = W.make_rhs("manufactured+noise", n)
-    store = ReplayStore(2)
-    ranks = [Solver(n, M, seg=seg, buffer=J, K=K, world=2, rank=r, pgrid=pgrid,
-                    replay_store=store) for r in range(2)]
-    fl = [s.local_f(f) for s in ranks]
-    assert ranks[0].f_halo > 0 and fl[0].shape == ranks[0].f_shape
-    ft = [torch.from_numpy(x).cuda() for x in fl]
-    for _ in range(ranks[0].exchanges_per_solve + 1):
-        outs = [s.solve(ft[r]).cpu().numpy() for r, s in enumerate(ranks)]
     with Solver(n, M, seg=seg, buffer=J, K=K) as s1:
         single = s1.solve(torch.from_numpy(f).cuda()).cpu().numpy()
-    for r, s in enumerate(ranks):
-        assert np.array_equal(outs[r], s.block_of(single)), r
+    for dd_min in (0, 4):
+        ranks, outs, _ = run_ranks(n, M, seg, J, K, pgrid, f, dd_min=dd_min)
+        fl = ranks[0].local_f(f)
+        assert ranks[0].f_halo > 0 and fl.shape == ranks[0].f_shape
+        for r, s in enumerate(ranks):
+            assert np.array_equal(outs[r], s.block_of(single)), (dd_min, r)
+            s.close()

@@ -473,33 +473,56 @@ def test_c5_shapes_at_256_match_oracle(case):
     assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
 
 
-def test_c4_two_ranks_full_size_equal_single_gpu():
+@pytest.mark.parametrize("dd_min", [0, 1 << 20])
+def test_c4_two_ranks_full_size_equal_single_gpu(dd_min):
     # BASELINE configs[3] (C4) at 2 GPUs: global 1024 x 512 x 512, h = 1/512, R = (2,1,1),
     # manufactured f, 64^3 segments, J = 2, K = 4, M = 8 (coarsest 4 x 2 x 2).  Both ranks run
-    # on this GPU through the replay backend (no rank waits on another); each rank's block
-    # must equal the single-GPU solve of the same global problem.
-    from paper_1406_7808_b200 import ReplayStore
+    # on this GPU, one host thread each, through the host-store backend (no rank waits on
+    # another inside a kernel); each rank's block must equal the single-GPU solve of the same
+    # global problem.  dd_min = 0 (default): level T (32^3 per rank) is domain-decomposed with
+    # halo exchanges and level 3 is gathered; 2^20: level T itself is gathered.
+    import threading
+
+    from paper_1406_7808_b200 import HostStore
     n, M, seg, J, K, pgrid, h = (1024, 512, 512), 8, 64, 2, 4, (2, 1, 1), 1.0 / 512
     R = W.extents(n, h)
     with Solver(n, M, seg=seg, buffer=J, K=K, h=h) as s1:
         f = torch.from_numpy(W.manufactured_f_block(h, R, (0, 0, 0), n)).cuda()
         single = s1.solve(f)
         del f
-    store = ReplayStore(2)
+    store = HostStore(2)
     ranks = [Solver(n, M, seg=seg, buffer=J, K=K, h=h, world=2, rank=r, pgrid=pgrid,
-                    replay_store=store) for r in range(2)]
+                    host_store=store, dd_min=dd_min) for r in range(2)]
+    assert (ranks[0].level_A < ranks[0].T) == (dd_min == 0)
     fl = []
     for s in ranks:
         lo = [s.block_lo[d] - s.f_halo for d in range(3)]
         dims = [s.block_n[d] + 2 * s.f_halo for d in range(3)]
         fl.append(torch.from_numpy(W.manufactured_f_block(h, R, lo, dims)).cuda())
-    outs = None
-    for _ in range(ranks[0].exchanges_per_solve + 1):
-        outs = [s.solve(fl[r]) for r, s in enumerate(ranks)]
+    outs, errs = [None, None], []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                outs[r] = ranks[r].solve(fl[r])
+            st.synchronize()
+        except Exception as e:
+            errs.append((r, e))
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
     for r, s in enumerate(ranks):
         lo, nb = s.block_lo, s.block_n
         blk = single[lo[2]:lo[2] + nb[2], lo[1]:lo[1] + nb[1], lo[0]:lo[0] + nb[0]]
         assert torch.equal(outs[r], blk), r      # bitwise (R25)
+        calls = s.comm_calls()
+        assert all(calls[l] == 0 for l in range(s.T + 1, s.M + 1)), calls  # SR levels
     for s in ranks:
         s.close()
 

@@ -1,8 +1,10 @@
-"""Multi-rank path on CPU (gloo, world size 2): the product's partition arithmetic drives a
-decomposed oracle solve -- each rank runs only its own segments and the ranks all-gather
-their level-T blocks at the k = 1 hand-off (the library's exchange points).
-The result must equal the single-process solve BITWISE (R25): SR segments are independent
- and the coarse levels are solved redundantly."""
+"""Multi-rank path on CPU (gloo): the product's partition arithmetic drives a decomposed
+oracle solve -- each rank runs only its own segments; the conventional levels A < l <= T
+are domain-decomposed with a halo exchange before every operator application, and level A
+is all-gathered (the library's exchange points; tests/dd_oracle.py).  The
+result must equal the single-process solve BITWISE (R25): SR segments are independent
+(PAPER.md:44), a decomposed V-cycle replicates the serial one and the
+agglomerated levels are solved redundantly."""
 import os
 import socket
 
@@ -26,41 +28,32 @@ def _free_port():
 
 
 CASES = {
-    "x-split": dict(n=(32, 16, 16), M=3, seg=8, buffer=2, K=2, pgrid=(2, 1, 1)),
-    "y-split": dict(n=(16, 32, 16), M=3, seg=8, buffer=1, K=1, pgrid=(1, 2, 1)),
+    # agglomeration at T (dd_min larger than the level-T block)
+    "x-split": dict(n=(32, 16, 16), M=3, seg=8, buffer=2, K=2, pgrid=(2, 1, 1), dd_min=1 << 20),
+    "y-split": dict(n=(16, 32, 16), M=3, seg=8, buffer=1, K=1, pgrid=(1, 2, 1), dd_min=1 << 20),
+    # decomposed conventional levels with halo exchanges
+    "dd-x": dict(n=(64, 32, 32), M=5, seg=16, buffer=2, K=2, pgrid=(2, 1, 1), dd_min=4),
+    "dd-xy-J3": dict(n=(32, 32, 16), M=4, seg=8, buffer=3, K=1, pgrid=(2, 2, 1), dd_min=2),
+    "dd-xyz": dict(n=(32, 32, 32), M=4, seg=8, buffer=2, K=1, pgrid=(2, 2, 2), dd_min=2),
 }
 
 
 def _worker(rank, world, port, case, outq):
     from paper_1406_7808_b200 import partition
+    from tests.dd_oracle import DDOracle
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     c = CASES[case]
-    part = partition(c["n"], c["M"], c["seg"], c["buffer"], c["K"], world, rank, c["pgrid"])
+    part = partition(c["n"], c["M"], c["seg"], c["buffer"], c["K"], world, rank, c["pgrid"],
+                     dd_min=c["dd_min"])
     f = W.make_rhs("manufactured+noise", c["n"])
-    o = O.Oracle(O.Config(n=c["n"], M=c["M"], seg=c["seg"], buffer=c["buffer"], K=c["K"]))
-    # own segments (array order (z, y, x) vs the partition's (x, y, z))
-    lo = [part["coord"][d] * part["segs_per_rank"][d] for d in range(3)]
-    hi = [lo[d] + part["segs_per_rank"][d] for d in range(3)]
-    o.segs = [p for p in o.segs if all(lo[d] <= p[2 - d] < hi[d] for d in range(3))]
-    Tn = part["level_T_n"]
-    Tlo_all = [None] * world
-    dist.all_gather_object(Tlo_all, part["level_T_lo"])
-
-    def exchange(uT, RT):
-        for fld in (uT, RT):
-            mine = torch.from_numpy(np.ascontiguousarray(
-                fld[_box(part["level_T_lo"], Tn)]))
-            got = [torch.empty_like(mine) for _ in range(world)]
-            dist.all_gather(got, mine)
-            for q in range(world):
-                fld[_box(Tlo_all[q], Tn)] = got[q].numpy()
-
-    o.exchange_T = exchange
+    o = DDOracle(O.Config(n=c["n"], M=c["M"], seg=c["seg"], buffer=c["buffer"], K=c["K"]),
+                 part, c["pgrid"])
     u = o.solve(f)
     bl, bn = part["block_lo"], part["block_n"]
-    outq.put((rank, u[bl[2]:bl[2] + bn[2], bl[1]:bl[1] + bn[1], bl[0]:bl[0] + bn[0]].copy()))
+    outq.put((rank, (u[bl[2]:bl[2] + bn[2], bl[1]:bl[1] + bn[1], bl[0]:bl[0] + bn[0]].copy(),
+                     part["level_A"], o.n_exchanges)))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -88,11 +81,16 @@ def test_decomposed_solve_equals_single_process(case):
     f = W.make_rhs("manufactured+noise", c["n"])
     ref = O.solve(f, O.Config(n=c["n"], M=c["M"], seg=c["seg"], buffer=c["buffer"], K=c["K"]))
     from paper_1406_7808_b200 import partition
+    T = c["M"] - c["K"]
     for r in range(world):
-        part = partition(c["n"], c["M"], c["seg"], c["buffer"], c["K"], world, r, c["pgrid"])
+        part = partition(c["n"], c["M"], c["seg"], c["buffer"], c["K"], world, r, c["pgrid"],
+                         dd_min=c["dd_min"])
         bl, bn = part["block_lo"], part["block_n"]
         blk = ref[bl[2]:bl[2] + bn[2], bl[1]:bl[1] + bn[1], bl[0]:bl[0] + bn[0]]
-        assert np.array_equal(res[r], blk), (case, r)
+        u, A, nex = res[r]
+        assert np.array_equal(u, blk), (case, r)
+        assert (A < T) == case.startswith("dd"), (case, A, T)
+        assert nex > 0
 
 
 def test_partition_blocks_tile_the_grid():
