@@ -153,7 +153,10 @@ __device__ void op_restrict(const Lvl& Lf, const Lvl& Lc, const COp<T>& o, int t
   const int ch = tid & 7;
   const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
   const int fo[3] = {goff(Lf, 0), goff(Lf, 1), goff(Lf, 2)};
-  for (int base = tid - ch; base < 8 * n; base += nth) {  // warp-uniform trip count
+  // whole warps run the loop (the shuffles need all 32 lanes), so the bound is 8 n rounded
+  // up to a multiple of 32; lanes past the last coarse cell compute a copy of it
+  const int nl = (8 * n + 31) & ~31;
+  for (int base = tid - ch; base < nl; base += nth) {  // warp-uniform trip count
     const int c = base >> 3;
     const bool ok = c < n;
     int X, Y, Z;
@@ -253,9 +256,6 @@ __global__ void __launch_bounds__(kThreadsC, 1)
   // indexed kernel-parameter reads go through the constant cache and miss (~1 us per op)
   __shared__ COp<T> sop[kCoarseMaxOps];
   __shared__ Lvl sL[kCoarseMaxLevels];
-  extern __shared__ __align__(16) unsigned char dyn[];
-  T* dres = reinterpret_cast<T*>(dyn);  // resident buffers (used in CTA 0 only)
-  const int rank = (int)cl.block_rank();
   {
     const int* src = reinterpret_cast<const int*>(ol.op);
     int* dst = reinterpret_cast<int*>(sop);
@@ -264,32 +264,9 @@ __global__ void __launch_bounds__(kThreadsC, 1)
     const int* ls = reinterpret_cast<const int*>(ol.L);
     int* ld = reinterpret_cast<int*>(sL);
     for (int k = threadIdx.x; k < (int)(sizeof(sL) / sizeof(int)); k += blockDim.x) ld[k] = ls[k];
-    if (rank == 0)  // the tiny levels' arrays into shared memory
-      for (int r = 0; r < ol.nres; ++r)
-        for (int e = threadIdx.x; e < ol.res_n[r]; e += blockDim.x)
-          dres[ol.res_off[r] + e] = ol.res_g[r][e];
   }
   __syncthreads();
-  if (ol.nres > 0) {
-    // redirect every operation's pointers into a resident buffer to CTA 0's copy (a
-    // distributed-shared-memory address on the other CTAs)
-    auto rm = [&](const T* p) -> T* {
-      for (int r = 0; r < ol.nres; ++r)
-        if (p >= ol.res_g[r] && p < ol.res_g[r] + ol.res_n[r])
-          return cl.map_shared_rank(dres + ol.res_off[r], 0) + (p - ol.res_g[r]);
-      return const_cast<T*>(p);
-    };
-    for (int i = threadIdx.x; i < ol.n; i += blockDim.x) {
-      COp<T>& o = sop[i];
-      o.a = rm(o.a);
-      o.b = rm(o.b);
-      o.c = rm(o.c);
-      o.d = rm(o.d);
-      if (!o.v.global) o.v.p = rm(o.v.p);
-    }
-    __syncthreads();
-  }
-  cl.sync();  // CTA 0's copies are in place before any operation reads them
+  const int rank = (int)cl.block_rank();
   if (ol.prof && rank == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -360,11 +337,6 @@ __global__ void __launch_bounds__(kThreadsC, 1)
       ol.prof[i + 1] = t;
     }
   }
-  // (the last operation ended with a cluster barrier: every write to CTA 0's copies is done)
-  if (rank == 0)
-    for (int r = 0; r < ol.nres; ++r)
-      for (int e = threadIdx.x; e < ol.res_n[r]; e += blockDim.x)
-        const_cast<T*>(ol.res_g[r])[e] = dres[ol.res_off[r] + e];
 }
 
 }  // namespace
@@ -386,13 +358,9 @@ void launch_coarse_exec(const COpList<T>& ops, cudaStream_t st) {
   if (ops.n <= 0) return;
   // (per launch: the attribute is per device, and a process may drive several)
   cudaFuncSetAttribute(k_coarse_exec<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  const size_t dyn = (size_t)ops.res_total * sizeof(T);
-  cudaFuncSetAttribute(k_coarse_exec<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(dyn, 16));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kCluster);
   cfg.blockDim = dim3(kThreadsC);
-  cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;

@@ -28,24 +28,12 @@ struct COp {
   double c0, c1;   // CHEB: c_mom, c_res
 };
 
-constexpr int kCoarseMaxRes = 16;
-constexpr int kCoarseMaxResElems = 12 * 1024;  // (96 KB of fp64)
-
 template <class T>
 struct COpList {
   int n;
   unsigned long long* prof;  // optional: %globaltimer after every operation (debug)
   Lvl L[kCoarseMaxLevels];
   COp<T> op[kCoarseMaxOps];
-  // resident buffers: the arrays of the tiny levels live in CTA 0's shared memory for the
-  // whole launch (copied in at the start, out at the end); every operation's pointers into
-  // them are redirected there (CTA 0 directly, the other CTAs through distributed shared
-  // memory), so the chains of tiny operations make no L2 round trips
-  int nres;
-  const T* res_g[kCoarseMaxRes];
-  int res_n[kCoarseMaxRes];
-  int res_off[kCoarseMaxRes];
-  int res_total;
 };
 
 // Conventional single-segment level small enough for the executor.

@@ -95,22 +95,4 @@ template <class T>
 bool launch_pset1_fused(const Lvl& L, const Lvl& Lc, const T* w, T* uout, FusedRhs<T> b,
                         double c0, cudaStream_t st);
 
-// Segment-resident half visits of the small SR levels (seg.cu; E = 14 or 22 cubic boxes):
-// one CTA per segment holds the storage box in shared memory.
-//   down: [src 1: u = Pi(w), S^1 (c1)] [R != null: tau from R (rres) -> rhs_out, t_out]
-//         S^2 (c0, cm, cr); u -> uout; r = b - A u; uc, rc = avg8 on the targets of half-
-//         width jr (0: V_T)
-//   up:   u += P(w - t); S^2; u -> uout
-template <class T>
-bool seg_ok(const Lvl& L);
-// (Lw: the layout of w for the interpolation -- Lc, or the footprint copy of level T)
-template <class T>
-bool launch_seg_down(const Lvl& L, const Lvl& Lc, const Lvl& Lw, const T* uin, T* uout,
-                     FusedRhs<T> b, const T* R, T* rhs_out, T* t_out, int jt, const T* w, T* uc,
-                     T* rc, int jr, int src, double c1, double c0, double cm, double cr,
-                     cudaStream_t st);
-template <class T>
-bool launch_seg_up(const Lvl& L, const Lvl& Lc, const T* uin, T* uout, FusedRhs<T> b, const T* w,
-                   const T* t, double c0, double cm, double cr, cudaStream_t st);
-
 }  // namespace srfmg

@@ -114,20 +114,17 @@ struct sr_fmg {
   long long hcalls = 0;
   long long launches = 0;
   bool sync_debug = false;
-  bool trace = false;  // SR_FMG_TRACE=1: print every collective (multi-rank debugging)
+  bool trace = false;  // SR_FMG_TRACE=1: print every launch, operation and collective
+  bool cexec_one = false;  // SR_FMG_CEXEC_ONE=1: one executor launch per operation (debug)
   bool fused = true;  // SR_FMG_FUSED=0 disables the fused TMA kernels
   bool force = false; // SR_FMG_FORCE_FUSED=1: use them even on levels too small to fill the GPU
   int fused_min_e = 0; // SR_FMG_FUSED_MIN_E: smallest storage extent given to the TMA kernels
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
-  bool seg = true;    // segment-resident half visits on the small SR levels (seg.cu);
-                      // SR_FMG_SEG=0 off
   bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
   bool tau_fuse = true;      // tau inside the next pre-smoothing pass; SR_FMG_TAU_FUSE=0 off
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
   // disables it.  flush_fn: enqueue the recorded operations (called before every launch)
   bool cexec = true;
-  bool cexec_res = true;  // tiny levels resident in the executor's shared memory
-                          // (SR_FMG_CEXEC_RES=0 off)
   void (*flush_fn)(void*) = nullptr;
   void* flush_ctx = nullptr;
   int prof_cls = -1, prof_level = -1;
@@ -471,6 +468,9 @@ struct Launch {
   Launch(sr_fmg* h_, cudaStream_t st_, int cls, int level, double bytes) : h(h_), st(st_) {
     if (h->flush_fn) h->flush_fn(h->flush_ctx);  // recorded coarse-level operations first
     h->launches++;
+    if (h->trace)
+      fprintf(stderr, "sr_fmg[rank %d]: launch %s level %d\n", h->rank, srfmg::kKernelNames[cls],
+              level);
     if (cls == h->prof_cls && level == h->prof_level) {
       if (h->prof_used == h->prof.size()) {
         ProfRec r{};
@@ -580,28 +580,6 @@ struct Schedule {
       for (int i = 0; i <= std::min(h->M, srfmg::kCoarseMaxLevels - 1); ++i) cops.L[i] = h->L[i];
       cops_top = 0;
       cops_bytes = 0;
-      // resident buffers: the arrays of the tiny (CTA-0) levels, smallest first, within the
-      // shared-memory budget
-      cops.nres = 0;
-      cops.res_total = 0;
-      if (h->cexec_res)
-        for (int l = 0; l <= std::min(h->M, srfmg::kCoarseMaxLevels - 1); ++l) {
-          const Lvl& L = h->L[l];
-          if (dd(l) || !srfmg::coarse_level_tiny(L)) continue;
-          const LevelBufs& bb = h->B[l];
-          const void* bufs[4] = {bb.u[0], bb.u[1], bb.rhs, bb.t};
-          for (const void* b : bufs) {
-            const int ne = (int)((L.ss * L.nsegs + 31) / 32 * 32);
-            if (!b || cops.nres == srfmg::kCoarseMaxRes ||
-                cops.res_total + ne > srfmg::kCoarseMaxResElems * 8 / (int)sizeof(T))
-              continue;
-            cops.res_g[cops.nres] = (const T*)b;
-            cops.res_n[cops.nres] = (int)(L.ss * L.nsegs);
-            cops.res_off[cops.nres] = cops.res_total;
-            cops.res_total += ne;
-            cops.nres++;
-          }
-        }
     }
     cops.op[cops.n] = o;
     // tiny: every level the operation touches fits one CTA
@@ -609,6 +587,10 @@ struct Schedule {
     cops.n++;
     cops_top = std::max(cops_top, o.lf);
     cops_bytes += bytes;
+    if (h->trace)
+      fprintf(stderr, "sr_fmg[rank %d]:   op %d code %d lf %d lc %d tiny %d\n", h->rank,
+              cops.n - 1, o.code, o.lf, o.lc, cops.op[cops.n - 1].tiny);
+    if (h->cexec_one) flush();  // debugging: one launch per operation
   }
   void flush() {
     if (cops.n == 0 || flushing) return;
@@ -1135,7 +1117,6 @@ struct Schedule {
     if (L.st27)  // the 27-point pass (fused27.cu) under the conditions cheb() uses
       return base && fills(L, 10) &&
              srfmg::cheb27_fused_ok<T>(L);
-    if (seg_on(lc)) return base;  // the segment-resident down pass forms the tau
     return base &&
            (fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e)) &&
            srfmg::cheb2_fused_ok<T>(L) && srfmg::cheb_spec_ok<T>(L);
@@ -1144,89 +1125,12 @@ struct Schedule {
   // fig:mgv (l <= T) and fig:mgvsr (l > T) are the same recursion over level descriptors.
   // entry = the FMG visit of level l (fig:fmg L139-141 / fig:fmgsr L221-223): Pi and S^alpha
   // run first, fused with the V-cycle's first half where a pass exists.
-  // segment-resident half visits (seg.cu) on the small SR levels below M, for F(1,2,2): the
-  // choice depends on the level's segment shape only (every partition makes it alike)
-  bool seg_on(int l) const {
-    const Lvl& L = h->L[l];
-    return h->seg && h->fused && l > h->T && l < h->M && h->d.alpha == 1 && h->d.nu1 == 2 &&
-           h->d.nu2 == 2 && srfmg::seg_ok<T>(L);
-  }
-  // the k = 1 coarse source of the segment passes: the level-T array, or the footprint
-  // copy of a decomposed level T (filled by the caller)
-  const Lvl& seg_coarse(int l) const {
-    return (dd(l - 1) && l - 1 == h->T) ? h->LT2 : h->L[l - 1];
-  }
-  void seg_down(int l, const View<T>& b, bool entry) {
-    const Lvl& L = h->L[l];
-    LevelBufs& bb = h->B[l];
-    const CellCounts& c = h->cells[l];
-    // FMG entry at k = 1: the interpolation source u_T is shared by all segments while the
-    // same launch restricts into it, so the pass reads a copy (the footprint copy, with the
-    // neighbours' ghosts when level T is decomposed)
-    const bool cp = entry && l - 1 == h->T;
-    if (cp) {
-      if (dd(l - 1)) {
-        footprint_T(false);
-      } else {
-        Launch g(h, st, KC_PROLONG, l - 1, 0.0);
-        srfmg::launch_block_diff<T>(h->L[l - 1], U(l - 1), nullptr, h->LT2, (T*)h->wT2, st);
-      }
-    }
-    const bool tau = pend_tau == l;
-    const int jt = pend_jr;
-    pend_tau = -1;
-    const double rho0 = 1.0 / h->sigma[l];
-    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
-    T* rc = tau_fuse_ok(l - 1) ? (T*)h->B[l - 1].rres : (T*)h->B[l - 1].rhs;
-    {
-      // words: u read (or coarse 1/8), b read, u written, rhs + t written (tau), coarse 2/8
-      Launch g(h, st, KC_CHEB_FUSED, l,
-               w * ((entry ? c.cg / 8.0 : c.storage) + c.storage + c.storage +
-                    (tau ? 2.0 * c.storage : 0.0) + c.compute / 4.0));
-      const bool ok = srfmg::launch_seg_down<T>(
-          L, h->L[l - 1], cp ? h->LT2 : h->L[l - 1], (const T*)bb.u[bb.cur],
-          (T*)bb.u[1 - bb.cur], frhs(b), tau ? (const T*)bb.rres : nullptr, (T*)bb.rhs, (T*)bb.t,
-          jt, cp ? (const T*)h->wT2 : U(l - 1), U(l - 1), rc, jr_for(l), entry ? 1 : 0,
-          1.0 / h->theta[l], 1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
-      if (!ok) {
-        h->sticky = SR_ERR_UNSUPPORTED_CONFIG;
-        h->err = "segment-resident pass: no instantiation for this level";
-      }
-    }
-    bb.cur = 1 - bb.cur;
-  }
-  void seg_up(int l, const View<T>& b) {
-    const Lvl& L = h->L[l];
-    LevelBufs& bb = h->B[l];
-    const CellCounts& c = h->cells[l];
-    const bool fp = dd(l - 1) && l - 1 == h->T;
-    if (fp) footprint_T(true);
-    else if (dd(l - 1)) halo_u(l - 1);
-    const double rho0 = 1.0 / h->sigma[l];
-    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
-    {
-      Launch g(h, st, KC_PROLONG, l, w * (c.storage + c.storage + c.storage + c.cg / 4.0));
-      const bool ok = srfmg::launch_seg_up<T>(
-          L, seg_coarse(l), (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur], frhs(b),
-          fp ? (const T*)h->wT2 : U(l - 1), fp ? (const T*)h->zT2 : (const T*)h->B[l - 1].t,
-          1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st);
-      if (!ok) {
-        h->sticky = SR_ERR_UNSUPPORTED_CONFIG;
-        h->err = "segment-resident pass: no instantiation for this level";
-      }
-    }
-    bb.cur = 1 - bb.cur;
-  }
-
   void vcycle(int l, View<T> b, bool entry = false) {
     if (l == 0) {  // L120-121: exact solve
       coarsest(b);
       return;
     }
-    const bool sg = seg_on(l);
-    if (sg) {
-      seg_down(l, b, entry);  // [Pi, S^1,] [tau,] S^2, r, restriction: L221-222, L232-236
-    } else if (entry) {
+    if (entry) {
       if (pset1_on(l, b)) {
         pset1(l, b);                 // Pi onto C ∪ GSR and S^1, one pass
       } else {
@@ -1234,10 +1138,8 @@ struct Schedule {
         cheb(l, h->d.alpha, b);      // S^alpha
       }
     }
-    if (!sg) {
-      cheb(l, h->d.nu1, b);  // L112 / L232
-      restrict_std(l, b);
-    }
+    cheb(l, h->d.nu1, b);  // L112 / L232
+    restrict_std(l, b);
     const int jr = jr_for(l);
     // a8: the level-T hand-off (R16).  Multi-GPU: the blocks of the agglomeration level A
     // (T, or below a decomposed T) are all-gathered; a decomposed coarse level refreshes its
@@ -1257,10 +1159,6 @@ struct Schedule {
       tau_std(l - 1, jr);  // L116-117 / L234-236
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
-    if (sg) {
-      seg_up(l, b);  // L241-242
-      return;
-    }
     prolong(l, 1);                    // L118 / L241
     cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
   }
@@ -1646,6 +1544,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->sync_debug = sd && sd[0] == '1';
   const char* tr = std::getenv("SR_FMG_TRACE");
   h->trace = tr && tr[0] == '1';
+  if (const char* e = std::getenv("SR_FMG_CEXEC_ONE")) h->cexec_one = e[0] == '1';
   const char* fu = std::getenv("SR_FMG_FUSED");
   h->fused = !(fu && fu[0] == '0');
   const char* ff = std::getenv("SR_FMG_FORCE_FUSED");
@@ -1653,9 +1552,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_FUSED_MIN_E")) h->fused_min_e = std::atoi(e);
   const char* ce = std::getenv("SR_FMG_CEXEC");
   h->cexec = !(ce && ce[0] == '0');
-  if (const char* e = std::getenv("SR_FMG_CEXEC_RES")) h->cexec_res = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SR_FMG_SEG")) h->seg = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_TAU_FUSE")) h->tau_fuse = std::atoi(e) != 0;
   if (d->device >= 0) {
@@ -1709,7 +1606,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
     h->hbytes = (size_t)std::max(face, 1LL) * h->esize;
     if (h->A < h->T) ok = ok && alloc(&h->hsend, h->hbytes) && alloc(&h->hrecv, h->hbytes);
   }
-  if (h->K > 0)  // copy of level T for the first SR level (footprint / entry source)
+  if (h->world > 1 && h->A < h->T)  // footprint copy of a decomposed level T
     ok = ok && alloc(&h->wT2, (size_t)h->LT2.ss * h->esize) &&
          alloc(&h->zT2, (size_t)h->LT2.ss * h->esize);
   std::vector<double> inv = coarsest_inverse(h->L[0]);

@@ -55,6 +55,10 @@ SOLVE_CASES = [
     ("C3-like-64", (64, 64, 64), 5, 8, 2, 3, "manufactured+noise"),
     ("noncubic", (64, 32, 32), 4, 16, 2, 2, "manufactured+noise"),
     ("one-seg", (32, 32, 32), 4, 32, 2, 3, "random"),
+    # thin coarsest grids (2x1x1, 1x4x1): executor operations on levels of fewer than 4
+    # cells (a restriction onto 2 coarse cells once left a warp's shuffles half-populated)
+    ("thin-2x1x1", (64, 32, 32), 5, 16, 2, 2, "manufactured+noise"),
+    ("thin-1x4x1", (32, 128, 32), 5, 16, 2, 2, "bumps"),
 ]
 
 

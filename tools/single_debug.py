@@ -1,0 +1,20 @@
+"""Single-GPU solve of one grid shape with SR_FMG_TRACE/SR_FMG_SYNC (GPU box debugging)."""
+import faulthandler
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+from paper_1406_7808_b200 import Solver  # noqa: E402
+
+n = tuple(int(v) for v in sys.argv[1].split(","))
+M, seg, K = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+faulthandler.dump_traceback_later(25, exit=True)
+f = W.make_rhs("manufactured+noise", n)
+with Solver(n, M, seg=seg, buffer=2, K=K, use_graph=False) as s:
+    u = s.solve(torch.from_numpy(f).cuda()).cpu().numpy()
+print("done", np.isfinite(u).all(), flush=True)
