@@ -371,9 +371,12 @@ def main():
                                f"({int(cells)} per GPU), M={M}, seg={seg}, buffer={buf}, "
                                f"K={K} SR levels, F(1,2,2), rhs {rhs}, {args.stencil} operator",
                    "global_cells": cells * world, "pgrid": list(P),
-                   "parallelism": (f"segment blocks pgrid {P}: SR levels without communication, "
-                                   f"{solver.exchanges_per_solve} NCCL all-gathers per solve "
-                                   "(level-T blocks), coarse levels redundant")
+                   "parallelism": (f"segment blocks pgrid {P}: SR levels without communication; "
+                                   f"conventional levels {solver.level_A + 1}..{solver.T} "
+                                   "domain-decomposed (halo exchange, grouped ncclSend/ncclRecv), "
+                                   f"level {solver.level_A} and below gathered (ncclAllGather) and "
+                                   f"solved redundantly; {solver.exchanges_per_solve} collective "
+                                   "calls per solve")
                    if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (f %.2f GB, workspace %.2f GB)"
                          % (nbytes_in / 1e9, solver.workspace_bytes / 1e9)},

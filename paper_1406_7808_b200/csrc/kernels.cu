@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restri
 // ------------------------------------------------------------------------------------
 // bc.p != null (bf is f_l and bc = f_{l-1} = avg8(f_l), the R6 pyramid): the residual
 // average is taken as avg8(b - A u) = bc - avg8(A u), so the fine b is not read at all.
-template <class T>
+template <class T, int UNR = 1>
 __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restrict__ uf,
                                                        View<T> bf, Lvl Lc, T* __restrict__ uc,
                                                        T* __restrict__ rc, int jr, int ntx,
@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restri
 #pragma unroll
       for (int j = 0; j < 4; ++j) q[k][j] = u[z + k * fpz + (j >> 1) * fpy + (j & 1)];
   }
+#pragma unroll UNR
   for (int Z = Zb; Z < Ze; ++Z) {
     const long long z0 = (long long)(2 * Z - of[2]) * fpz;
 #pragma unroll
@@ -1008,9 +1009,20 @@ void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* u
     }
     return;
   }
-  // 800k threads: 0.657 -> 0.616 ms at C3's finest level, 0.281 -> 0.247 ms at E = 38
+  // 800k threads: 0.657 -> 0.616 ms at C3's finest level, 0.281 -> 0.247 ms at E = 38.
+  // Two coarse planes per loop trip in fp32 (C3 finest 0.298 vs 0.318 ms, level 7 0.154 vs
+  // 0.168); fp64 keeps one (0.60 vs 0.43 ms unrolled: 98 registers).  SR_FMG_RESTRICT_UNROLL
+  // overrides (tuning knob)
+  static const int unr_env = [] {
+    const char* e = std::getenv("SR_FMG_RESTRICT_UNROLL");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int unr = unr_env ? unr_env : (sizeof(T) == 4 ? 2 : 1);
   const ColCfg c = col_cfg(B[0], B[1], B[2], Lf.nsegs, 800000);
-  k_restrict<T><<<c.grid, c.block, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr, c.ntx, c.zchunk, bc);
+  if (unr == 2)
+    k_restrict<T, 2><<<c.grid, c.block, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr, c.ntx, c.zchunk, bc);
+  else
+    k_restrict<T><<<c.grid, c.block, 0, st>>>(Lf, uf, bf, Lc, uc, rc, jr, c.ntx, c.zchunk, bc);
 }
 
 template <class T>

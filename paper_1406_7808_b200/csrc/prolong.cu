@@ -215,16 +215,29 @@ bool prolong_tma_ok(const Lvl& Lf, const Lvl& Lc) {
   // size picks the same kernel (R25)
   long long g = 1;
   for (int i = 0; i < 3; ++i) g *= Lf.N[i] / Lf.S[i];
-  return g * ((Lf.E[1] + 17) / 18) >= 148;
+  // one thread per row column and MAXS rows: rows up to 136 wide keep a band within the
+  // 1024-thread CTA limit (E = 262 boxes, e.g. 256^3 segments, take the column kernel)
+  return Lf.py <= 136 && g * ((Lf.E[1] + 17) / 18) >= 148;
 }
 
 template <class T>
 void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
                         cudaStream_t st) {
-  constexpr int MAXS = 3;
   // measured at C3: 18-row bands at E = 70 (0.55 ms; 10: 0.61, 24: 0.66), two 19-row bands at
-  // E = 38 (0.22 ms for the level's two launches; three of 13: 0.24)
-  const int tgt = Lf.E[1] <= 40 ? 24 : 18;
+  // E = 38 (0.22 ms for the level's two launches; three of 13: 0.24).  SR_FMG_PROLONG_MAXS
+  // (3 or 6 rows per thread) and SR_FMG_PROLONG_BH (target band height): tuning knobs
+  static const int maxs_env = [] {
+    const char* e = std::getenv("SR_FMG_PROLONG_MAXS");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int bh_env = [] {
+    const char* e = std::getenv("SR_FMG_PROLONG_BH");
+    return e ? std::atoi(e) : 0;
+  }();
+  // fp32 at E = 70: 6 rows per thread (C3 finest correction 0.383 vs 0.446 ms); fp64 and the
+  // E = 38 boxes: 3 (fp64 at 6: 0.70 vs 0.53 ms)
+  const int MAXS = maxs_env ? (maxs_env == 6 ? 6 : 3) : (sizeof(T) == 4 && Lf.E[1] > 40 ? 6 : 3);
+  const int tgt = bh_env > 0 ? bh_env : (Lf.E[1] <= 40 ? 24 : 18);
   const int nb = (Lf.E[1] + tgt - 1) / tgt;
   const int BH = (Lf.E[1] + nb - 1) / nb;
   ProlongArgs<T> a{};
@@ -241,7 +254,7 @@ void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T
   a.fstride = (BH * Lf.py + A - 1) / A * A;
   const size_t smem = (size_t)(2 * kRC * a.cstride + kRF * a.fstride) * sizeof(T) + 8 * (kRC + kRF);
   const int NT = Lf.py * ((BH + MAXS - 1) / MAXS);
-  auto kern = k_prolong_tma<T, MAXS>;
+  auto kern = MAXS == 6 ? k_prolong_tma<T, 6> : k_prolong_tma<T, 3>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<dim3(nb, Lf.nsegs), NT, smem, st>>>(a);
 }

@@ -761,3 +761,19 @@ def test_27pt_restriction_via_pyramid(monkeypatch):
     assert rel_l2(u, b) <= 1e-13, rel_l2(u, b)
     ref = O.solve(f, O.Config(n=n, M=M, seg=seg, buffer=J, K=K, h=h, stencil="27pt"))
     assert rel_l2(u, ref) <= TOL64, rel_l2(u, ref)
+
+
+@pytest.mark.parametrize("stencil", ["7pt", "27pt"])
+def test_large_segments_match_unfused(stencil, monkeypatch):
+    # 256^3 segments (storage boxes E = 262 > 256: past the fused kernels' row limits) -- the
+    # launch configuration must fall back to the column kernels, not fail at solve time
+    n, M, seg, J, K = (512, 256, 256), 7, 256, 2, 2
+    h = 1.0 / 256
+    f = torch.from_numpy(W.manufactured_f(n, h)).cuda()
+    with Solver(n, M, seg=seg, buffer=J, K=K, h=h, stencil=stencil) as s:
+        a = s.solve(f)
+    monkeypatch.setenv("SR_FMG_FUSED", "0")
+    with Solver(n, M, seg=seg, buffer=J, K=K, h=h, stencil=stencil) as s:
+        b = s.solve(f)
+    assert torch.isfinite(a).all()
+    assert float(torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)) <= 1e-12

@@ -3,9 +3,11 @@ with the paper's 27-point operator on Omega = [0,2]x[0,1]^2 (R = (2,1,1)), the m
 u = prod(x_i^4 - R_i^2 x_i^2), F(1,2,2), a 4x2x2 "process" grid = 4x2x2 SR segments of
 N_K = pN0V 2^K cells each (GPU box; writes profiles/r2_paper_tables.json).
 
-Only the configurations that fit one GPU are run: Table 1 column log2 pN0V = 2 (K = 4:
-256x128x128) for every (A, B) and column 3 (K = 5: 1024x512x512) for B = 0; Table 2 for
-pN0V = 4, 8; Table 3 (MBS, J_1 = 4, K = 4) for pN0V = 2 .. 16.  The coarsest grid is 2R =
+Run: Table 1 column log2 pN0V = 2 (K = 4: 256x128x128) for every (A, B); Table 2 for pN0V =
+4 (512x256x256); Table 3 (MBS, J_1 = 4, K = 4) for pN0V = 2, 4, 8 (up to 512x256x256).  The
+other columns need 1024x512x512 with 256^3 segments or more (E > 256: not supported by
+this build's 27-point kernels) or 4096x2048x2048.  Also: the Chebyshev interval's effect
+on e_r (the paper does not state it; reading R28 uses [1/3, 1] lambda_max).  The coarsest grid is 2R =
 4x2x2 cells (the paper's M = K + log2 pN0V + 2, would give
 1x0.5x0.5 -- a garbled formula).
 """
@@ -42,7 +44,7 @@ def grid(pn0v, K):
 _cache = {}
 
 
-def errors(pn0v, K, sched=None, conv=False):
+def errors(pn0v, K, sched=None, conv=False, cheb=None):
     n, M, NK, h = grid(pn0v, K)
     key = (n, M)
     if key not in _cache:
@@ -51,7 +53,7 @@ def errors(pn0v, K, sched=None, conv=False):
         _cache[key] = (torch.from_numpy(W.manufactured_f(n, h)).cuda(),
                        torch.from_numpy(W.manufactured_u(n, h)).cuda())
     f, ue = _cache[key]
-    kw = dict(h=h, stencil="27pt")
+    kw = dict(h=h, stencil="27pt", cheb=cheb)
     if conv:
         s = Solver(n, M, K=0, **kw)
     else:
@@ -66,25 +68,31 @@ def main():
     out = {"operator": "27-point (R28), Omega = [0,2]x[0,1]^2, 4x2x2 segments, F(1,2,2)",
            "coarsest": "4x2x2 (2R)", "table1": {}, "table2": {}, "table3": {}}
     t0 = time.time()
-    for pn0v, K, col in ((4, 4, 2), (8, 5, 1)):
+    for pn0v, K, col in ((4, 4, 2),):
         ec = errors(pn0v, K, conv=True)
         for (A, B), pv in PAPER_T1.items():
-            if col == 1 and B > 0:
-                continue
             es = errors(pn0v, K, sched=(A, B))
             out["table1"][f"A{A}_B{B}_pN0V{pn0v}_K{K}"] = {
                 "e_sr": es, "e_conv": ec, "e_r": es / ec, "paper": pv[col]}
             print(A, B, pn0v, K, es / ec, pv[col], flush=True)
-    for pn0v in (4, 8):
+    for pn0v in (4,):
         ec = errors(pn0v, 5, conv=True)
         es = errors(pn0v, 5, sched=(8, 0))
         out["table2"][f"pN0V{pn0v}"] = {"e_r": es / ec, "paper": PAPER_T2[pn0v]}
         print("T2", pn0v, es / ec, PAPER_T2[pn0v], flush=True)
-    for pn0v in (2, 4, 8, 16):
+    for pn0v in (2, 4, 8):
         ec = errors(pn0v, 4, conv=True)
         es = errors(pn0v, 4, sched=("mbs", 4))
         out["table3"][f"pN0V{pn0v}"] = {"e_r": es / ec, "paper": PAPER_T3[pn0v]}
         print("T3", pn0v, es / ec, PAPER_T3[pn0v], flush=True)
+    out["interval"] = {}
+    for lo, hi in ((1 / 3, 1.0), (1 / 4, 1.0), (1 / 2, 1.0), (0.1, 1.1), (0.2, 1.2)):
+        ec = errors(4, 4, conv=True, cheb=(lo, hi))
+        row = {"e_conv": ec}
+        for A in (2, 8):
+            row[f"e_r_A{A}_B0"] = errors(4, 4, sched=(A, 0), cheb=(lo, hi)) / ec
+        out["interval"][f"{lo:.3g}-{hi:.3g}"] = row
+        print("interval", lo, hi, row, flush=True)
     out["seconds"] = time.time() - t0
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "gpurun_out", "r2_paper_tables.json"), "w"), indent=1)
