@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(Lvl L, const T* __restri
 // ------------------------------------------------------------------------------------
 // bc.p != null (bf is f_l and bc = f_{l-1} = avg8(f_l), the R6 pyramid): the residual
 // average is taken as avg8(b - A u) = bc - avg8(A u), so the fine b is not read at all.
+// (launch bounds without a minimum block count: the compiler's own register choice, 64 in
+// fp64, measured best -- an explicit minimum of 1 lets it take 96 and the finest-level
+// restriction slows from 0.43 to 0.64 ms; 4 (64, with spills) 0.48; 5 (48) 0.56 ms)
 template <class T, int UNR = 1>
 __global__ void __launch_bounds__(kThreads) k_restrict(Lvl Lf, const T* __restrict__ uf,
                                                        View<T> bf, Lvl Lc, T* __restrict__ uc,
