@@ -46,7 +46,7 @@ ORACLE_SAMPLE = dict(n=(128, 128, 128), M=6, seg=16, buffer=2, K=4, rhs="manufac
 PGRID = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 # kernel classes (sr_fmg_kernel_name) that can dominate the finest level: the roofline line
 # reports the one with the largest device time per solve
-KC_CANDIDATES = (1, 3, 7, 8)  # k_restrict, k_prolong, k_cheb2, k_pass_entry (Pi + S^1)
+KC_CANDIDATES = (1, 3, 7, 8, 10)  # k_restrict, k_prolong, k_cheb2, entry (Pi + S^1), up pass
 
 
 def parse():

@@ -95,4 +95,14 @@ template <class T>
 bool launch_pset1_fused(const Lvl& L, const Lvl& Lc, const T* w, T* uout, FusedRhs<T> b,
                         double c0, cudaStream_t st);
 
+// Up half of an SR level visit in one pass (up.cu): u += P(w - t) on C ∪ GSR (R10, R17),
+// then the degree-2 Chebyshev smoothing on C (R8); fin.p: the last pass of the solve, the
+// genuine cells into the user's u.  Lc / w / t: the coarse level's layout and arrays.
+template <class T>
+bool up2_fused_ok(const Lvl& L, const Lvl& Lc);
+template <class T>
+bool launch_up2_fused(const Lvl& L, const Lvl& Lc, const T* u_in, T* u_out, const T* w,
+                      const T* t, FusedRhs<T> b, double c0, double cm, double cr,
+                      cudaStream_t st, FinalOut<T> fin);
+
 }  // namespace srfmg

@@ -122,6 +122,8 @@ struct sr_fmg {
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
   bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
   bool tau_fuse = true;      // tau inside the next pre-smoothing pass; SR_FMG_TAU_FUSE=0 off
+  bool up_fuse = false;      // correction + post-smoothing in one pass (up.cu): measured
+                             // slower than the two passes; SR_FMG_UP_FUSE=1 on
   // coarse-level executor (coarse.cu) for the small conventional levels; SR_FMG_CEXEC=0
   // disables it.  flush_fn: enqueue the recorded operations (called before every launch)
   bool cexec = true;
@@ -1160,8 +1162,56 @@ struct Schedule {
       tau_std(l - 1, jr);  // L116-117 / L234-236
     }
     vcycle(l - 1, sview(l - 1));  // L117 / L237-240
+    if (up_on(l, b)) {
+      up2(l, b, l == h->M);  // L241-242 in one pass (at l = M: the solve's last pass)
+      return;
+    }
     prolong(l, 1);                    // L118 / L241
     cheb(l, h->d.nu2, b, l == h->M);  // L119 / L242 (at l = M: the solve's last pass)
+  }
+
+  // correction + degree-2 post-smoothing in one pass (up.cu) on the SR levels the fused
+  // Chebyshev pass takes; the choice uses the single-GPU shape of the coarse level (R25)
+  bool up_on(int l, const View<T>& b) const {
+    const Lvl& L = h->L[l];
+    // (l - 1 > T: the coarse w and t in segment storage, whose row pitch the pass fixes)
+    return h->up_fuse && h->fused && l - 1 > h->T && h->d.nu2 == 2 && !L.st27 && L.nlg == 0.0 &&
+           tma_rhs_ok(b) && fills(L, 40) && (h->force || L.E[1] >= h->fused_min_e) &&
+           srfmg::up2_fused_ok<T>(L, glob(l - 1));
+  }
+  void up2(int l, const View<T>& b, bool last) {
+    const Lvl& L = h->L[l];
+    LevelBufs& bb = h->B[l];
+    const CellCounts& c = h->cells[l];
+    const bool fp = dd(l - 1) && l - 1 == h->T;
+    if (fp) footprint_T(true);  // k = 1 from a decomposed level T: w - t with its ghosts
+    const double rho0 = 1.0 / h->sigma[l];
+    const double rho1 = 1.0 / (2.0 * h->sigma[l] - rho0);
+    const bool fin = last && final_out != nullptr;
+    srfmg::FinalOut<T> fo{};
+    const double nv = (double)h->blk_n[0] * h->blk_n[1] * h->blk_n[2];
+    if (fin) {
+      fo.p = final_out;
+      for (int i = 0; i < 3; ++i) fo.bo[i] = h->blk_lo[i];
+      fo.sy = h->blk_n[0];
+      fo.sz = (long long)h->blk_n[0] * h->blk_n[1];
+    }
+    bool ok;
+    {
+      // algorithmic words: u read (C u GSR), rhs (C), w and t (1/8 each), u or user u written
+      Launch g(h, st, KC_PASS_UP, l, w * (c.cg + c.compute + c.cg / 4.0 + (fin ? nv : c.cg)));
+      ok = srfmg::launch_up2_fused<T>(
+          L, fp ? h->LT2 : h->L[l - 1], (const T*)bb.u[bb.cur], (T*)bb.u[1 - bb.cur],
+          fp ? (const T*)h->wT2 : U(l - 1), fp ? (const T*)h->zT2 : (const T*)h->B[l - 1].t,
+          frhs(b), 1.0 / h->theta[l], rho1 * rho0, 2.0 * rho1 / h->delta[l], st, fo);
+    }
+    if (!ok) {  // (up_on checked the single-GPU fit; a rank's block never needs more)
+      h->sticky = SR_ERR_UNSUPPORTED_CONFIG;
+      h->err = "fused up pass: no instantiation for this level";
+      return;
+    }
+    bb.cur = 1 - bb.cur;
+    if (fin) final_done = true;
   }
 
   void run(T* uout) {
@@ -1556,6 +1606,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_TAU_FUSE")) h->tau_fuse = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_UP_FUSE")) h->up_fuse = std::atoi(e) != 0;
   if (d->device >= 0) {
     cudaError_t e = cudaSetDevice(d->device);
     if (e != cudaSuccess) {

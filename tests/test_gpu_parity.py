@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("needs CUDA", allow_module_level=True)
 
-from paper_1406_7808_b200 import Solver  # noqa: E402
+from paper_1406_7808_b200 import Solver, kernel_names  # noqa: E402
 
 TOL64, TOL32 = 1e-11, 1e-4
 
@@ -396,6 +396,36 @@ def test_fused_fmg_entry_matches_oracle(case, dtype, monkeypatch):
     monkeypatch.setenv("SR_FMG_PSET1", "1")
     u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
     monkeypatch.setenv("SR_FMG_PSET1", "0")
+    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    assert rel_l2(u, b) <= (1e-13 if dtype == "f64" else 1e-5), (name, rel_l2(u, b))
+    if dtype == "f64":
+        ref = _oracle(rhs, f, n, M, seg, J, K)
+        assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", PSET_CASES, ids=[c[0] for c in PSET_CASES])
+def test_up_pass_correction_and_smoothing(case, dtype, monkeypatch):
+    # u += P(w - t) and the degree-2 post-smoothing in one pass (up.cu) vs the correction
+    # kernel followed by the degree-2 pass: equal up to rounding; oracle parity
+    name, n, M, seg, J, K, rhs = case
+    f = W.make_rhs(rhs, n)
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_UP_FUSE", "1")
+    with Solver(n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype) as s:
+        ft = torch.from_numpy(f.astype(np.float64 if dtype == "f64" else np.float32)).cuda()
+        u = s.solve(ft).cpu().numpy().astype(np.float64)
+        # the case takes the fused up pass on at least one level (the finest when it fits)
+        ups = 0
+        for lvl in range(M + 1):
+            s.profile_select(kernel_names().index("k_pass_up"), lvl)
+            s.solve(ft)
+            torch.cuda.synchronize()
+            ups += s.profile_read()[2]
+        s.profile_select(-1, -1)
+    if name in ("J2-S64", "J3-S64", "J2-S32", "noncubic"):
+        assert ups > 0, name
+    monkeypatch.setenv("SR_FMG_UP_FUSE", "0")
     b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
     assert rel_l2(u, b) <= (1e-13 if dtype == "f64" else 1e-5), (name, rel_l2(u, b))
     if dtype == "f64":
