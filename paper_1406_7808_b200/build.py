@@ -17,7 +17,7 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libsrfmg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["kernels.cu", "fused.cu", "fused27.cu", "prolong.cu", "pset.cu", "up.cu", "coarse.cu", "solver.cpp"]
+SOURCES = ["kernels.cu", "fused.cu", "fused27.cu", "prolong.cu", "pset.cu", "up.cu", "restrict.cu", "coarse.cu", "solver.cpp"]
 HEADERS = ["kernels.cuh", "fused.cuh", "tma.cuh", "coarse.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", CSRC,

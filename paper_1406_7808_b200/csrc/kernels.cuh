@@ -54,6 +54,12 @@ void launch_cheb_step(const Lvl& L, const T* cur, const T* prev, View<T> b, T* o
 template <class T>
 void launch_restrict(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc, int jr,
                      cudaStream_t st, T* scratch = nullptr, View<T> bc = View<T>{});
+// the same restriction on an SR level through bulk-copy-fed bands (restrict.cu): bc = the
+// pyramid f_{l-1} (bf unused), or bc.p = null and bf the level's segment-storage rhs; false
+// when no instantiation fits the level (nothing launched)
+template <class T>
+bool launch_restrict_seg(const Lvl& Lf, const T* uf, View<T> bf, const Lvl& Lc, T* uc, T* rc,
+                         int jr, cudaStream_t st, View<T> bc);
 template <class T>
 void launch_tau(const Lvl& Lc, const T* u, T* rhs, T* t, int jr, cudaStream_t st);
 // uc = avg8(uf), rc = avg8(rf) on the restriction targets (rf: precomputed fine residual)

@@ -121,6 +121,8 @@ struct sr_fmg {
   int fused_min_e = 0; // SR_FMG_FUSED_MIN_E: smallest storage extent given to the TMA kernels
   bool pset1 = true;  // Pi + S^1 in one TMA pass at the FMG entry (pset.cu); SR_FMG_PSET1=0 off
   bool restrict_pyr = true;  // restriction of f-visits via the pyramid; SR_FMG_RESTRICT_PYR=0 off
+  bool restrict_seg = true;  // bulk-copy-fed restriction on SR levels (restrict.cu);
+                             // SR_FMG_RESTRICT_SEG=0 off
   bool tau_fuse = true;      // tau inside the next pre-smoothing pass; SR_FMG_TAU_FUSE=0 off
   bool up_fuse = false;      // correction + post-smoothing in one pass (up.cu): measured
                              // slower than the two passes; SR_FMG_UP_FUSE=1 on
@@ -1093,6 +1095,12 @@ struct Schedule {
                                            pyr27 ? fview(l - 1) : View<T>{});
       return;
     }
+    // SR levels (segment storage; per segment, so every partition runs it, R25): the
+    // bulk-copy-fed bands when an instantiation fits
+    if (l > h->T && h->restrict_seg && !L.st27 && (use_pyr || !b.global) &&
+        srfmg::launch_restrict_seg<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), rc, jr, st,
+                                      use_pyr ? fview(l - 1) : View<T>{}))
+      return;
     // the free ping-pong buffer of level l is scratch for the 27-point residual
     srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), rc, jr, st,
                               (T*)h->B[l].u[1 - h->B[l].cur],
@@ -1605,6 +1613,7 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   h->cexec = !(ce && ce[0] == '0');
   if (const char* e = std::getenv("SR_FMG_PSET1")) h->pset1 = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_RESTRICT_PYR")) h->restrict_pyr = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SR_FMG_RESTRICT_SEG")) h->restrict_seg = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_TAU_FUSE")) h->tau_fuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("SR_FMG_UP_FUSE")) h->up_fuse = std::atoi(e) != 0;
   if (d->device >= 0) {

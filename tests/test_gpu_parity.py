@@ -435,6 +435,23 @@ def test_up_pass_correction_and_smoothing(case, dtype, monkeypatch):
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("case", PSET_CASES, ids=[c[0] for c in PSET_CASES])
+def test_restrict_seg_matches_column_kernel(case, dtype, monkeypatch):
+    # the bulk-copy-fed restriction on the SR levels (restrict.cu) vs the column-marching
+    # k_restrict: the same uc, rc up to the order of the 8-child sums; oracle parity
+    name, n, M, seg, J, K, rhs = case
+    f = W.make_rhs(rhs, n)
+    monkeypatch.setenv("SR_FMG_RESTRICT_SEG", "1")
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    monkeypatch.setenv("SR_FMG_RESTRICT_SEG", "0")
+    b = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K, dtype=dtype)
+    assert rel_l2(u, b) <= (1e-13 if dtype == "f64" else 1e-5), (name, rel_l2(u, b))
+    if dtype == "f64":
+        ref = _oracle(rhs, f, n, M, seg, J, K)
+        assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", PSET_CASES, ids=[c[0] for c in PSET_CASES])
 def test_tau_fused_into_presmoothing(case, dtype, monkeypatch):
     # tau (Eq. 4) computed inside the first degree-2 pass of the coarse SR level's V-cycle
     # vs the separate tau kernel: the same rhs, t and smoothing up to rounding; oracle parity
