@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(kThreadsC, 1)
   __syncthreads();
   const int rank = (int)cl.block_rank();
   if (ol.prof && rank == 0 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    // SM cycle counter (CTA 0 stays on one SM): %globaltimer ticks in ~1 us steps
+    const unsigned long long t = (unsigned long long)clock64();
     ol.prof[0] = t;
   }
   for (int i = 0; i < ol.n; ++i) {
@@ -332,8 +332,7 @@ __global__ void __launch_bounds__(kThreadsC, 1)
     else
       cl.sync();  // the operation's results are visible to every CTA of the cluster
     if (ol.prof && rank == 0 && threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      const unsigned long long t = (unsigned long long)clock64();
       ol.prof[i + 1] = t;
     }
   }

@@ -31,7 +31,7 @@ struct COp {
 template <class T>
 struct COpList {
   int n;
-  unsigned long long* prof;  // optional: %globaltimer after every operation (debug)
+  unsigned long long* prof;  // optional: SM clock64 after every operation (debug)
   Lvl L[kCoarseMaxLevels];
   COp<T> op[kCoarseMaxOps];
 };

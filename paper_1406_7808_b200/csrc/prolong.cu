@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
+#include <type_traits>
 
 #include "fused.cuh"
 #include "tma.cuh"
@@ -34,13 +35,19 @@ struct ProlongArgs {
   int fstride;  // elements per fine smem plane
 };
 
-template <class T, int MAXS>
-__global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__ ProlongArgs<T> a) {
+// PYC != 0: the fine row pitch (and the coarse one, PYC/2 + 4, as the segment storage of
+// the next coarser SR level has) at compile time; ADD: the correction (fig:mgvsr L241)
+template <class T, int MAXS, int ADD, int PYC>
+// (6 rows per thread: at most 72 x 4 threads, registers up to 128 -- no spills)
+__global__ void __launch_bounds__(MAXS == 6 ? 512 : 1024, 1)
+    k_prolong_tma(const __grid_constant__ ProlongArgs<T> a) {
   extern __shared__ __align__(128) unsigned char sm[];
   const Lvl& Lf = a.Lf;
   const Lvl& Lc = a.Lc;
   const int s = blockIdx.y;
   const int Ey = Lf.E[1], Ez = Lf.E[2], Ex = Lf.E[0];
+  const int fpy = PYC ? PYC : Lf.py;
+  const int cpyc = PYC ? PYC / 2 + 4 : Lc.py;
   const int r0 = blockIdx.x * a.BH, r1 = min(Ey, r0 + a.BH);
   // fine segment geometry
   const int px = s % Lf.ns[0] + Lf.so[0], py_ = (s / Lf.ns[0]) % Lf.ns[1] + Lf.so[1],
@@ -61,14 +68,14 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
   const int cy_lo = max((gy_lo >> 1) - 1, 0), cy_hi = min(((gy_hi - 1) >> 1) + 1, Lc.N[1] - 1);
   const int cz_lo = max((gz_lo >> 1) - 1, 0), cz_hi = min(((gz_hi - 1) >> 1) + 1, Lc.N[2] - 1);
   const int crows = cy_hi - cy_lo + 1;
-  const uint32_t cbytes = (uint32_t)(crows * Lc.py * sizeof(T));
-  const uint32_t fbytes = (uint32_t)((r1 - r0) * Lf.py * sizeof(T));
+  const uint32_t cbytes = (uint32_t)(crows * cpyc * sizeof(T));
+  const uint32_t fbytes = (uint32_t)((r1 - r0) * fpy * sizeof(T));
   T* cw = reinterpret_cast<T*>(sm);               // kRC planes of w
   T* ct = cw + kRC * a.cstride;                   // kRC planes of t (ADD)
   T* fu = ct + kRC * a.cstride;                   // kRF planes of fine u (ADD)
   uint64_t* bars = reinterpret_cast<uint64_t*>(fu + kRF * a.fstride);  // [0,kRC) coarse, then fine
-  const T* wseg = a.w + (long long)cs * Lc.ss + (long long)(cy_lo - ocy) * Lc.py;
-  const T* tseg = a.t + (long long)cs * Lc.ss + (long long)(cy_lo - ocy) * Lc.py;
+  const T* wseg = a.w + (long long)cs * Lc.ss + (long long)(cy_lo - ocy) * cpyc;
+  const T* tseg = ADD ? a.t + (long long)cs * Lc.ss + (long long)(cy_lo - ocy) * cpyc : nullptr;
   T* useg = a.uf + (long long)s * Lf.ss;
   const int P0 = gz_lo >> 1, P1 = (gz_hi - 1) >> 1;  // parent planes looped over
   const int fz0 = 2 * P0;                            // first fine plane of the loop (global)
@@ -80,26 +87,26 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
   __syncthreads();
   auto issue_c = [&](int c) {  // coarse plane c (global), c in [cz_lo, cz_hi]
     const int sl = (c - cz_lo) % kRC;
-    mbar_expect_tx(&bars[sl], a.add ? 2 * cbytes : cbytes);
+    mbar_expect_tx(&bars[sl], ADD ? 2 * cbytes : cbytes);
     const long long zo = (long long)(c - ocz) * Lc.pz;
     bulk_g2s(cw + sl * a.cstride, wseg + zo, cbytes, &bars[sl]);
-    if (a.add) bulk_g2s(ct + sl * a.cstride, tseg + zo, cbytes, &bars[sl]);
+    if (ADD) bulk_g2s(ct + sl * a.cstride, tseg + zo, cbytes, &bars[sl]);
   };
   auto issue_f = [&](int gz) {  // fine plane gz (global), ADD only
     const int sl = (gz - gz_lo) % kRF;
     mbar_expect_tx(&bars[kRC + sl], fbytes);
-    bulk_g2s(fu + sl * a.fstride, useg + (long long)(gz - oz) * Lf.pz + (long long)r0 * Lf.py,
+    bulk_g2s(fu + sl * a.fstride, useg + (long long)(gz - oz) * Lf.pz + (long long)r0 * fpy,
              fbytes, &bars[kRC + sl]);
   };
   int nc = cz_lo, nf = gz_lo;  // next coarse / fine plane to issue (thread 0)
   if (threadIdx.x == 0) {
     for (; nc <= min(cz_hi, cz_lo + kRC - 1); ++nc) issue_c(nc);
-    if (a.add)
+    if (ADD)
       for (; nf < min(gz_lo + kRF, gz_hi); ++nf) issue_f(nf);
   }
 
   // ---- this thread: column tx, rows r0 + g*MAXS + k
-  const int tx = threadIdx.x % Lf.py, g = threadIdx.x / Lf.py;
+  const int tx = threadIdx.x % fpy, g = threadIdx.x / fpy;
   const int gx = ox + tx;
   const bool xin = tx < Ex && gx >= 0 && gx < Lf.N[0];
   int cxo[2];
@@ -129,8 +136,8 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
     if (ok) out_mask |= 1u << k;
     P = min(max(P, cy_lo), cy_hi);
     Q = min(max(Q, cy_lo), cy_hi);
-    yo[k][0] = (P - cy_lo) * Lc.py;
-    yo[k][1] = (Q - cy_lo) * Lc.py;
+    yo[k][0] = (P - cy_lo) * cpyc;
+    yo[k][1] = (Q - cy_lo) * cpyc;
   }
   auto interp = [&](int c, T* I) {  // xy-interpolants of real coarse plane c for all slots
     const int sl = (c - cz_lo) % kRC;
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
       for (int j = 0; j < 4; ++j) {
         const int o = yo[k][j >> 1] + cxo[j & 1];
         v[j] = pw[o];
-        if (a.add) v[j] = v[j] - pt[o];
+        if (ADD) v[j] = v[j] - pt[o];
       }
       // I = W0 (W0 v_pp + W1 sx v_pn) + W1 sy (W0 v_np + W1 sx v_nn)
       I[k] = W0 * (W0 * v[0] + W1x * v[1]) + W1 * sy[k] * (W0 * v[2] + W1x * v[3]);
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
   wait_c(P0);
   get(P0 - 1, Im);
   get(P0, I0);
-  T* const ucol = useg + (long long)(r0 + g * MAXS) * Lf.py + tx;
+  T* const ucol = useg + (long long)(r0 + g * MAXS) * fpy + tx;
   const long long pzf = Lf.pz;
   for (int P = P0; P <= P1; ++P) {
     const int cn = min(P + 1, Lc.N[2] - 1);
@@ -178,24 +185,24 @@ __global__ void __launch_bounds__(1024, 1) k_prolong_tma(const __grid_constant__
       const int gz = 2 * P + e;
       if (gz < gz_lo || gz >= gz_hi) continue;
       const T* uin = nullptr;
-      if (a.add) {
+      if (ADD) {
         const int n = gz - gz_lo;
         mbar_wait(&bars[kRC + n % kRF], (n / kRF) & 1);
-        uin = fu + (n % kRF) * a.fstride + (g * MAXS) * Lf.py + tx;
+        uin = fu + (n % kRF) * a.fstride + (g * MAXS) * fpy + tx;
       }
       T* orow = ucol + (long long)(gz - oz) * pzf;
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
         if (!((out_mask >> k) & 1u)) continue;
         const T acc = W0 * I0[k] + W1 * (e ? Ip[k] : Im[k]);
-        orow[k * Lf.py] = a.add ? uin[k * Lf.py] + acc : acc;
+        orow[k * fpy] = ADD ? uin[k * fpy] + acc : acc;
       }
     }
     __syncthreads();  // coarse plane P-1 and fine planes 2P, 2P+1 are free
     if (threadIdx.x == 0) {
       // planes P..P+3 may now be resident (the slot of P-1 is free); fine 2P+2..2P+5
       for (; nc <= min(cz_hi, P + 3); ++nc) issue_c(nc);
-      if (a.add)
+      if (ADD)
         for (; nf <= min(gz_hi - 1, 2 * P + 5); ++nf) issue_f(nf);
     }
 #pragma unroll
@@ -234,9 +241,9 @@ void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T
     const char* e = std::getenv("SR_FMG_PROLONG_BH");
     return e ? std::atoi(e) : 0;
   }();
-  // fp32 at E = 70: 6 rows per thread (C3 finest correction 0.383 vs 0.446 ms); fp64 and the
-  // E = 38 boxes: 3 (fp64 at 6: 0.70 vs 0.53 ms)
-  const int MAXS = maxs_env ? (maxs_env == 6 ? 6 : 3) : (sizeof(T) == 4 && Lf.E[1] > 40 ? 6 : 3);
+  // 6 rows per thread from E = 22 on (C3, fp64: finest correction 0.515 vs 0.538 ms, level 7
+  // 0.207 vs 0.221; fp32 finest 0.311 vs 0.416 ms), 3 on the E = 14 boxes (0.074 vs 0.090)
+  const int MAXS = maxs_env ? (maxs_env == 6 ? 6 : 3) : (Lf.E[1] >= 22 ? 6 : 3);
   const int tgt = bh_env > 0 ? bh_env : (Lf.E[1] <= 40 ? 24 : 18);
   const int nb = (Lf.E[1] + tgt - 1) / tgt;
   const int BH = (Lf.E[1] + nb - 1) / nb;
@@ -254,7 +261,20 @@ void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T
   a.fstride = (BH * Lf.py + A - 1) / A * A;
   const size_t smem = (size_t)(2 * kRC * a.cstride + kRF * a.fstride) * sizeof(T) + 8 * (kRC + kRF);
   const int NT = Lf.py * ((BH + MAXS - 1) / MAXS);
-  auto kern = MAXS == 6 ? k_prolong_tma<T, 6> : k_prolong_tma<T, 3>;
+  // compile-time pitches for the C3-type boxes (E = 70, 38 over a coarse SR level)
+  const int pyc = (Lf.py == 72 || Lf.py == 40) && Lc.py == Lf.py / 2 + 4 ? Lf.py : 0;
+  auto pick = [&](auto MS) {
+    constexpr int M = decltype(MS)::value;
+    if (add) {
+      if (pyc == 72) return k_prolong_tma<T, M, 1, 72>;
+      if (pyc == 40) return k_prolong_tma<T, M, 1, 40>;
+      return k_prolong_tma<T, M, 1, 0>;
+    }
+    if (pyc == 72) return k_prolong_tma<T, M, 0, 72>;
+    if (pyc == 40) return k_prolong_tma<T, M, 0, 40>;
+    return k_prolong_tma<T, M, 0, 0>;
+  };
+  auto kern = MAXS == 6 ? pick(std::integral_constant<int, 6>{}) : pick(std::integral_constant<int, 3>{});
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<dim3(nb, Lf.nsegs), NT, smem, st>>>(a);
 }

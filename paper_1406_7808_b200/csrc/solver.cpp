@@ -615,8 +615,8 @@ struct Schedule {
         cudaStreamSynchronize(st);
         for (int i = 0; i < cops.n; ++i) {
           const srfmg::COp<T>& o = cops.op[i];
-          fprintf(stderr, "cexec op %2d code %d lf %d lc %d tiny %d  %8.2f us\n", i, o.code, o.lf,
-                  o.lc, o.tiny, (buf[i + 1] - buf[i]) * 1e-3);
+          fprintf(stderr, "cexec op %2d code %d lf %d lc %d tiny %d  %8llu cycles\n", i, o.code,
+                  o.lf, o.lc, o.tiny, buf[i + 1] - buf[i]);
         }
       } else {
         srfmg::launch_coarse_exec<T>(cops, st);
