@@ -39,12 +39,16 @@ struct PsetArgs {
   int cpl;      // elements per staged coarse plane
 };
 
-template <class T, int PY, int BH, int MAXS>
+template <class T, int PY, int BH, int MAXS, int PW = 0>
 struct GP {
   static constexpr int kAl = 16 / (int)sizeof(T);
   static constexpr int FP = PY + kAl;
   static constexpr int NG = (BH + 2 + MAXS - 1) / MAXS;
   static constexpr int NT = PY * NG;
+  // PW: one producer warp after the compute threads (rounded up to whole warps) issues every
+  // copy; else thread 0 issues them after each plane barrier
+  static constexpr int NTC = PW ? (NT + 31) / 32 * 32 : NT;
+  static constexpr int NTP = PW ? NTC + 32 : NT;
   static constexpr int TR = NG * MAXS;  // thread rows, from r0 - 1
   static constexpr int A = 128 / (int)sizeof(T);
   static constexpr int U0S = ((TR + 2) * PY + A - 1) / A * A;
@@ -52,14 +56,14 @@ struct GP {
   static constexpr int RF = 4, RC = 8;  // powers of two: slot/phase by shifts
   static constexpr int CROWS = TR / 2 + 3;
   static size_t smem(int cpl) {
-    return (size_t)(4 * U0S + RF * FS + RC * cpl) * sizeof(T) + 8 * (RF + RC);
+    return (size_t)(4 * U0S + RF * FS + RC * cpl) * sizeof(T) + 8 * (2 * RF + RC);
   }
 };
 
-template <class T, int PY, int BH, int MAXS, int ZQ, int NB>
-__global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
+template <class T, int PY, int BH, int MAXS, int ZQ, int NB, int PW>
+__global__ void __launch_bounds__(GP<T, PY, BH, MAXS, PW>::NTP, NB)
     k_pset1s(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ PsetArgs<T> a) {
-  using G = GP<T, PY, BH, MAXS>;
+  using G = GP<T, PY, BH, MAXS, PW>;
   constexpr int NCR = MAXS / 2 + 2;
   static_assert(MAXS % 2 == 0 && BH % 2 == 0, "row pairs");
   constexpr int YP = (ZQ + 1) & 1;  // J mod 2 (ZQ = (J + 1) mod 4)
@@ -74,7 +78,9 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
   T* u0s = reinterpret_cast<T*>(sm);
   T* fs = u0s + 4 * G::U0S;
   T* cs_ = fs + G::RF * G::FS;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(cs_ + G::RC * a.cpl);  // [0,RF) f, then coarse
+  // [0,RF) f full, [RF,RF+RC) coarse full, [RF+RC, 2RF+RC) f empty (plane step done)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cs_ + G::RC * a.cpl);
+  uint64_t* fdone = bars + G::RF + G::RC;
 
   const int px = s % L.ns[0] + L.so[0];
   const int pyy = (s / L.ns[0]) % L.ns[1] + L.so[1];
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
   const T* cw = a.w + (long long)cseg * Lc.ss + (long long)(cy_lo - ocy) * Lc.py;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < G::RF + G::RC; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 2 * G::RF + G::RC; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -122,13 +128,35 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
     const int n = c - cz_lo;
     mbar_wait(&bars[G::RF + (n & (G::RC - 1))], (n / G::RC) & 1);
   };
-  int nc = cz_lo;
-  if (threadIdx.x == 0) {
+  int nc = cz_lo;  // (PW = 0: next coarse plane to issue, thread 0)
+  if (!PW && threadIdx.x == 0) {
     for (int z = 0; z < min(G::RF, Ez); ++z) issue_f(z);
     for (; nc <= min(cz_hi, cz_lo + G::RC - 1); ++nc) issue_c(nc);
   }
-
-  const int tx = threadIdx.x % PY, g = threadIdx.x / PY;
+  if (PW && threadIdx.x >= G::NTC) {  // ---- producer warp: the copy schedule, off the compute path
+    if (threadIdx.x == G::NTC) {
+      int nc = cz_lo;
+      for (int z = 0; z < min(G::RF, Ez); ++z) issue_f(z);
+      for (; nc <= min(cz_hi, cz_lo + G::RC - 1); ++nc) issue_c(nc);
+      for (int z = 0; z < Ez; ++z) {
+        mbar_wait(&fdone[z & (G::RF - 1)], (z / G::RF) & 1);  // plane step z done
+        if (z + G::RF < Ez) issue_f(z + G::RF);  // rhs plane z is consumed
+        const int live = max(cz_lo, ((oz + z + 2) >> 1) - 1);
+        for (; nc <= cz_hi && nc < live + G::RC; ++nc) issue_c(nc);
+      }
+      for (int c = max(cz_lo, nc - G::RC); c < nc; ++c) wait_c(c);  // nothing left in flight
+    }
+    return;
+  }
+  // ---- compute threads.  The NTC - NT padding threads (PW) run the same code on the last
+  // row group with every mask clear and no shared-memory stores, so that all NTC threads reach
+  // each (aligned) named barrier from the same instruction
+  auto csync = [] {
+    if constexpr (PW) asm volatile("bar.sync 1, %0;" ::"n"(G::NTC) : "memory");
+    else __syncthreads();
+  };
+  const bool pad = PW && threadIdx.x >= G::NT;
+  const int tx = threadIdx.x % PY, g = min((int)threadIdx.x / PY, G::NG - 1);
   const int y0 = sb + g * MAXS;
   const int gx = ox + tx;
   const bool tok = tx < Ex;
@@ -140,10 +168,10 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) {
     const int y = y0 + k, gy = oy + y;
-    const bool in = tin && y >= 0 && y < Ey && gy >= 0 && gy < L.N[1];
+    const bool in = !pad && tin && y >= 0 && y < Ey && gy >= 0 && gy < L.N[1];
     if (in) in_mask |= 1u << k;
     if (in && tcx && y >= 1 && y <= Ey - 2) c_mask |= 1u << k;
-    if (y >= r0 && y < r1) rw_mask |= 1u << k;
+    if (!pad && y >= r0 && y < r1) rw_mask |= 1u << k;
     dk[k] = T(6 + dxo + (gy == 0 ? 1 : 0) + (gy == L.N[1] - 1 ? 1 : 0));
   }
   // prolongation geometry (R10): x parent / neighbour column in the staged coarse rows
@@ -222,7 +250,7 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
     for (int k = 0; k < MAXS; ++k) {
       const T v = ((in_mask >> k) & 1u) ? pv[k] : T(0);
       u0q[k][RS] = v;
-      up[k * PY] = v;
+      if (!pad) up[k * PY] = v;
     }
   };
   {  // the interpolants at the first in-domain plane: I(P0), and I(P0-1) if it is even
@@ -236,7 +264,7 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
     }
   }
   source(std::integral_constant<int, 0>{}, 0);
-  __syncthreads();
+  csync();
   const T ih2 = T(L.inv_h2);
   const T c0 = a.c0;
   T* const ob = oseg + (long long)y0 * PY + tx;
@@ -270,11 +298,15 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
       const T v1 = ((act >> k) & 1u) ? v0 + c0 * r : v0;
       if ((wr >> k) & 1u) orow[k * PY] = v1;
     }
-    __syncthreads();  // the only barrier of the plane step
+    csync();  // the only barrier of the plane step
     if (threadIdx.x == 0) {
-      if (z + G::RF < Ez) issue_f(z + G::RF);  // rhs plane z is consumed
-      const int live = max(cz_lo, ((oz + z + 2) >> 1) - 1);
-      for (; nc <= cz_hi && nc < live + G::RC; ++nc) issue_c(nc);
+      if constexpr (PW) {
+        mbar_arrive(&fdone[z & (G::RF - 1)]);  // to the producer
+      } else {
+        if (z + G::RF < Ez) issue_f(z + G::RF);  // rhs plane z is consumed
+        const int live = max(cz_lo, ((oz + z + 2) >> 1) - 1);
+        for (; nc <= cz_hi && nc < live + G::RC; ++nc) issue_c(nc);
+      }
     }
   };
   for (int zb = 0; zb < Ez; zb += 4) {
@@ -283,14 +315,14 @@ __global__ void __launch_bounds__(GP<T, PY, BH, MAXS>::NT, NB)
     if (zb + 2 < Ez) step(std::integral_constant<int, 2>{}, zb + 2);
     if (zb + 3 < Ez) step(std::integral_constant<int, 3>{}, zb + 3);
   }
-  if (threadIdx.x == 0)  // no bulk copy may still target this CTA's shared memory
+  if (!PW && threadIdx.x == 0)  // no bulk copy may still target this CTA's shared memory
     for (int c = max(cz_lo, nc - G::RC); c < nc; ++c) wait_c(c);
 }
 
-template <class T, int PY, int BH, int MAXS, int ZQ, int NB = 2>
+template <class T, int PY, int BH, int MAXS, int ZQ, int NB = 2, int PW = 0>
 bool try_pset(const Lvl& L, const Lvl& Lc, const T* w, T* uout, const FusedRhs<T>& b, double c0,
               cudaStream_t st, bool launch) {
-  using G = GP<T, PY, BH, MAXS>;
+  using G = GP<T, PY, BH, MAXS, PW>;
   if (L.py != PY || L.E[0] > PY || !b.global) return false;
   const int cpl = (int)(((long long)G::CROWS * Lc.py + G::A - 1) / G::A * G::A);
   const size_t smem = G::smem(cpl);
@@ -308,9 +340,9 @@ bool try_pset(const Lvl& L, const Lvl& Lc, const T* w, T* uout, const FusedRhs<T
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   if (!encode_dense_tmap<T>(&map, b, G::FP, G::TR)) return false;
-  auto kern = k_pset1s<T, PY, BH, MAXS, ZQ, NB>;
+  auto kern = k_pset1s<T, PY, BH, MAXS, ZQ, NB, PW>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);  // per device
-  kern<<<dim3((L.E[1] + BH - 1) / BH, L.nsegs), G::NT, smem, st>>>(map, a);
+  kern<<<dim3((L.E[1] + BH - 1) / BH, L.nsegs), G::NTP, smem, st>>>(map, a);
   return true;
 }
 
@@ -325,6 +357,14 @@ bool pset_geom(const Lvl& L, const Lvl& Lc, const T* w, T* uout, const FusedRhs<
                double c0, cudaStream_t st, bool launch) {
   constexpr int NB = sizeof(T) == 4 ? 3 : 2;
   if (sizeof(T) == 4 && try_pset<T, 72, 14, 8, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch))
+    return true;
+  // fp64 at E = 70: a producer warp issues the copies (120 registers; SR_FMG_PSET_PW=0: thread
+  // 0 after each plane barrier, as the other geometries, where the extra warp costs spills)
+  static const bool pw = [] {
+    const char* e = std::getenv("SR_FMG_PSET_PW");
+    return !(e && e[0] == '0');
+  }();
+  if (sizeof(T) == 8 && pw && try_pset<T, 72, 10, 4, ZQ, NB, 1>(L, Lc, w, uout, b, c0, st, launch))
     return true;
   return try_pset<T, 72, 10, 4, ZQ, NB>(L, Lc, w, uout, b, c0, st, launch) ||
          // E = 134: 10-row bands at one CTA per SM (4.9 ms at C5; 6-row bands at two: 6.7 ms)
