@@ -25,6 +25,7 @@ ap.add_argument("--config", default="C3")
 ap.add_argument("--dtype", default="f64")
 ap.add_argument("--what", default="solve", choices=["solve", "cheb", "restrict", "prolong", "correct"])
 ap.add_argument("--graph", type=int, default=1)
+ap.add_argument("--level", type=int, default=-1, help="level of the single operation (default M)")
 a = ap.parse_args()
 n, M, seg, buf, K, rhs = WORKLOADS[a.config]
 s = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=a.dtype, use_graph=bool(a.graph))
@@ -33,17 +34,18 @@ u = torch.empty_like(f)
 s.solve(f, u)
 s.solve(f, u)
 torch.cuda.synchronize()
+lv = M if a.level < 0 else a.level
 torch.cuda.profiler.start()
 if a.what == "solve":
     s.solve(f, u)
 elif a.what == "cheb":
-    s.debug_op(0, M, 2, f)
+    s.debug_op(0, lv, 2, f)
 elif a.what == "restrict":
-    s.debug_op(1, M, 0, f)
+    s.debug_op(1, lv, 0, f)
 elif a.what == "prolong":
-    s.debug_op(3, M, 0, f)
+    s.debug_op(3, lv, 0, f)
 elif a.what == "correct":
-    s.debug_op(4, M, 0, f)
+    s.debug_op(4, lv, 0, f)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("ok")
