@@ -105,7 +105,16 @@ typedef struct {
   /* the first level below is all-gathered once per visit and it and the coarser levels    */
   /* are solved redundantly on every rank.  0 = default (32); a value    */
   /* larger than the level-T block agglomerates at T (no decomposed coarse levels).         */
+  /* sr_levels = 0 with world > 1 is the paper's non-SR baseline: every  */
+  /* level down to A is decomposed, the finest included (fine-level halo exchanges); the   */
+  /* finest rank block must then have at least dd_min cells per dimension.                  */
   int32_t dd_min;
+  /* world > 1: how the levels <= A are solved.  0 (default) = redundant: */
+  /* level A is all-gathered and every rank solves the levels <= A.  1 = idle: the blocks of */
+  /* level A are gathered onto rank 0 alone, rank 0 solves the levels <= A while the other   */
+  /* ranks idle, and rank 0 sends u_A (and the tau snapshot t_A) back to every rank.  Same   */
+  /* arithmetic, bitwise the same result.                                                    */
+  int32_t coarse_idle;
 } sr_fmg_desc_t;
 
 typedef struct {

@@ -49,6 +49,7 @@ class Desc(ctypes.Structure):
         ("nl_gamma", ctypes.c_double),
         ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
         ("dd_min", ctypes.c_int32),
+        ("coarse_idle", ctypes.c_int32),
     ]
 
 

@@ -31,7 +31,7 @@ class LevelInfo:
 
 def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha=1, nu1=2,
               nu2=2, cheb=None, device=None, use_graph=True, world=1, rank=0,
-              pgrid=(1, 1, 1), stencil="7pt", nl_gamma=0.0, dd_min=0) -> Desc:
+              pgrid=(1, 1, 1), stencil="7pt", nl_gamma=0.0, dd_min=0, coarse_idle=False) -> Desc:
     if isinstance(n, int):
         n = (n, n, n)
     d = Desc()
@@ -56,13 +56,15 @@ def make_desc(n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None, alpha
     d.use_graph = 1 if use_graph else 0
     d.world, d.rank = int(world), int(rank)
     d.dd_min = int(dd_min)
+    d.coarse_idle = 1 if coarse_idle else 0
     return d
 
 
-def partition(n, M, seg, buffer, K, world, rank, pgrid, sched=None, dd_min=0) -> dict:
+def partition(n, M, seg, buffer, K, world, rank, pgrid, sched=None, dd_min=0,
+              coarse_idle=False) -> dict:
     """This rank's block of a multi-GPU descriptor (host arithmetic, no GPU)."""
     d = make_desc(n, M, seg, buffer, K, sched=sched, world=world, rank=rank, pgrid=pgrid,
-                  dd_min=dd_min)
+                  dd_min=dd_min, coarse_idle=coarse_idle)
     p = Partition()
     check(lib.sr_fmg_partition(ctypes.byref(d), ctypes.byref(p)))
     return dict(world=p.world, rank=p.rank, coord=tuple(p.coord),
@@ -97,17 +99,20 @@ class Solver:
 
     Parameters mirror sr_fmg_desc_t: n (n1, n2, n3) or an int for a cube, M, seg (S),
     buffer (J), K (SR levels), dtype "f64"/"f32", h (fine cell size), sched (Eq. 5 A, B),
-    F(alpha, nu1, nu2) degrees, Chebyshev interval fractions.
+    F(alpha, nu1, nu2) degrees, Chebyshev interval fractions.  Multi-GPU: world, rank,
+    pgrid, nccl_id (or host_store, tests), dd_min (decomposed coarse levels), coarse_idle
+    (levels <= A on rank 0 alone instead of redundantly); K = 0 with
+    world > 1 is the conventional distributed FMG with fine-level halo exchanges.
     """
 
     def __init__(self, n, M, seg=0, buffer=2, K=0, dtype="f64", h=None, sched=None,
                  alpha=1, nu1=2, nu2=2, cheb=None, device=None, use_graph=True,
                  world=1, rank=0, pgrid=(1, 1, 1), nccl_id=None, host_store=None,
-                 stencil="7pt", nl_gamma=0.0, allocator=None, dd_min=0):
+                 stencil="7pt", nl_gamma=0.0, allocator=None, dd_min=0, coarse_idle=False):
         if isinstance(n, int):
             n = (n, n, n)
         d = make_desc(n, M, seg, buffer, K, dtype, h, sched, alpha, nu1, nu2, cheb, device,
-                      use_graph, world, rank, pgrid, stencil, nl_gamma, dd_min)
+                      use_graph, world, rank, pgrid, stencil, nl_gamma, dd_min, coarse_idle)
         if allocator == "torch":
             # the workspace comes from PyTorch's caching allocator (desc.alloc / desc.free);
             # the callbacks must outlive the handle

@@ -154,6 +154,7 @@ struct sr_fmg {
   // before every operator application); levels l <= A are gathered once and solved
   // redundantly on every rank (the paper's redundant coarse grid)
   int A = 0;
+  bool idle = false;                        // levels <= A on rank 0 only (desc.coarse_idle)
   int dd_min = 0;                           // a level stays decomposed while every block
                                             // dimension has at least dd_min cells
   srfmg::Lvl LT2{};                         // level T block with the k = 1 footprint ghosts
@@ -221,10 +222,16 @@ sr_status_t validate(const sr_fmg_desc_t* d, std::string& msg) {
     if (d->pgrid[i] < 1 || d->pgrid[i] > d->world) return bad("need 1 <= pgrid[d] <= world");
   if ((long long)d->pgrid[0] * d->pgrid[1] * d->pgrid[2] != d->world) return bad("world != prod(pgrid)");
   if (d->rank < 0 || d->rank >= d->world) return bad("rank out of range");
+  if (d->coarse_idle != 0 && d->coarse_idle != 1) return bad("coarse_idle must be 0 or 1");
   if (d->world > 1) {
-    for (int i = 0; i < 3; ++i)
-      if (d->sr_levels == 0 || (d->n[i] / d->seg) % d->pgrid[i])
-        return bad("world > 1 needs sr_levels >= 1 and pgrid dividing the segment grid");
+    for (int i = 0; i < 3; ++i) {
+      if (d->sr_levels > 0 && (d->n[i] / d->seg) % d->pgrid[i])
+        return bad("world > 1 needs pgrid dividing the segment grid");
+      // sr_levels = 0 (conventional distributed FMG): the rank blocks tile the fine grid and
+      // coarsen evenly onto level M-1 at least
+      if (d->sr_levels == 0 && (d->n[i] % d->pgrid[i] || (d->n[i] / d->pgrid[i]) % 2))
+        return bad("world > 1 with sr_levels = 0 needs pgrid dividing n into even blocks");
+    }
   }
   // supported-config checks
   if (d->world > 1 && d->comm != 0 && d->comm != 1) {
@@ -280,9 +287,9 @@ void make_plan(sr_fmg* h) {
     if (h->K > 0) {
       h->nsr[i] = (int)(d->n[i] / d->seg) / d->pgrid[i];
       h->blk_n[i] = h->nsr[i] * d->seg;
-    } else {
+    } else {  // conventional FMG: a pgrid block of the fine grid (world 1: the whole grid)
       h->nsr[i] = 0;
-      h->blk_n[i] = (int)d->n[i];
+      h->blk_n[i] = (int)(d->n[i] / d->pgrid[i]);
     }
     h->blk_lo[i] = h->coord[i] * h->blk_n[i];
     h->blkT_n[i] = h->blk_n[i] >> h->K;
@@ -293,7 +300,8 @@ void make_plan(sr_fmg* h) {
   h->H.assign(h->M + 1, 0);
   h->flo.assign(h->M + 1, {0, 0, 0});
   h->fdim.assign(h->M + 1, {0, 0, 0});
-  if (h->world > 1) {
+  // (sr_levels = 0: every level reads f_l on the rank's block only -- no halo)
+  if (h->world > 1 && h->K > 0) {
     int h1 = 0;
     for (int l = h->T + 1; l <= h->M; ++l) {
       const int j = buffer_of(d, l - h->T);
@@ -314,6 +322,7 @@ void make_plan(sr_fmg* h) {
   // onto level l-1); the first level that does not is gathered (A), and every level <= A is
   // solved redundantly
   h->dd_min = d->dd_min > 0 ? d->dd_min : 32;
+  h->idle = h->world > 1 && d->coarse_idle == 1;
   h->A = h->T;
   if (h->world > 1) {
     while (h->A >= 1) {
@@ -383,6 +392,17 @@ void make_plan(sr_fmg* h) {
     L2.pz = (long long)L2.py * L2.E[1];
     L2.ss = round_up(L2.pz * L2.E[2], 32);
   }
+}
+
+// checks that need the plan: the conventional distributed FMG (sr_levels = 0, world > 1)
+// decomposes the finest level itself, so its rank blocks must not fall under dd_min
+bool plan_ok(const sr_fmg* h, std::string& msg) {
+  if (h->world > 1 && h->K == 0 && h->A >= h->M) {
+    msg = "world > 1 with sr_levels = 0: the finest rank block has fewer than dd_min cells in "
+          "some dimension (lower dd_min or use fewer ranks)";
+    return false;
+  }
+  return true;
 }
 
 // dense inverse of A_0 (7-point, reflected ghosts) by Gauss-Jordan in fp64 (R7)
@@ -515,10 +535,14 @@ struct Schedule {
 
   // f_l as a dense view: the user's (haloed) block at l = M, the rank's haloed local
   // pyramid block on SR levels (multi-GPU), the global f_l otherwise
-  View<T> fview(int l) {
+  // sr_read: the view an SR level's restriction reads (f_{l} near its segments' F regions):
+  // on multi-GPU the rank's haloed local f_T even when level T is gathered -- an idle rank
+  // (desc.coarse_idle) never assembles the global f_T
+  View<T> fview(int l, bool sr_read = false) {
     View<T> v{};
     v.global = 1;
-    const bool local = l > h->T || (l == h->M) || (h->world > 1 && l > h->A);
+    const bool local = l > h->T || (l == h->M) || (h->world > 1 && l > h->A) ||
+                       (sr_read && h->world > 1 && l == h->T);
     if (local && (l == h->M || l >= h->T)) {
       v.base = (l == h->M) ? f : (const T*)(h->world > 1 ? h->B[l].floc : h->B[l].fpyr);
       for (int i = 0; i < 3; ++i) {
@@ -984,22 +1008,59 @@ struct Schedule {
     T* rcv = (T*)h->xrecv;
     for (int k = 0; k < nf; ++k)
       srfmg::launch_box_copy<T>(sbase[k], ssy[k], ssz[k], slo[k], nb3, snd + k * nb, 1, st);
-    const sr_status_t r = h->comm->allgather(h, snd, rcv, (size_t)nf * nb * sizeof(T), st);
+    const size_t bytes = (size_t)nf * nb * sizeof(T);
+    sr_status_t r = SR_OK;
+    if (!h->idle) {
+      r = h->comm->allgather(h, snd, rcv, bytes, st);
+    } else {
+      // idle coarse grid: the blocks go to rank 0 alone, one NCCL group
+      std::vector<Xfer> xs;
+      if (h->rank == 0) {
+        for (int q = 1; q < h->world; ++q) xs.push_back(Xfer{q, 1, rcv + q * nf * nb, bytes});
+      } else {
+        xs.push_back(Xfer{0, 0, snd, bytes});
+      }
+      r = h->comm->group(h, xs.data(), (int)xs.size(), st);
+    }
     if (r != SR_OK) h->sticky = r;
     h->comm_calls[lvl]++;
     h->exch++;
     h->launches += nf;
+    if (h->idle && h->rank != 0) return;  // only rank 0 assembles level A
     for (int q = 0; q < h->world; ++q) {
       const int c[3] = {q % h->d.pgrid[0], (q / h->d.pgrid[0]) % h->d.pgrid[1],
                         q / (h->d.pgrid[0] * h->d.pgrid[1])};
       int lo[3];
       for (int i = 0; i < 3; ++i) lo[i] = c[i] * nb3[i];
       if (q == h->rank && sbase[0] == dbase[0]) continue;  // already in place
+      // (the rank's own block from its send buffer: a gather to rank 0 receives no copy)
+      T* from = q == h->rank ? snd : rcv + q * nf * nb;
       for (int k = 0; k < nf; ++k)
-        srfmg::launch_box_copy<T>(dbase[k], dsy[k], dsz[k], lo, nb3, rcv + (q * nf + k) * nb, 0,
-                                  st);
+        srfmg::launch_box_copy<T>(dbase[k], dsy[k], dsz[k], lo, nb3, from + k * nb, 0, st);
       h->launches += nf;
     }
+  }
+  // idle coarse grid: rank 0 alone runs the levels <= A (redundant: every rank)
+  bool solves_A() const { return !h->idle || h->rank == 0; }
+  // idle coarse grid: rank 0 sends its level-A solution u_A (and the tau snapshot t_A for a
+  // correction) to every other rank, whole storage arrays, one NCCL group
+  void bcast_A(bool with_t) {
+    flush();
+    const int a = h->A;
+    const Lvl& LA = h->L[a];
+    const size_t bytes = (size_t)LA.ss * LA.nsegs * sizeof(T);
+    std::vector<Xfer> xs;
+    for (int q = 1; q < h->world; ++q) {
+      if (h->rank != 0 && q != h->rank) continue;
+      const int peer = h->rank == 0 ? q : 0, rcv = h->rank == 0 ? 0 : 1;
+      xs.push_back(Xfer{peer, rcv, U(a), bytes});
+      if (with_t) xs.push_back(Xfer{peer, rcv, h->B[a].t, bytes});
+    }
+    if (h->trace) fprintf(stderr, "sr_fmg[rank %d]: broadcast level %d\n", h->rank, a);
+    const sr_status_t r = h->comm->group(h, xs.data(), (int)xs.size(), st);
+    if (r != SR_OK) h->sticky = r;
+    h->comm_calls[a]++;
+    h->exch++;
   }
   // u_A and R_A: the blocks written by this rank's restriction into the global level-A
   // arrays (k = 1 restriction when A = T, else the restriction from the decomposed A + 1)
@@ -1092,19 +1153,19 @@ struct Schedule {
       const bool pyr27 = pyr && b.global && h->restrict_pyr;
       srfmg::launch_resid27_fused<T>(L, U(l), scratch, frhs(b), st, pyr27 ? 1 : 0);
       srfmg::launch_restrict_from_resid<T>(L, U(l), scratch, h->L[l - 1], U(l - 1), rc, jr, st,
-                                           pyr27 ? fview(l - 1) : View<T>{});
+                                           pyr27 ? fview(l - 1, l > h->T) : View<T>{});
       return;
     }
     // SR levels (segment storage; per segment, so every partition runs it, R25): the
     // bulk-copy-fed bands when an instantiation fits
     if (l > h->T && h->restrict_seg && !L.st27 && (use_pyr || !b.global) &&
         srfmg::launch_restrict_seg<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), rc, jr, st,
-                                      use_pyr ? fview(l - 1) : View<T>{}))
+                                      use_pyr ? fview(l - 1, l > h->T) : View<T>{}))
       return;
     // the free ping-pong buffer of level l is scratch for the 27-point residual
     srfmg::launch_restrict<T>(h->L[l], U(l), b, h->L[l - 1], U(l - 1), rc, jr, st,
                               (T*)h->B[l].u[1 - h->B[l].cur],
-                              use_pyr ? fview(l - 1) : View<T>{});  // L113-115 / L233, L235
+                              use_pyr ? fview(l - 1, l > h->T) : View<T>{});  // L113-115 / L233, L235
   }
 
   void tau_from_rres(int lc, int jr) {  // the separate tau on R parked in rres
@@ -1157,7 +1218,11 @@ struct Schedule {
     // ghost ring for the tau instead
     if (h->world > 1 && l - 1 == h->A) gather_uR();
     if (dd(l - 1)) halo_u(l - 1);
-    if (cx(l - 1)) {  // conventional level: F = V = Omega (jr = 0)
+    // an idle rank (l - 1 == A, desc.coarse_idle) skips the tau and the coarse V-cycle:
+    // rank 0 runs them and sends w_A and t_A back
+    if (!solves_A() && l - 1 == h->A) {
+      // (nothing here: rank 0 forms the tau rhs and t_A)
+    } else if (cx(l - 1)) {  // conventional level: F = V = Omega (jr = 0)
       srfmg::COp<T> o = cop(srfmg::kCopTau, l - 1, l - 1);
       o.a = U(l - 1);
       o.c = (T*)h->B[l - 1].rhs;
@@ -1169,7 +1234,8 @@ struct Schedule {
     } else {
       tau_std(l - 1, jr);  // L116-117 / L234-236
     }
-    vcycle(l - 1, sview(l - 1));  // L117 / L237-240
+    if (solves_A() || l - 1 > h->A) vcycle(l - 1, sview(l - 1));  // L117 / L237-240
+    if (h->idle && l - 1 == h->A) bcast_A(true);  // w_A and t_A to the idle ranks
     if (up_on(l, b)) {
       up2(l, b, l == h->M);  // L241-242 in one pass (at l = M: the solve's last pass)
       return;
@@ -1255,7 +1321,7 @@ struct Schedule {
       }
       gather_f();
     }
-    for (int l = h->A; l >= 1; --l) {
+    for (int l = h->A; l >= 1 && solves_A(); --l) {
       const Lvl& L = h->L[l];
       if (l < M && cx(l)) {
         srfmg::COp<T> o = cop(srfmg::kCopPyramid, l, l - 1);
@@ -1269,9 +1335,12 @@ struct Schedule {
                                (T*)h->B[l - 1].fpyr, st);
     }
     pyr = true;
-    coarsest(fview(0));  // fig:fmg L137-138
-    for (int l = 1; l <= M; ++l)  // fig:fmg L139-142 (l <= T), fig:fmgsr L220-223 (l > T)
+    if (solves_A()) coarsest(fview(0));  // fig:fmg L137-138
+    for (int l = 1; l <= M; ++l) {  // fig:fmg L139-142 (l <= T), fig:fmgsr L220-223 (l > T)
+      if (l <= h->A && !solves_A()) continue;  // idle rank
+      if (h->idle && l == h->A + 1) bcast_A(false);  // u_A for the interpolation
       vcycle(l, fview(l), /*entry=*/true);
+    }
     if (!final_done) {
       const Lvl& L = h->L[M];
       Launch g(h, st, KC_GATHER, M, w * 2.0 * h->blk_n[0] * (double)h->blk_n[1] * h->blk_n[2]);
@@ -1577,6 +1646,10 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
   sr_fmg* h = new sr_fmg();
   h->d = *d;
   make_plan(h);
+  if (!plan_ok(h, msg)) {
+    delete h;
+    return fail(nullptr, SR_ERR_UNSUPPORTED_CONFIG, msg);
+  }
   for (int l = 1; l <= h->M; ++l) {
     const Lvl &Lf = h->L[l], &Lc = h->L[l - 1];
     if (l - 1 > h->T && Lc.J < (Lf.J + 1) / 2) {
@@ -1663,13 +1736,21 @@ sr_status_t sr_fmg_create_ex(const sr_fmg_desc_t* d, sr_fmg_t** out) {
         face = std::max(face, 2LL * (L.J + 1) * L.E[(i + 1) % 3] * L.E[(i + 2) % 3]);
     };
     for (int l = h->A + 1; l <= h->T; ++l) slab(h->L[l]);
-    if (h->A < h->T) slab(h->LT2);
+    if (h->A < h->T && h->K > 0) slab(h->LT2);
     h->hbytes = (size_t)std::max(face, 1LL) * h->esize;
     if (h->A < h->T) ok = ok && alloc(&h->hsend, h->hbytes) && alloc(&h->hrecv, h->hbytes);
   }
-  if (h->world > 1 && h->A < h->T)  // footprint copy of a decomposed level T
-    ok = ok && alloc(&h->wT2, (size_t)h->LT2.ss * h->esize) &&
-         alloc(&h->zT2, (size_t)h->LT2.ss * h->esize);
+  if (h->world > 1 && h->A < h->T) {
+    // zT2: the zero t of the corrections from w - t copies (dwt on the decomposed levels
+    // below T, the footprint copy wT2 of level T); wT2 only with SR levels above T
+    long long zs = 0;
+    for (int l = h->A + 1; l < h->T; ++l) zs = std::max(zs, h->L[l].ss);
+    if (h->K > 0) {
+      zs = std::max(zs, h->LT2.ss);
+      ok = ok && alloc(&h->wT2, (size_t)h->LT2.ss * h->esize);
+    }
+    ok = ok && alloc(&h->zT2, (size_t)std::max(zs, 1LL) * h->esize);
+  }
   std::vector<double> inv = coarsest_inverse(h->L[0]);
   const size_t n0sq = inv.size();
   ok = ok && alloc(&h->ainv, n0sq * h->esize);
@@ -1907,6 +1988,7 @@ sr_status_t sr_fmg_partition(const sr_fmg_desc_t* d, sr_fmg_partition_t* out) {
   sr_fmg tmp;
   tmp.d = *d;
   make_plan(&tmp);
+  if (!plan_ok(&tmp, msg)) return fail(nullptr, SR_ERR_UNSUPPORTED_CONFIG, msg);
   std::memset(out, 0, sizeof(*out));
   out->world = tmp.world;
   out->rank = tmp.rank;

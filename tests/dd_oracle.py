@@ -19,9 +19,13 @@ from oracle.ops import apply_A, cheb_constants, fill_bc_ghosts, prolong, residua
 
 
 class DDOracle(Oracle):
-    def __init__(self, cfg, part, pgrid):
+    def __init__(self, cfg, part, pgrid, idle=False):
         super().__init__(cfg)
         self.part, self.pgrid = part, pgrid
+        # idle coarse grid (desc.coarse_idle): the level-A blocks are
+        # gathered onto rank 0, which alone runs the levels <= A and sends u_A (and t_A)
+        # back; emulated for decomposed A < T (the agglomeration at T is the base vsr's)
+        self.idle = idle
         self.A = part["level_A"]
         self.world = int(np.prod(pgrid))
         self.rank = part["rank"]
@@ -99,13 +103,31 @@ class DDOracle(Oracle):
             self.n_exchanges += 1
 
     def gather(self, l, fields):
-        """All-gather of every rank's block of level l into the global fields."""
+        """All-gather of every rank's block of level l into the global fields (idle: a
+        gather onto rank 0 only)."""
         for fld in fields:
             mine = torch.from_numpy(np.ascontiguousarray(fld[self.blk(l)]))
-            got = [torch.empty_like(mine) for _ in range(self.world)]
-            dist.all_gather(got, mine)
+            if self.idle:
+                got = [torch.empty_like(mine) for _ in range(self.world)] if self.rank == 0 else None
+                dist.gather(mine, got, dst=0)
+                if self.rank != 0:
+                    continue
+            else:
+                got = [torch.empty_like(mine) for _ in range(self.world)]
+                dist.all_gather(got, mine)
             for q in range(self.world):
                 fld[self.blk(l, q)] = got[q].numpy()
+        self.n_exchanges += 1
+
+    def solves_A(self):
+        return not self.idle or self.rank == 0
+
+    def bcast(self, fields):
+        """Idle coarse grid: rank 0's whole arrays to every rank."""
+        for fld in fields:
+            buf = torch.from_numpy(np.ascontiguousarray(fld.a))
+            dist.broadcast(buf, src=0)
+            fld.a[...] = buf.numpy()
         self.n_exchanges += 1
 
     # -- the oracle's Chebyshev recurrence with an exchange before each application -------
@@ -158,7 +180,10 @@ class DDOracle(Oracle):
             fill_bc_ghosts(uc, domc)
             bc = Field(domc, fill=0.0)
             bc[Bc] = R[Bc] + apply_A(uc, Bc, hc, self.st, g)             # L117 (Eq. 4)
-        self.vconv(lc, bc)
+        if self.dd(lc) or self.solves_A():
+            self.vconv(lc, bc)
+        if self.idle and not self.dd(lc):
+            self.bcast((uc, t))                                          # w_A, t_A
         if self.dd(lc):
             self.halo(uc, lc)                                            # w on the ghosts
         e = Field(uc.box, array=uc.a - t.a)
@@ -167,10 +192,16 @@ class DDOracle(Oracle):
         self._dd_cheb(self.cfg.nu2, u, b, B, l)                          # L119
 
     def fmg_conventional(self):
+        assert not self.idle or self.A < self.T, "idle emulated for decomposed A < T only"
         u0 = self.u[0]
         u0[self.dom[0]] = 0.0
-        self.vconv(0, self.f[0])
+        if self.solves_A():
+            self.vconv(0, self.f[0])
         for l in range(1, self.T + 1):
+            if l <= self.A and not self.solves_A():
+                continue                                                 # idle rank
+            if self.idle and l == self.A + 1:
+                self.bcast((self.u[self.A],))                            # u_A for Pi
             src = self.u[l - 1]
             if self.dd(l - 1):
                 self.halo(src, l - 1)

@@ -96,13 +96,28 @@ def test_unsupported_configs():
 
 def test_multi_gpu_descriptor_validation():
     from paper_1406_7808_b200._lib import SR_ERR_INVALID_ARGUMENT, lib
-    for kw in (dict(world=2, pgrid=(2, 1, 1), sr_levels=0),     # multi-GPU needs SR levels
+    for kw in (dict(world=3, pgrid=(3, 1, 1), sr_levels=0),     # K = 0: 32 % 3 != 0
+               dict(world=2, pgrid=(2, 1, 1), coarse_idle=2),    # coarse_idle not 0/1
                dict(world=3, pgrid=(3, 1, 1)),                   # 2 segments per dim
                dict(world=2, pgrid=(1, 1, 1)),                   # world != prod(pgrid)
                dict(world=2, pgrid=(2, 1, 1), rank=2)):          # rank out of range
         d = _desc(**kw)
         h = ctypes.c_void_p()
         assert lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(h)) == SR_ERR_INVALID_ARGUMENT
+
+
+def test_conventional_multi_gpu_partition():
+    # K = 0 (conventional distributed FMG): pgrid blocks of the fine grid,
+    # no f halo, the finest level decomposed; rejected when the finest block < dd_min
+    from paper_1406_7808_b200 import partition
+    from paper_1406_7808_b200._lib import SR_ERR_UNSUPPORTED_CONFIG, lib
+    p = partition((64, 64, 64), 5, 0, 0, 0, 2, 1, (2, 1, 1), dd_min=8)
+    assert p["block_lo"] == (32, 0, 0) and p["block_n"] == (32, 64, 64)
+    assert p["f_halo"] == 0 and p["f_dims"] == (32, 64, 64)
+    assert p["level_A"] == 2            # 32 -> 16 -> 8 cells wide: levels 5, 4, 3 decomposed
+    d = _desc(n=(32, 32, 32), M=4, sr_levels=0, world=2, pgrid=(2, 1, 1), dd_min=32)
+    h = ctypes.c_void_p()
+    assert lib.sr_fmg_create_ex(ctypes.byref(d), ctypes.byref(h)) == SR_ERR_UNSUPPORTED_CONFIG
 
 
 def test_partition_and_nccl_id_need_no_gpu():

@@ -112,6 +112,64 @@ def test_ranks_equal_single_gpu(case, force, monkeypatch):
         s.close()
 
 
+VARIANTS = [
+    # name, n, M, seg, J, K, pgrid, dtype, dd_min, idle
+    # idle coarse grid (desc.coarse_idle): levels <= A on rank 0 alone
+    ("idle-agg-T", (64, 64, 64), 5, 8, 2, 2, (2, 1, 1), "f64", 0, True),
+    ("idle-dd-2x2x2", (128, 128, 128), 6, 32, 2, 2, (2, 2, 2), "f64", 4, True),
+    ("idle-dd-4x1x1-f32", (128, 32, 32), 5, 16, 2, 2, (4, 1, 1), "f32", 2, True),
+    # conventional distributed FMG (K = 0): the finest level decomposed,
+    # halo exchanges on every level down to A
+    ("K0-2x1x1", (64, 64, 64), 5, 0, 0, 0, (2, 1, 1), "f64", 8, False),
+    ("K0-2x2x2-idle", (64, 64, 64), 5, 0, 0, 0, (2, 2, 2), "f64", 8, True),
+    ("K0-4x1x1-f32", (128, 64, 64), 5, 0, 0, 0, (4, 1, 1), "f32", 8, False),
+    ("K0-1x2x2-big", (128, 128, 128), 6, 0, 0, 0, (1, 2, 2), "f64", 16, False),
+]
+
+
+@pytest.mark.timeout(150)
+@pytest.mark.parametrize("case", VARIANTS, ids=[c[0] for c in VARIANTS])
+def test_idle_and_conventional_ranks_equal_single_gpu(case):
+    name, n, M, seg, J, K, pgrid, dt, dd_min, idle = case
+    npd = np.float64 if dt == "f64" else np.float32
+    f = W.make_rhs("manufactured+noise", n).astype(npd)
+    with Solver(n, M, seg=seg, buffer=J, K=K, dtype=dt) as s1:
+        single = s1.solve(torch.from_numpy(f).cuda()).cpu().numpy()
+    ranks, outs, _ = run_ranks(n, M, seg, J, K, pgrid, f, dt, dd_min, solves=2,
+                               coarse_idle=idle)
+    T, A = ranks[0].T, ranks[0].level_A
+    if K == 0:
+        assert T == M and A < M, (name, A)   # the finest level is decomposed
+        assert ranks[0].f_halo == 0
+    launches = [s.launches_per_solve for s in ranks]
+    calls = [s.comm_calls() for s in ranks]
+    for r, s in enumerate(ranks):
+        assert np.array_equal(outs[r], s.block_of(single)), (name, r)
+        c = calls[r]
+        assert all(c[l] == 0 for l in range(T + 1, s.M + 1)), c
+        assert all(c[l] > 0 for l in range(A + 1, T + 1)), c
+        assert c[A] >= 1 and all(c[l] == 0 for l in range(A)), c
+    if idle:
+        # against the redundant coarse grid: the ranks other than 0 launch fewer kernels
+        # (none of the levels <= A) and level A carries one broadcast per gather besides
+        red, red_outs, _ = run_ranks(n, M, seg, J, K, pgrid, f, dt, dd_min, solves=1)
+        for r, s in enumerate(red):
+            assert np.array_equal(red_outs[r], outs[r]), (name, r)
+            if r > 0:
+                assert launches[r] < s.launches_per_solve, (launches, r)
+            assert calls[r][A] > s.comm_calls()[A], (calls[r], s.comm_calls())
+            s.close()
+    if dt == "f64":
+        ref = O.solve(f.astype(np.float64), O.Config(n=n, M=M, seg=seg, buffer=J, K=K))
+        full = np.zeros_like(ref)
+        for r, s in enumerate(ranks):
+            lo, nb = s.block_lo, s.block_n
+            full[lo[2]:lo[2] + nb[2], lo[1]:lo[1] + nb[1], lo[0]:lo[0] + nb[0]] = outs[r]
+        assert rel_l2(full, ref) <= 1e-11
+    for s in ranks:
+        s.close()
+
+
 @pytest.mark.timeout(150)
 def test_multirank_local_f_uses_halo_only():
     # f outside a rank's haloed block must not matter: perturb it and get the same block

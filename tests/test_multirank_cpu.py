@@ -35,6 +35,13 @@ CASES = {
     "dd-x": dict(n=(64, 32, 32), M=5, seg=16, buffer=2, K=2, pgrid=(2, 1, 1), dd_min=4),
     "dd-xy-J3": dict(n=(32, 32, 16), M=4, seg=8, buffer=3, K=1, pgrid=(2, 2, 1), dd_min=2),
     "dd-xyz": dict(n=(32, 32, 32), M=4, seg=8, buffer=2, K=1, pgrid=(2, 2, 2), dd_min=2),
+    # the idle coarse grid (levels <= A on rank 0 alone)
+    "dd-x-idle": dict(n=(64, 32, 32), M=5, seg=16, buffer=2, K=2, pgrid=(2, 1, 1), dd_min=4,
+                      idle=True),
+    # conventional distributed FMG (K = 0): the finest level decomposed too
+    "dd-K0-x": dict(n=(32, 16, 16), M=3, seg=8, buffer=2, K=0, pgrid=(2, 1, 1), dd_min=4),
+    "dd-K0-xyz-idle": dict(n=(32, 32, 32), M=4, seg=8, buffer=2, K=0, pgrid=(2, 2, 2), dd_min=4,
+                           idle=True),
 }
 
 
@@ -46,10 +53,10 @@ def _worker(rank, world, port, case, outq):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     c = CASES[case]
     part = partition(c["n"], c["M"], c["seg"], c["buffer"], c["K"], world, rank, c["pgrid"],
-                     dd_min=c["dd_min"])
+                     dd_min=c["dd_min"], coarse_idle=c.get("idle", False))
     f = W.make_rhs("manufactured+noise", c["n"])
     o = DDOracle(O.Config(n=c["n"], M=c["M"], seg=c["seg"], buffer=c["buffer"], K=c["K"]),
-                 part, c["pgrid"])
+                 part, c["pgrid"], idle=c.get("idle", False))
     u = o.solve(f)
     bl, bn = part["block_lo"], part["block_n"]
     outq.put((rank, (u[bl[2]:bl[2] + bn[2], bl[1]:bl[1] + bn[1], bl[0]:bl[0] + bn[0]].copy(),

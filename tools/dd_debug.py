@@ -24,6 +24,7 @@ ap.add_argument("--pgrid", default="4,1,1")
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--dd_min", type=int, default=2)
 ap.add_argument("--dump", type=float, default=60)
+ap.add_argument("--idle", type=int, default=0)
 a = ap.parse_args()
 n = tuple(int(v) for v in a.n.split(","))
 pg = tuple(int(v) for v in a.pgrid.split(","))
@@ -36,7 +37,7 @@ with Solver(n, a.M, seg=a.seg, buffer=a.J, K=a.K, dtype=a.dtype) as s1:
 print("single done", flush=True)
 store = HostStore(world)
 ranks = [Solver(n, a.M, seg=a.seg, buffer=a.J, K=a.K, dtype=a.dtype, world=world, rank=r,
-                pgrid=pg, host_store=store, dd_min=a.dd_min) for r in range(world)]
+                pgrid=pg, host_store=store, dd_min=a.dd_min, coarse_idle=bool(a.idle)) for r in range(world)]
 print("A", ranks[0].level_A, "T", ranks[0].T, "dd", ranks[0].dd_levels(), flush=True)
 fl = [torch.from_numpy(s.local_f(f)).cuda() for s in ranks]
 outs = [None] * world
@@ -57,4 +58,6 @@ for t in th:
 for t in th:
     t.join()
 for r, s in enumerate(ranks):
-    print("rank", r, "bitwise", np.array_equal(outs[r].cpu().numpy(), s.block_of(single)), flush=True)
+    o, b = outs[r].cpu().numpy(), s.block_of(single)
+    print("rank", r, "bitwise", np.array_equal(o, b), "max diff", float(np.abs(o - b).max()),
+          flush=True)
