@@ -749,6 +749,248 @@ __global__ void __launch_bounds__(SpecGeom<T, PY, BH, MAXS, RG, 2>::NT,
   }
 }
 
+// =====================================================================================
+// Packed fp32 degree-2 pass: k_cheb2l's plan, coefficients and rounding, with TWO
+// x-adjacent cells per thread (x0 = 2 t, x0 + 1) and the arithmetic of both in sm_100's
+// paired fp32 instructions (FADD2 / FFMA2 on float2).  The centre, next-plane, y-neighbour
+// and u1 accesses are 8-byte shared-memory words; the x-neighbours outside the pair, and
+// the rhs of a dense f (its TMA box starts at an odd column on the SR levels), are single
+// loads.  Per lane the operations and their order are exactly k_cheb2l's:
+//   sum = ((z- + z+) + (y- + y+)) + (x- + x+),  r = fma(ih2, sum, fma(-(d + dz), u, f)),
+//   u1 = fma(c0, r, u0),  u2 = fma(cr, r, fma(cm, u1 - u0, u1))
+// so the result is bitwise k_cheb2l's (c1 - u0 as fma(-1, u0, c1): exact, one rounding).
+// =====================================================================================
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 ld2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
+
+template <int PY, int BH, int MAXS, int RG>
+struct PackGeom {
+  using G = SpecGeom<float, PY, BH, MAXS, RG, 2>;
+  static constexpr int PX = PY / 2;        // threads per row group
+  static constexpr int NT = PX * G::NG;
+  static_assert(PY % 2 == 0, "pair layout needs an even row pitch");
+};
+
+template <int PY, int BH, int MAXS, int RG, int FIN = 0>
+__global__ void __launch_bounds__(PackGeom<PY, BH, MAXS, RG>::NT,
+                                  SpecGeom<float, PY, BH, MAXS, RG, 2>::MINB)
+    k_cheb2p(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ Cheb2Args<float> a) {
+  using G = SpecGeom<float, PY, BH, MAXS, RG, 2>;
+  using P = PackGeom<PY, BH, MAXS, RG>;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const Lvl& L = a.L;
+  const int Ex = L.E[0], Ey = L.E[1], Ez = L.E[2];
+  const long long pz = L.pz;
+  const int s = blockIdx.y;
+  const int r0 = blockIdx.x * BH, r1 = min(Ey, r0 + BH);
+  const int s0 = max(0, r0 - 1), s1 = min(Ey, r1 + 1);
+  const int q0 = max(0, r0 - 2), q1 = min(Ey, r1 + 2);
+  float* u0s = reinterpret_cast<float*>(sm);
+  float* fs = u0s + G::RU * G::U0S;
+  float* u1s = fs + G::RF * G::FS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(u1s + G::NU1 * G::U1S);
+
+  const int px = s % L.ns[0] + L.so[0];
+  const int pyy = (s / L.ns[0]) % L.ns[1] + L.so[1];
+  const int pzz = s / (L.ns[0] * L.ns[1]) + L.so[2];
+  const int ox = px * L.S[0] - (L.J + 1);
+  const int oy = pyy * L.S[1] - (L.J + 1);
+  const int oz = pzz * L.S[2] - (L.J + 1);
+  const float* useg = a.uin + (long long)s * L.ss;
+  float* oseg = a.uout + (long long)s * L.ss;
+  const float* rseg = RG ? nullptr : a.rhs_seg + (long long)s * L.ss;
+  const uint32_t u0_bytes = (uint32_t)((q1 - q0) * PY * sizeof(float));
+  const int oxt = ox - a.foff[0];
+  const int oxa = oxt & ~(G::kAl - 1);
+  const int fsh = RG ? oxt - oxa : 0;
+  const uint32_t f_bytes = RG ? (uint32_t)((BH + 2) * G::FP * sizeof(float))
+                              : (uint32_t)((s1 - s0) * PY * sizeof(float));
+  {  // zero every buffer once: dead slots read margin rows and rows no copy fills
+    const int nw = (int)((G::RU * G::U0S + G::RF * G::FS + G::NU1 * G::U1S) * sizeof(float) / 16);
+    uint4* z4 = reinterpret_cast<uint4*>(sm);
+    for (int i = threadIdx.x; i < nw; i += P::NT) z4[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < G::RU + G::RF; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  auto issue_u0 = [=](int z) {
+    const int sl = z % G::RU;
+    mbar_expect_tx(&bars[sl], u0_bytes);
+    bulk_g2s(u0s + sl * G::U0S + (q0 - s0 + 1) * PY, useg + (long long)z * pz + (long long)q0 * PY,
+             u0_bytes, &bars[sl]);
+  };
+  auto issue_f = [=, &fmap](int z) {
+    const int sl = z % G::RF;
+    mbar_expect_tx(&bars[G::RU + sl], f_bytes);
+    if (RG)
+      tma_3d(fs + sl * G::FS, &fmap, oxa, oy + s0 - a.foff[1], oz + z - a.foff[2],
+             &bars[G::RU + sl]);
+    else
+      bulk_g2s(fs + sl * G::FS, rseg + (long long)z * pz + (long long)s0 * PY, f_bytes,
+               &bars[G::RU + sl]);
+  };
+  if (threadIdx.x == 0) {
+    for (int z = 0; z < min(G::RU, Ez); ++z) issue_u0(z);
+    for (int z = 0; z < min(3, Ez); ++z) issue_f(z);
+  }
+
+  const int x0 = 2 * (threadIdx.x % P::PX), g = threadIdx.x / P::PX;
+  const int y0 = s0 + g * MAXS;
+  const float ih2 = float(L.inv_h2);
+  // per slot and lane: the step coefficients (0 on dead cells), minus the scaled diagonal
+  float2 c0k[MAXS], crk[MAXS], ndk[MAXS];
+  bool wr[MAXS];
+  unsigned gen_mask = 0;  // FIN: bit 2k + j = genuine cell (slot k, lane j)
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    const int y = y0 + k;
+    const int gy = oy + y;
+    float cc[2], rr[2], dd[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int x = x0 + j, gx = ox + x;
+      const bool tin = x < Ex && gx >= 0 && gx < L.N[0];
+      const bool c = tin && x >= 1 && x <= Ex - 2 && y < s1 && y >= 1 && y <= Ey - 2 && gy >= 0 &&
+                     gy < L.N[1];
+      cc[j] = c ? a.c0 : 0.f;
+      rr[j] = c ? a.cr : 0.f;
+      const int nb = 6 + (gx == 0) + (gx == L.N[0] - 1) + (gy == 0) + (gy == L.N[1] - 1);
+      dd[j] = -(float(nb) * ih2);
+      if constexpr (FIN == 1) {
+        const int vlo = L.J + 1;
+        if (y >= r0 && y < r1 && y0 < s1 && tin && gy >= 0 && gy < L.N[1] && x >= vlo &&
+            x < vlo + L.S[0] && y >= vlo && y < vlo + L.S[1])
+          gen_mask |= 1u << (2 * k + j);
+      }
+    }
+    c0k[k] = make_float2(cc[0], cc[1]);
+    crk[k] = make_float2(rr[0], rr[1]);
+    ndk[k] = make_float2(dd[0], dd[1]);
+    wr[k] = y >= r0 && y < r1 && y0 < s1;
+  }
+  float* fbase = nullptr;
+  if constexpr (FIN == 1)
+    fbase = a.fin.p + (long long)(oy + y0 - a.fin.bo[1]) * a.fin.sy + (ox + x0 - a.fin.bo[0]);
+  const float* const u0b = u0s + (y0 - s0 + 1) * PY + x0;
+  const float* const fb = fs + (y0 - s0) * G::FP + x0 + fsh;
+  float* const u1b = u1s + (y0 - s0 + 1) * PY + x0;
+  float* const ob = oseg + (long long)y0 * PY + x0;
+  auto ldf = [&](const float* p) {  // rhs pair: 8-byte aligned only for segment storage
+    if constexpr (RG) return make_float2(p[0], p[1]);
+    else return ld2(p);
+  };
+  float2 u0q[MAXS][3], u1q[MAXS][3];
+  mbar_wait(&bars[0], 0);
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    u0q[k][0] = ld2(u0b + k * PY);
+    u0q[k][1] = u0q[k][2] = make_float2(0.f, 0.f);
+    u1q[k][0] = u1q[k][1] = u1q[k][2] = make_float2(0.f, 0.f);
+  }
+  const float2 cm2 = make_float2(a.cm, a.cm), ih2v = make_float2(ih2, ih2);
+  const float2 mone = make_float2(-1.f, -1.f);
+
+  auto step = [&](auto RR, int z) {
+    constexpr int R = decltype(RR)::value;  // z % 3: u0 ring slot, u1 buffer, queue slot
+    constexpr int IM = (R + 2) % 3, I0 = R, IP = (R + 1) % 3;
+    if (z < Ez) {
+      if (z + 1 < Ez) mbar_wait(&bars[(z + 1) % G::RU], ((z + 1) / G::RU) & 1);
+      mbar_wait(&bars[G::RU + z % G::RF], (z / G::RF) & 1);
+      const float* pl = u0b + (z % G::RU) * G::U0S;
+      const float* pn = u0b + ((z + 1) % G::RU) * G::U0S;
+      const float* fp = fb + (z % G::RF) * G::FS;
+      float* u1w = u1b + R * G::U1S;
+      const int gz = oz + z;
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k)
+        u0q[k][IP] = (z + 1 < Ez) ? ld2(pn + k * PY) : make_float2(0.f, 0.f);
+      if (gz >= 0 && gz < L.N[2] && z >= 1 && z <= Ez - 2) {  // uniform: C planes
+        const float ndz = -(float((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0)) * ih2);
+        const float2 ndz2 = make_float2(ndz, ndz);
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) {
+          const float2 v0 = u0q[k][I0];
+          const float2 ym = (k == 0) ? ld2(pl - PY) : u0q[k > 0 ? k - 1 : 0][I0];
+          const float2 yp = (k == MAXS - 1) ? ld2(pl + MAXS * PY) : u0q[k + 1 < MAXS ? k + 1 : k][I0];
+          const float2 xs = f2add(make_float2(pl[k * PY - 1], v0.x), make_float2(v0.y, pl[k * PY + 2]));
+          const float2 sum = f2add(f2add(f2add(u0q[k][IM], u0q[k][IP]), f2add(ym, yp)), xs);
+          const float2 r = f2fma(ih2v, sum, f2fma(f2add(ndk[k], ndz2), v0, ldf(fp + k * G::FP)));
+          const float2 v1 = f2fma(c0k[k], r, v0);
+          u1q[k][I0] = v1;
+          st2(u1w + k * PY, v1);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) {
+          u1q[k][I0] = u0q[k][I0];
+          st2(u1w + k * PY, u0q[k][I0]);
+        }
+      }
+    }
+    __syncthreads();  // the only barrier of the plane step
+    if (threadIdx.x == 0) {
+      if (z + G::RU < Ez) issue_u0(z + G::RU);  // u0 slot of plane z is free
+      if (z >= 1 && z + 2 < Ez) issue_f(z + 2);  // rhs slot of plane z-2 is free
+    }
+    if (z >= 1) {
+      const int zz = z - 1;
+      const int gz = oz + zz;
+      if (gz >= 0 && gz < L.N[2]) {
+        constexpr int J2 = (R + 1) % 3, J1 = (R + 2) % 3, J0 = R;
+        float2 v2[MAXS];
+        if (zz >= 1 && zz <= Ez - 2) {  // uniform: C planes
+          const float ndz = -(float((gz == 0 ? 1 : 0) + (gz == L.N[2] - 1 ? 1 : 0)) * ih2);
+          const float2 ndz2 = make_float2(ndz, ndz);
+          const float* u1r = u1b + J1 * G::U1S;
+          const float* fp = fb + (zz % G::RF) * G::FS;
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k) {
+            const float2 u0v = u0q[k][J1];
+            const float2 c1 = u1q[k][J1];
+            const float2 ym = (k == 0) ? ld2(u1r - PY) : u1q[k > 0 ? k - 1 : 0][J1];
+            const float2 yp = (k == MAXS - 1) ? ld2(u1r + MAXS * PY) : u1q[k + 1 < MAXS ? k + 1 : k][J1];
+            const float2 xs =
+                f2add(make_float2(u1r[k * PY - 1], c1.x), make_float2(c1.y, u1r[k * PY + 2]));
+            const float2 sum = f2add(f2add(f2add(u1q[k][J2], u1q[k][J0]), f2add(ym, yp)), xs);
+            const float2 r = f2fma(ih2v, sum, f2fma(f2add(ndk[k], ndz2), c1, ldf(fp + k * G::FP)));
+            v2[k] = f2fma(crk[k], r, f2fma(cm2, f2fma(mone, u0v, c1), c1));
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k) v2[k] = u0q[k][J1];
+        }
+        if constexpr (FIN != 1) {
+          float* orow = ob + (long long)zz * pz;
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k)
+            if (wr[k]) st2(orow + k * PY, v2[k]);
+        } else {
+          // last pass: genuine cells of a genuine plane go to the user's u (R19); the user
+          // row's column parity is arbitrary, so the two lanes store separately
+          if (zz >= L.J + 1 && zz < L.J + 1 + L.S[2]) {
+            float* frow = fbase + (long long)(gz - a.fin.bo[2]) * a.fin.sz;
+#pragma unroll
+            for (int k = 0; k < MAXS; ++k) {
+              if ((gen_mask >> (2 * k)) & 1u) frow[k * a.fin.sy] = v2[k].x;
+              if ((gen_mask >> (2 * k + 1)) & 1u) frow[k * a.fin.sy + 1] = v2[k].y;
+            }
+          }
+        }
+      }
+    }
+  };
+  for (int zb = 0; zb <= Ez; zb += 3) {
+    step(std::integral_constant<int, 0>{}, zb);
+    if (zb + 1 <= Ez) step(std::integral_constant<int, 1>{}, zb + 1);
+    if (zb + 2 <= Ez) step(std::integral_constant<int, 2>{}, zb + 2);
+  }
+}
+
 // ---- host side ---------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -894,6 +1136,38 @@ bool try_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaS
   return true;
 }
 
+// packed fp32 pass (k_cheb2p) for the plain and last degree-2 passes; SR_FMG_CHEB_PACK=0
+// restores the scalar lean pass (A/B; the results are bitwise the same)
+bool packed() {  // read per launch (a captured solve keeps the choice it was captured with)
+  const char* e = std::getenv("SR_FMG_CHEB_PACK");
+  return !(e && e[0] == '0');
+}
+template <int PY, int BH, int MAXS>
+bool try_pack(const Lvl& L, const Cheb2Args<float>& a, FusedRhs<float> b, int nst, cudaStream_t st) {
+  if (!packed() || nst != 2 || a.tout || L.py != PY || L.E[0] > PY) return false;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  dim3 grid((L.E[1] + BH - 1) / BH, L.nsegs);
+  auto go = [&](auto kern, size_t smem, int nt) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, nt, smem, st>>>(map, a);
+  };
+  const bool fin = a.fin.p != nullptr;
+  if (b.global) {
+    using G = SpecGeom<float, PY, BH, MAXS, 1, 2>;
+    using P = PackGeom<PY, BH, MAXS, 1>;
+    if (!encode_rhs_map<float>(&map, b, G::FP, BH + 2)) return false;
+    if (fin) go(k_cheb2p<PY, BH, MAXS, 1, 1>, G::SMEM, P::NT);
+    else go(k_cheb2p<PY, BH, MAXS, 1, 0>, G::SMEM, P::NT);
+  } else {
+    using G = SpecGeom<float, PY, BH, MAXS, 0, 2>;
+    using P = PackGeom<PY, BH, MAXS, 0>;
+    if (fin) go(k_cheb2p<PY, BH, MAXS, 0, 1>, G::SMEM, P::NT);
+    else go(k_cheb2p<PY, BH, MAXS, 0, 0>, G::SMEM, P::NT);
+  }
+  return true;
+}
+
 template <class T>
 bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
   // Band shapes per row pitch, measured (C3, DESIGN.md §9 keeps the losing ones):
@@ -907,7 +1181,10 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
            try_spec<T, 136, 14, 4>(L, a, b, nst, st) || try_spec<T, 24, 22, 3>(L, a, b, nst, st) ||
            try_spec<T, 16, 14, 2>(L, a, b, nst, st);
   else
-    return try_spec<T, 72, 14, 8>(L, a, b, nst, st) || try_spec<T, 40, 22, 8>(L, a, b, nst, st) ||
+    // packed fp32 pass at E = 70 (C3 finest pair 0.903 -> 0.862 ms); at E = 38 the 20-thread
+    // row groups straddle warps more often and it measures no faster (0.376 vs 0.373 ms)
+    return try_pack<72, 14, 4>(L, a, b, nst, st) ||
+           try_spec<T, 72, 14, 8>(L, a, b, nst, st) || try_spec<T, 40, 22, 8>(L, a, b, nst, st) ||
            try_spec<T, 136, 14, 4>(L, a, b, nst, st) || try_spec<T, 24, 22, 3>(L, a, b, nst, st) ||
            try_spec<T, 16, 14, 2>(L, a, b, nst, st);
 }

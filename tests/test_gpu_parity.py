@@ -373,6 +373,32 @@ def test_fused_and_step_kernels_agree(dtype, force, monkeypatch):
     assert rel_l2(a, b) <= (1e-13 if dtype == "f64" else 1e-5)
 
 
+PACK_CASES = [
+    # name, n, M, seg, J, K: E = 70 and 38 boxes (dense f), the tau-fed passes (segment rhs),
+    # the last pass into the user's u; odd and even buffer widths
+    ("S64-J2", (128, 128, 128), 6, 64, 2, 2),
+    ("S32-J2", (128, 128, 128), 6, 32, 2, 3),
+    ("S64-J1-noncubic", (128, 64, 192), 5, 64, 1, 2),
+    ("S32-J3", (64, 64, 64), 5, 32, 3, 2),
+]
+
+
+@pytest.mark.parametrize("case", PACK_CASES, ids=[c[0] for c in PACK_CASES])
+def test_packed_fp32_pass_bitwise(case, monkeypatch):
+    # the packed fp32 degree-2 pass (k_cheb2p: FADD2/FFMA2 on x pairs) performs k_cheb2l's
+    # operations in k_cheb2l's order per cell: the solves are bitwise equal
+    name, n, M, seg, J, K = case
+    f = torch.from_numpy(W.make_rhs("manufactured+noise", n).astype(np.float32)).cuda()
+    monkeypatch.setenv("SR_FMG_FORCE_FUSED", "1")
+    monkeypatch.setenv("SR_FMG_CHEB_PACK", "1")
+    with Solver(n, M, seg=seg, buffer=J, K=K, dtype="f32") as s:
+        a = s.solve(f).cpu().numpy()
+    monkeypatch.setenv("SR_FMG_CHEB_PACK", "0")
+    with Solver(n, M, seg=seg, buffer=J, K=K, dtype="f32") as s:
+        b = s.solve(f).cpu().numpy()
+    assert np.array_equal(a, b), (name, float(np.abs(a - b).max()))
+
+
 # FMG entry Pi + S^1 in one TMA pass (pset.cu) vs prolongation + degree-1 step: the buffer
 # widths J = 0..3 give every residue of the storage origin mod 4 (fine row pairs vs coarse
 # rows in y, fine plane pairs vs coarse planes in z)
