@@ -82,6 +82,9 @@ bool cheb2_fused_ok(const Lvl& L);
 // TMA-fed prolongation (prolong.cu): u_f = P(w) (add = 0) or u_f += P(w - t) (add = 1)
 template <class T>
 bool prolong_tma_ok(const Lvl& Lf, const Lvl& Lc);
+// the TMA prolongation's band plan fits (row width, shared memory for the coarse rows)
+template <class T>
+bool prolong_tma_fits(const Lvl& Lf, const Lvl& Lc);
 template <class T>
 void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
                         cudaStream_t st);

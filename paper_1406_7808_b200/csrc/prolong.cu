@@ -215,21 +215,14 @@ __global__ void __launch_bounds__(MAXS == 6 ? 512 : 1024, 1)
 
 }  // namespace
 
+// band plan of the TMA prolongation: rows per thread, band height, shared memory
+struct TmaBandPlan {
+  int maxs, nb, BH;
+  long long cstride, fstride;
+  size_t smem;
+};
 template <class T>
-bool prolong_tma_ok(const Lvl& Lf, const Lvl& Lc) {
-  (void)Lc;
-  // enough bands to fill the GPU, counted over the GLOBAL segment grid so that every world
-  // size picks the same kernel (R25)
-  long long g = 1;
-  for (int i = 0; i < 3; ++i) g *= Lf.N[i] / Lf.S[i];
-  // one thread per row column and MAXS rows: rows up to 136 wide keep a band within the
-  // 1024-thread CTA limit (E = 262 boxes, e.g. 256^3 segments, take the column kernel)
-  return Lf.py <= 136 && g * ((Lf.E[1] + 17) / 18) >= 148;
-}
-
-template <class T>
-void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
-                        cudaStream_t st) {
+TmaBandPlan prolong_plan(const Lvl& Lf, const Lvl& Lc) {
   // measured at C3: 18-row bands at E = 70 (0.55 ms; 10: 0.61, 24: 0.66), two 19-row bands at
   // E = 38 (0.22 ms for the level's two launches; three of 13: 0.24).  SR_FMG_PROLONG_MAXS
   // (3 or 6 rows per thread) and SR_FMG_PROLONG_BH (target band height): tuning knobs
@@ -241,12 +234,44 @@ void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T
     const char* e = std::getenv("SR_FMG_PROLONG_BH");
     return e ? std::atoi(e) : 0;
   }();
+  TmaBandPlan p{};
   // 6 rows per thread from E = 22 on (C3, fp64: finest correction 0.515 vs 0.538 ms, level 7
   // 0.207 vs 0.221; fp32 finest 0.311 vs 0.416 ms), 3 on the E = 14 boxes (0.074 vs 0.090)
-  const int MAXS = maxs_env ? (maxs_env == 6 ? 6 : 3) : (Lf.E[1] >= 22 ? 6 : 3);
+  p.maxs = maxs_env ? (maxs_env == 6 ? 6 : 3) : (Lf.E[1] >= 22 ? 6 : 3);
   const int tgt = bh_env > 0 ? bh_env : (Lf.E[1] <= 40 ? 24 : 18);
-  const int nb = (Lf.E[1] + tgt - 1) / tgt;
-  const int BH = (Lf.E[1] + nb - 1) / nb;
+  p.nb = (Lf.E[1] + tgt - 1) / tgt;
+  p.BH = (Lf.E[1] + p.nb - 1) / p.nb;
+  const int crows = p.BH / 2 + 3;
+  const int A = 128 / (int)sizeof(T);
+  p.cstride = ((long long)crows * Lc.py + A - 1) / A * A;
+  p.fstride = ((long long)p.BH * Lf.py + A - 1) / A * A;
+  p.smem = (size_t)(2 * kRC * p.cstride + kRF * p.fstride) * sizeof(T) + 8 * (kRC + kRF);
+  return p;
+}
+
+template <class T>
+bool prolong_tma_fits(const Lvl& Lf, const Lvl& Lc) {
+  return Lf.py <= 136 && prolong_plan<T>(Lf, Lc).smem <= 227 * 1024;
+}
+
+template <class T>
+bool prolong_tma_ok(const Lvl& Lf, const Lvl& Lc) {
+  // enough bands to fill the GPU, counted over the GLOBAL segment grid so that every world
+  // size picks the same kernel (R25)
+  long long g = 1;
+  for (int i = 0; i < 3; ++i) g *= Lf.N[i] / Lf.S[i];
+  // one thread per row column and MAXS rows: rows up to 136 wide keep a band within the
+  // 1024-thread CTA limit (E = 262 boxes, e.g. 256^3 segments, take the column kernel); the
+  // coarse rows are staged whole, so a wide coarse level (the first SR level over a large
+  // conventional level T, e.g. C5 with K = 2) can exceed shared memory: column kernel
+  return g * ((Lf.E[1] + 17) / 18) >= 148 && prolong_tma_fits<T>(Lf, Lc);
+}
+
+template <class T>
+void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T* t, int add,
+                        cudaStream_t st) {
+  const TmaBandPlan pp = prolong_plan<T>(Lf, Lc);
+  const int MAXS = pp.maxs, nb = pp.nb, BH = pp.BH;
   ProlongArgs<T> a{};
   a.Lf = Lf;
   a.Lc = Lc;
@@ -255,11 +280,9 @@ void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T
   a.t = t;
   a.add = add;
   a.BH = BH;
-  const int crows = BH / 2 + 3;
-  const int A = 128 / (int)sizeof(T);
-  a.cstride = (crows * Lc.py + A - 1) / A * A;
-  a.fstride = (BH * Lf.py + A - 1) / A * A;
-  const size_t smem = (size_t)(2 * kRC * a.cstride + kRF * a.fstride) * sizeof(T) + 8 * (kRC + kRF);
+  a.cstride = (int)pp.cstride;
+  a.fstride = (int)pp.fstride;
+  const size_t smem = pp.smem;
   const int NT = Lf.py * ((BH + MAXS - 1) / MAXS);
   // compile-time pitches for the C3-type boxes (E = 70, 38 over a coarse SR level)
   const int pyc = (Lf.py == 72 || Lf.py == 40) && Lc.py == Lf.py / 2 + 4 ? Lf.py : 0;
@@ -280,6 +303,8 @@ void launch_prolong_tma(const Lvl& Lf, T* uf, const Lvl& Lc, const T* w, const T
 }
 
 template bool prolong_tma_ok<double>(const Lvl&, const Lvl&);
+template bool prolong_tma_fits<double>(const Lvl&, const Lvl&);
+template bool prolong_tma_fits<float>(const Lvl&, const Lvl&);
 template bool prolong_tma_ok<float>(const Lvl&, const Lvl&);
 template void launch_prolong_tma<double>(const Lvl&, double*, const Lvl&, const double*,
                                          const double*, int, cudaStream_t);

@@ -895,9 +895,10 @@ struct Schedule {
     const T* tc = fp ? (const T*)h->zT2 : tsrc;
     Launch g(h, st, KC_PROLONG, l,
              w * (add ? 2.0 : 1.0) * c.cg + w * (add ? 2.0 : 1.0) * h->cells[l - 1].cg / 8.0);
-    if (h->fused && h->L[l].py <= 136 &&
-        (h->force || (srfmg::prolong_tma_ok<T>(h->L[l], h->L[l - 1]) &&
-                                  h->L[l].E[1] >= h->fused_min_e)))
+    // (decided on the single-GPU shape of the coarse level, R25; the rank's block must fit too)
+    const Lvl Lg = glob(l - 1);
+    if (h->fused && srfmg::prolong_tma_fits<T>(h->L[l], Lg) && srfmg::prolong_tma_fits<T>(h->L[l], Lc) &&
+        (h->force || (srfmg::prolong_tma_ok<T>(h->L[l], Lg) && h->L[l].E[1] >= h->fused_min_e)))
       srfmg::launch_prolong_tma<T>(h->L[l], U(l), Lc, wc, tc, add, st);
     else
       srfmg::launch_prolong<T>(h->L[l], U(l), Lc, wc, tc, add, st);

@@ -550,6 +550,30 @@ def test_c5_shapes_at_256_match_oracle(case):
     assert rel_l2(u, ref) <= TOL64, (name, rel_l2(u, ref))
 
 
+def test_wide_coarse_level_under_first_sr_level_matches_oracle():
+    # K = 2 over a long level T (256 x 64 x 64): the TMA correction would stage coarse rows
+    # of 264 doubles, more shared memory than a CTA has -- the column kernel takes it (C5
+    # with K = 2 at 1024^3 has the same shape: level T 256^3)
+    n, M, seg, J, K = (1024, 256, 256), 8, 128, 2, 2
+    f = W.make_rhs("bumps", n)
+    ref = _oracle("bumps", f, n, M, seg, J, K)
+    u = _gpu_solve(f, n=n, M=M, seg=seg, buffer=J, K=K)
+    assert rel_l2(u, ref) <= TOL64, rel_l2(u, ref)
+
+
+@pytest.mark.parametrize("seg,K", [(128, 2), (128, 3), (128, 5), (32, 2), (32, 3), (32, 5)])
+def test_c5_full_size_sr_level_sweep_runs(seg, K):
+    # BASELINE configs[4]'s sweep of the SR level count at full size (1024^3, fp64): every
+    # (S, K) solves; the solve is linear (u(2 f) = 2 u(f) bitwise) and finite
+    n, M = (1024, 1024, 1024), 9
+    f1 = _bumps_on_device(n, 1.0 / n[0])
+    with Solver(n, M, seg=seg, buffer=2, K=K) as s:
+        u1 = s.solve(f1)
+        u2 = s.solve(2.0 * f1)
+        assert torch.isfinite(u1).all()
+        assert torch.equal(u2, 2.0 * u1)
+
+
 @pytest.mark.parametrize("dd_min", [0, 1 << 20])
 def test_c4_two_ranks_full_size_equal_single_gpu(dd_min):
     # BASELINE configs[3] (C4) at 2 GPUs: global 1024 x 512 x 512, h = 1/512, R = (2,1,1),
