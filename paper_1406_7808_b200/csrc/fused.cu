@@ -1168,23 +1168,16 @@ bool try_pack(const Lvl& L, const Cheb2Args<float>& a, FusedRhs<float> b, int ns
   return true;
 }
 
-// A/B knob: split the small boxes (E = 22, 14) into two bands (more CTAs per SM for the
-// latency-bound levels); read per launch
-bool small_split() {
-  const char* e = std::getenv("SR_FMG_SMALL_SPLIT");
-  return e && e[0] == '1';
-}
-
 template <class T>
 bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cudaStream_t st) {
-  if (small_split() && (try_spec<T, 24, 11, 3>(L, a, b, nst, st) || try_spec<T, 16, 7, 2>(L, a, b, nst, st)))
-    return true;
   // Band shapes per row pitch, measured (C3, DESIGN.md §9 keeps the losing ones):
   //  E = 70 (64^3 segments): 14-row bands; fp64 4 cells per thread (0.77 vs 0.85 ms for 2
   //    bands of 35), fp32 8 cells per thread (finest pair 0.991 vs 1.032 ms for 10 of 4);
   //  E = 38 (32^3): fp64 19-row bands of 3 cells (0.60 ms; 22 of 6: 0.71, 16 of 6: 0.73,
   //    22 of 8: 0.76), fp32 22 of 8 (0.38; 14 of 8: 0.45, 38 of 8: 0.57);
-  //  E = 134 (128^3, C5): 14-row bands of 544 threads, one CTA per SM (6-row bands slower).
+  //  E = 134 (128^3, C5): 14-row bands of 544 threads, one CTA per SM (6-row bands slower);
+  //  E = 22 / 14: one band per segment (two bands of 11 / 7 rows: level 6 0.213 -> 0.299 ms,
+  //    level 5 0.139 -> 0.158 ms per solve; fp32 likewise slower).
   if constexpr (sizeof(T) == 8)
     return try_spec<T, 72, 14, 4>(L, a, b, nst, st) || try_spec<T, 40, 19, 3>(L, a, b, nst, st) ||
            try_spec<T, 136, 14, 4>(L, a, b, nst, st) || try_spec<T, 24, 22, 3>(L, a, b, nst, st) ||

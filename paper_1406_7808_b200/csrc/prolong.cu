@@ -238,10 +238,8 @@ TmaBandPlan prolong_plan(const Lvl& Lf, const Lvl& Lc) {
   // 6 rows per thread from E = 22 on (C3, fp64: finest correction 0.515 vs 0.538 ms, level 7
   // 0.207 vs 0.221; fp32 finest 0.311 vs 0.416 ms), 3 on the E = 14 boxes (0.074 vs 0.090)
   p.maxs = maxs_env ? (maxs_env == 6 ? 6 : 3) : (Lf.E[1] >= 22 ? 6 : 3);
-  const char* ss = std::getenv("SR_FMG_SMALL_SPLIT");  // A/B: two bands on E <= 22 boxes
-  const int tgt = bh_env > 0 ? bh_env
-                  : (ss && ss[0] == '1' && Lf.E[1] <= 22) ? (Lf.E[1] + 1) / 2
-                  : (Lf.E[1] <= 40 ? 24 : 18);
+  // (two bands on the E <= 22 boxes: slower, level 6 0.088 -> 0.111 ms per solve)
+  const int tgt = bh_env > 0 ? bh_env : (Lf.E[1] <= 40 ? 24 : 18);
   p.nb = (Lf.E[1] + tgt - 1) / tgt;
   p.BH = (Lf.E[1] + p.nb - 1) / p.nb;
   const int crows = p.BH / 2 + 3;
