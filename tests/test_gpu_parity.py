@@ -574,45 +574,47 @@ def test_c5_full_size_sr_level_sweep_runs(seg, K):
         assert torch.equal(u2, 2.0 * u1)
 
 
-@pytest.mark.parametrize("dd_min", [0, 1 << 20])
-def test_c4_two_ranks_full_size_equal_single_gpu(dd_min):
-    # BASELINE configs[3] (C4) at 2 GPUs: global 1024 x 512 x 512, h = 1/512, R = (2,1,1),
-    # manufactured f, 64^3 segments, J = 2, K = 4, M = 8 (coarsest 4 x 2 x 2).  Both ranks run
-    # on this GPU, one host thread each, through the host-store backend (no rank waits on
-    # another inside a kernel); each rank's block must equal the single-GPU solve of the same
-    # global problem.  dd_min = 0 (default): level T (32^3 per rank) is domain-decomposed with
-    # halo exchanges and level 3 is gathered; 2^20: level T itself is gathered.
+@pytest.mark.parametrize("world,dd_min", [(2, 0), (2, 1 << 20), (4, 0), (8, 0), (8, 1 << 20)])
+def test_c4_ranks_full_size_equal_single_gpu(world, dd_min):
+    # BASELINE configs[3] (C4) at the driver's scaling sizes: 512^3 per rank, global (512 P1,
+    # 512 P2, 512 P3) with pgrid (2,1,1) / (2,2,1) / (2,2,2), h = 1/512, R = pgrid, manufactured
+    # f, 64^3 segments, J = 2, K = 4, M = 8.  Every rank runs on this GPU, one host thread each,
+    # through the host-store backend (no rank waits on another inside a kernel); each rank's
+    # block must equal the single-GPU solve of the same global problem (up to 1024^3 at 8).
+    # dd_min = 0 (default): level T (32^3 per rank) is domain-decomposed with halo exchanges;
+    # 2^20: level T itself is gathered.
     import threading
 
     from paper_1406_7808_b200 import HostStore
-    n, M, seg, J, K, pgrid, h = (1024, 512, 512), 8, 64, 2, 4, (2, 1, 1), 1.0 / 512
+    pgrid = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}[world]
+    n = tuple(512 * p for p in pgrid)
+    M, seg, J, K, h = 8, 64, 2, 4, 1.0 / 512
     R = W.extents(n, h)
     with Solver(n, M, seg=seg, buffer=J, K=K, h=h) as s1:
         f = torch.from_numpy(W.manufactured_f_block(h, R, (0, 0, 0), n)).cuda()
-        single = s1.solve(f)
+        single = s1.solve(f).cpu()
         del f
-    store = HostStore(2)
-    ranks = [Solver(n, M, seg=seg, buffer=J, K=K, h=h, world=2, rank=r, pgrid=pgrid,
-                    host_store=store, dd_min=dd_min) for r in range(2)]
+    store = HostStore(world)
+    ranks = [Solver(n, M, seg=seg, buffer=J, K=K, h=h, world=world, rank=r, pgrid=pgrid,
+                    host_store=store, dd_min=dd_min) for r in range(world)]
     assert (ranks[0].level_A < ranks[0].T) == (dd_min == 0)
-    fl = []
-    for s in ranks:
-        lo = [s.block_lo[d] - s.f_halo for d in range(3)]
-        dims = [s.block_n[d] + 2 * s.f_halo for d in range(3)]
-        fl.append(torch.from_numpy(W.manufactured_f_block(h, R, lo, dims)).cuda())
-    outs, errs = [None, None], []
+    outs, errs = [None] * world, []
 
     def work(r):
         try:
             torch.cuda.set_device(0)
+            s = ranks[r]
+            lo = [s.block_lo[d] - s.f_halo for d in range(3)]
+            dims = [s.block_n[d] + 2 * s.f_halo for d in range(3)]
+            fl = torch.from_numpy(W.manufactured_f_block(h, R, lo, dims)).cuda()
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
-                outs[r] = ranks[r].solve(fl[r])
+                outs[r] = s.solve(fl).cpu()
             st.synchronize()
         except Exception as e:
             errs.append((r, e))
 
-    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
     for t in th:
         t.start()
     for t in th:
