@@ -63,7 +63,21 @@ __device__ __forceinline__ T apply_A(const Lvl& L, const T* __restrict__ u, long
   return (T(6) * c - s) * T(L.inv_h2) + T(L.nlg) * c * c * c;
 }
 
+// Index math of the operations: every executor operation is a short dependent chain per
+// thread, so the divisions by run-time extents (~15 instructions each) are a visible part of
+// an operation's latency.  Extents that are powers of two (all of the BASELINE grids) take
+// shifts and masks instead; the mapping is the same, so the results are too.
+__device__ __forceinline__ bool pow2(int v) { return (v & (v - 1)) == 0; }
+__device__ __forceinline__ int lg2(int v) { return __ffs(v) - 1; }  // v a power of two
+
 __device__ __forceinline__ void cell_of(int i, const int n[3], int& x, int& y, int& z) {
+  if (pow2(n[0]) && pow2(n[1])) {
+    const int l0 = lg2(n[0]), l1 = lg2(n[1]);
+    x = i & (n[0] - 1);
+    y = (i >> l0) & (n[1] - 1);
+    z = i >> (l0 + l1);
+    return;
+  }
   x = i % n[0];
   const int r = i / n[0];
   y = r % n[1];
@@ -80,6 +94,17 @@ struct ColMap {
 __device__ __forceinline__ ColMap col_map(int nx, int ny, int nz, int tid, int nth) {
   ColMap m;
   const int ncol = nx * ny;
+  if (pow2(nx) && pow2(ny) && pow2(nz) && pow2(nth)) {  // (ncol, nch, per: powers of two)
+    const int lx = lg2(nx), lc = lx + lg2(ny);
+    const int lch = max(0, min(lg2(nz), lg2(nth) - lc));
+    const int col = tid & (ncol - 1), ch = tid >> lc;
+    m.x = col & (nx - 1);
+    m.y = col >> lx;
+    m.z0 = ch << (lg2(nz) - lch);
+    m.z1 = min(nz, m.z0 + (nz >> lch));
+    m.ok = tid < (ncol << lch) && m.z0 < m.z1;
+    return m;
+  }
   const int nch = max(1, min(nz, nth / ncol));
   const int per = (nz + nch - 1) / nch;
   const int col = tid % ncol, ch = tid / ncol;
