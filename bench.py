@@ -202,6 +202,17 @@ def accuracy(solver_args, n, M, seg, buf, K, h, dtype, f_bench, u_bench):
     return out
 
 
+def ref_workload():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world == 1:
+        return ("C3: global 512x512x512 cells (134217728 per GPU), M=8, seg=64, buffer=2, K=4 SR "
+                "levels, F(1,2,2), rhs manufactured+noise, 7pt operator")
+    P = PGRID.get(world, (world, 1, 1))
+    n = (512 * P[0], 512 * P[1], 512 * P[2])
+    return (f"C4: global {n[0]}x{n[1]}x{n[2]} cells (134217728 per GPU), M=8, seg=64, buffer=2, "
+            "K=4 SR levels, F(1,2,2), rhs manufactured, 7pt operator")
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -220,11 +231,9 @@ def run_reference(args):
         "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic ({ORACLE_SAMPLE['rhs']}, seed {W.SEED})",
-        # our arm's workload; every step is a bounded sample of it (same segment grid, K, J)
-        "config": {"workload": "C3: global 512x512x512 cells (134217728 per GPU), M=8, "
-                               "seg=64, buffer=2, K=4 SR levels, F(1,2,2), rhs "
-                               "manufactured+noise, 7pt operator",
-                   "sample": sample_desc()},
+        # our arm's workload (C3 on one GPU, C4 weak scaling on N); every step is a bounded
+        # sample of it on this host (same segment grid, K, J)
+        "config": {"workload": ref_workload(), "sample": sample_desc()},
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle",
                          "sample": sample_desc()},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
