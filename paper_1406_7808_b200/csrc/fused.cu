@@ -1174,7 +1174,8 @@ bool launch_spec(const Lvl& L, const Cheb2Args<T>& a, FusedRhs<T> b, int nst, cu
   //  E = 70 (64^3 segments): 14-row bands; fp64 4 cells per thread (0.77 vs 0.85 ms for 2
   //    bands of 35), fp32 8 cells per thread (finest pair 0.991 vs 1.032 ms for 10 of 4);
   //  E = 38 (32^3): fp64 19-row bands of 3 cells (0.60 ms; 22 of 6: 0.71, 16 of 6: 0.73,
-  //    22 of 8: 0.76), fp32 22 of 8 (0.38; 14 of 8: 0.45, 38 of 8: 0.57);
+  //    22 of 8: 0.76; level 7 per solve, session 2: 19 of 3 0.616-0.631, 19 of 4 0.70-0.71,
+  //    13 of 3 0.67-0.68, 10 of 4 0.60-0.64 ms), fp32 22 of 8 (0.38; 14 of 8: 0.45, 38 of 8: 0.57);
   //  E = 134 (128^3, C5): 14-row bands of 544 threads, one CTA per SM (6-row bands slower);
   //  E = 22 / 14: one band per segment (two bands of 11 / 7 rows: level 6 0.213 -> 0.299 ms,
   //    level 5 0.139 -> 0.158 ms per solve; fp32 likewise slower).
