@@ -262,6 +262,14 @@ sr_status_t sr_fmg_set_host_store(sr_fmg_t *h, void *store);
  * the number of profiled launches of the last solve.  kernel_class -1 disables. */
 sr_status_t sr_fmg_profile_select(sr_fmg_t *h, int32_t kernel_class, int32_t level);
 sr_status_t sr_fmg_profile_read(sr_fmg_t *h, double *ms, double *bytes, int32_t *launches);
+/* Profiling ring (graph solves only): after profile_select and one capturing solve,
+ * profile_ring(h, n) makes graph solve number i (counted from this call) record its
+ * profiled launches into event set i % n, so n solves can run back to back with no host
+ * synchronisation between them; profile_read_slot(h, i, ...) reads set i once they have
+ * completed (same outputs as profile_read).  n = 0 turns the ring off. */
+sr_status_t sr_fmg_profile_ring(sr_fmg_t *h, int32_t nslots);
+sr_status_t sr_fmg_profile_read_slot(sr_fmg_t *h, int32_t slot, double *ms, double *bytes,
+                                     int32_t *launches);
 
 #ifdef __cplusplus
 }

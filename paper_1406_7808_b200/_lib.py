@@ -24,6 +24,7 @@ EXPORTED = [
     "sr_fmg_solve_host", "sr_fmg_set_stream", "sr_fmg_destroy", "sr_fmg_get_info",
     "sr_fmg_last_error", "sr_fmg_kernel_count", "sr_fmg_kernel_name",
     "sr_fmg_debug_level_io", "sr_fmg_debug_op", "sr_fmg_profile_select", "sr_fmg_profile_read",
+    "sr_fmg_profile_ring", "sr_fmg_profile_read_slot",
     "sr_fmg_partition", "sr_fmg_nccl_unique_id", "sr_fmg_host_store_create",
     "sr_fmg_host_store_destroy", "sr_fmg_set_host_store", "sr_fmg_solve_host_async",
     "sr_fmg_synchronize", "sr_fmg_vsolve", "sr_fmg_desc_size",
@@ -118,6 +119,9 @@ def _load():
         "sr_fmg_profile_select": (I32, [P, I32, I32]),
         "sr_fmg_profile_read": (I32, [P, ctypes.POINTER(D), ctypes.POINTER(D),
                                       ctypes.POINTER(I32)]),
+        "sr_fmg_profile_ring": (I32, [P, I32]),
+        "sr_fmg_profile_read_slot": (I32, [P, I32, ctypes.POINTER(D), ctypes.POINTER(D),
+                                           ctypes.POINTER(I32)]),
         "sr_fmg_partition": (I32, [ctypes.POINTER(Desc), ctypes.POINTER(Partition)]),
         "sr_fmg_nccl_unique_id": (I32, [P]),
         "sr_fmg_host_store_create": (P, [I32]),

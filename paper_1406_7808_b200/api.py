@@ -346,6 +346,15 @@ class Solver:
     def profile_select(self, kernel_class: int, level: int):
         check(lib.sr_fmg_profile_select(self._h, kernel_class, level), self._h)
 
+    def profile_ring(self, nslots: int):
+        check(lib.sr_fmg_profile_ring(self._h, int(nslots)), self._h)
+
+    def profile_read_slot(self, slot: int):
+        ms, by, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        check(lib.sr_fmg_profile_read_slot(self._h, int(slot), ctypes.byref(ms), ctypes.byref(by),
+                                           ctypes.byref(n)), self._h)
+        return ms.value, by.value, n.value
+
     def profile_read(self):
         ms, by, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
         check(lib.sr_fmg_profile_read(self._h, ctypes.byref(ms), ctypes.byref(by),

@@ -97,6 +97,8 @@ struct sr_fmg {
   // alternates two staging slots)
   struct GraphEnt {
     cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;     // kept while profiled: the event nodes below live in it
+    std::vector<cudaGraphNode_t> na, nb;  // event-record nodes of prof[i].a / prof[i].b
     const void* f = nullptr;
     void* u = nullptr;
     long long used = 0;
@@ -134,6 +136,11 @@ struct sr_fmg {
   int prof_cls = -1, prof_level = -1;
   std::vector<ProfRec> prof;
   size_t prof_used = 0;
+  // profiling ring (sr_fmg_profile_ring): graph solve i records its profiled launches into
+  // event set i % ring_n, so K solves run back to back and are read after one sync
+  int ring_n = 0;
+  long long ring_pos = 0;
+  std::vector<std::vector<ProfRec>> ring;
   long long workspace = 0;
   std::vector<long long> visits;
   // ---- partition (multi-GPU); world = 1: one block = the whole grid, halo 0
@@ -1555,9 +1562,29 @@ void dev_free(sr_fmg* h, void* p) {
   else cudaFree(p);
 }
 
+void drop_graph(sr_fmg::GraphEnt& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.graph) cudaGraphDestroy(g.graph);
+  g.exec = nullptr;
+  g.graph = nullptr;
+  g.na.clear();
+  g.nb.clear();
+}
+
+void free_ring(sr_fmg* h) {
+  for (auto& set : h->ring)
+    for (auto& r : set) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  h->ring.clear();
+  h->ring_n = 0;
+  h->ring_pos = 0;
+}
+
 void free_all(sr_fmg* h) {
-  for (auto& g : h->graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto& g : h->graphs) drop_graph(g);
+  free_ring(h);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_solve[i]) cudaEventDestroy(h->ev_solve[i]);
@@ -1821,10 +1848,7 @@ sr_status_t sr_fmg_solve(sr_fmg_t* h, const void* f, void* u) {
     ge = &h->graphs[0];
     for (auto& g : h->graphs)
       if (!g.exec || g.used < ge->used) ge = &g;
-    if (ge->exec) {
-      cudaGraphExecDestroy(ge->exec);
-      ge->exec = nullptr;
-    }
+    drop_graph(*ge);
     CU(h, cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
     sr_status_t st = enqueue_solve(h, f, u, h->cap);
     cudaGraph_t g = nullptr;
@@ -1832,12 +1856,51 @@ sr_status_t sr_fmg_solve(sr_fmg_t* h, const void* f, void* u) {
     if (st != SR_OK) return st;
     if (e != cudaSuccess) return fail(h, SR_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&ge->exec, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return fail(h, SR_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g);
+      return fail(h, SR_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    }
+    if (h->prof_used > 0) {  // profiled: find the event-record nodes of every ProfRec
+      size_t nn = 0;
+      CU(h, cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      CU(h, cudaGraphGetNodes(g, nodes.data(), &nn));
+      ge->na.assign(h->prof_used, nullptr);
+      ge->nb.assign(h->prof_used, nullptr);
+      for (cudaGraphNode_t n : nodes) {
+        cudaGraphNodeType ty;
+        cudaEvent_t ev = nullptr;
+        if (cudaGraphNodeGetType(n, &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord ||
+            cudaGraphEventRecordNodeGetEvent(n, &ev) != cudaSuccess)
+          continue;
+        for (size_t i = 0; i < h->prof_used; ++i) {
+          if (h->prof[i].a == ev) ge->na[i] = n;
+          if (h->prof[i].b == ev) ge->nb[i] = n;
+        }
+      }
+      ge->graph = g;
+    } else {
+      cudaGraphDestroy(g);
+    }
     ge->f = f;
     ge->u = u;
   }
   ge->used = ++h->gclock;
+  if (h->ring_n > 0 && ge->graph) {  // this solve's events: ring slot ring_pos % ring_n
+    auto& set = h->ring[(size_t)(h->ring_pos++ % h->ring_n)];
+    while (set.size() < h->prof_used) {
+      ProfRec r{};
+      CU(h, cudaEventCreate(&r.a));
+      CU(h, cudaEventCreate(&r.b));
+      set.push_back(r);
+    }
+    for (size_t i = 0; i < h->prof_used; ++i) {
+      set[i].bytes = h->prof[i].bytes;
+      if (!ge->na[i] || !ge->nb[i]) return fail(h, SR_ERR_CUDA, "profiling ring: event node missing");
+      CU(h, cudaGraphExecEventRecordNodeSetEvent(ge->exec, ge->na[i], set[i].a));
+      CU(h, cudaGraphExecEventRecordNodeSetEvent(ge->exec, ge->nb[i], set[i].b));
+    }
+  }
   CU(h, cudaGraphLaunch(ge->exec, h->stream));
   return SR_OK;
 }
@@ -2107,10 +2170,34 @@ sr_status_t sr_fmg_profile_select(sr_fmg_t* h, int32_t kernel_class, int32_t lev
   if (!h) return fail(nullptr, SR_ERR_INVALID_ARGUMENT, "handle is NULL");
   h->prof_cls = kernel_class;
   h->prof_level = level;
-  for (auto& g : h->graphs) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    g.exec = nullptr;
+  for (auto& g : h->graphs) drop_graph(g);
+  free_ring(h);
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_profile_ring(sr_fmg_t* h, int32_t nslots) {
+  if (!h || nslots < 0) return fail(h, SR_ERR_INVALID_ARGUMENT, "NULL handle or nslots < 0");
+  free_ring(h);
+  h->ring_n = nslots;
+  h->ring.resize((size_t)nslots);
+  return SR_OK;
+}
+
+sr_status_t sr_fmg_profile_read_slot(sr_fmg_t* h, int32_t slot, double* ms, double* bytes,
+                                     int32_t* launches) {
+  if (!h || !ms || !bytes || !launches) return fail(h, SR_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (slot < 0 || slot >= h->ring_n) return fail(h, SR_ERR_INVALID_ARGUMENT, "slot out of range");
+  double t = 0, b = 0;
+  const auto& set = h->ring[(size_t)slot];
+  for (const auto& r : set) {
+    float x = 0;
+    CU(h, cudaEventElapsedTime(&x, r.a, r.b));
+    t += x;
+    b += r.bytes;
   }
+  *ms = t;
+  *bytes = b;
+  *launches = (int32_t)set.size();
   return SR_OK;
 }
 

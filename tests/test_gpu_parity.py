@@ -763,6 +763,35 @@ def test_c5_full_size_linearity_and_scaling():
         assert torch.isfinite(u1).all()
 
 
+def test_profiling_ring_reads_every_step():
+    # bench.py's timed region: profile_select + one capturing solve, then profile_ring(K):
+    # K graph solves back to back, each recording its profiled launches into its own event
+    # set; after one sync every slot holds one step's launches (the same count and bytes as
+    # the per-solve profile_read) and the solution is unchanged
+    from paper_1406_7808_b200 import kernel_names
+    n = (128, 128, 128)
+    f = torch.from_numpy(W.make_rhs("manufactured+noise", n)).cuda()
+    with Solver(n, 6, seg=64, buffer=2, K=2) as s:
+        u = torch.empty_like(f)
+        ref = s.solve(f).clone()
+        s.profile_select(kernel_names().index("k_prolong"), 6)
+        s.solve(f, u)
+        torch.cuda.synchronize()
+        ms1, by1, n1 = s.profile_read()
+        assert n1 >= 1 and ms1 > 0
+        K = 5
+        s.profile_ring(K)
+        for _ in range(K + 2):
+            s.solve(f, u)
+        torch.cuda.synchronize()
+        for i in range(K):
+            ms, by, nl = s.profile_read_slot(i)
+            assert nl == n1 and by == by1 and ms > 0, (i, ms, by, nl)
+        s.profile_ring(0)
+        s.profile_select(-1, -1)
+        assert torch.equal(s.solve(f), ref)
+
+
 # ---- ABI details of SURVEY §8(b): the descriptor's allocator hooks, SR_ERR_NONFINITE ------
 def test_torch_caching_allocator_backs_the_workspace():
     # desc.alloc / desc.free through PyTorch's caching allocator: same results bitwise, the
