@@ -170,6 +170,32 @@ def test_idle_and_conventional_ranks_equal_single_gpu(case):
         s.close()
 
 
+OPS = [
+    # name, n, M, seg, J, K, pgrid, dd_min, extra Solver arguments
+    ("27pt-2x1x1", (64, 32, 32), 5, 16, 2, 2, (2, 1, 1), 0, dict(stencil="27pt", h=2.0 / 64)),
+    ("27pt-dd-2x2x1", (128, 64, 64), 5, 32, 2, 2, (2, 2, 1), 4, dict(stencil="27pt", h=2.0 / 128)),
+    ("nl-2x1x1", (64, 64, 64), 5, 16, 2, 2, (2, 1, 1), 0, dict(nl_gamma=1e4)),
+    ("nl-dd-2x2x2", (128, 128, 128), 6, 32, 2, 2, (2, 2, 2), 4, dict(nl_gamma=1e4)),
+    ("27pt-K0-2x1x1", (64, 32, 32), 5, 0, 0, 0, (2, 1, 1), 4, dict(stencil="27pt", h=2.0 / 64)),
+]
+
+
+@pytest.mark.timeout(150)
+@pytest.mark.parametrize("case", OPS, ids=[c[0] for c in OPS])
+def test_27pt_and_nonlinear_ranks_equal_single_gpu(case):
+    # the NEXT-row operators (f1: 27-point, f4: nonlinear FAS) through the multi-GPU path:
+    # the decomposed levels exchange the ghost ring (edges and corners included, which the
+    # 27-point stencil reads) before every operator application -- bitwise one GPU
+    name, n, M, seg, J, K, pgrid, dd_min, kw = case
+    f = W.make_rhs("manufactured+noise", n, h=kw.get("h"))
+    with Solver(n, M, seg=seg, buffer=J, K=K, **kw) as s1:
+        single = s1.solve(torch.from_numpy(f).cuda()).cpu().numpy()
+    ranks, outs, _ = run_ranks(n, M, seg, J, K, pgrid, f, "f64", dd_min, solves=1, **kw)
+    for r, s in enumerate(ranks):
+        assert np.array_equal(outs[r], s.block_of(single)), (name, r)
+        s.close()
+
+
 @pytest.mark.timeout(150)
 def test_multirank_local_f_uses_halo_only():
     # f outside a rank's haloed block must not matter: perturb it and get the same block
