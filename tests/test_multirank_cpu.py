@@ -116,3 +116,15 @@ def test_partition_blocks_tile_the_grid():
             sl = tuple(slice(lo[2 - d], lo[2 - d] + p["segs_per_rank"][2 - d]) for d in range(3))
             cover[sl] += 1
         assert np.all(cover == 1)
+
+
+def test_rank_blocks_of_every_rhs_kind_equal_the_global_rhs():
+    # bench.py at N > 1 evaluates each rank's haloed f block on its own (W.rhs_block); on the
+    # block's in-domain cells it must equal the global array bitwise
+    n, h = (64, 32, 32), 1.0 / 64
+    lo, dims = (30, -2, 4), (20, 20, 20)
+    for kind in ("manufactured", "bumps", "manufactured+noise"):
+        full = W.make_rhs(kind, n, h=h)
+        blk = W.rhs_block(kind, n, h, lo, dims)
+        assert blk.shape == (20, 20, 20)
+        assert np.array_equal(blk[:, 2:20, :], full[4:24, 0:18, 30:50]), kind

@@ -114,6 +114,33 @@ def gaussian_bumps(n, h, count=16, seed=SEED) -> np.ndarray:
     return f
 
 
+def gaussian_bumps_block(h, lo, dims, count=16, seed=SEED) -> np.ndarray:
+    """gaussian_bumps on the block of cells [lo, lo + dims) (paper order), shape (dims3,
+    dims2, dims1): a multi-GPU rank's (haloed) local block; cells outside the domain are
+    evaluated by the same formula (they are never used)."""
+    g = [(np.arange(lo[d], lo[d] + dims[d], dtype=np.float64) + 0.5) * h for d in range(3)]
+    f = np.zeros((dims[2], dims[1], dims[0]), dtype=np.float64)
+    for c, w, a in gaussian_bumps_params(count, seed):
+        e = [np.exp(-((g[d] - c[d]) ** 2) / (2.0 * w * w)) for d in range(3)]
+        f += a * (e[2][:, None, None] * e[1][None, :, None] * e[0][None, None, :])
+    return f
+
+
+def rhs_block(kind: str, n, h, lo, dims, seed=SEED) -> np.ndarray:
+    """make_rhs(kind, n, h) restricted to the block [lo, lo + dims) (cells outside the
+    domain: the formula's value, or 0 for the sampled noise/random kinds)."""
+    if kind == "manufactured":
+        return manufactured_f_block(h, extents(n, h), lo, dims)
+    if kind == "bumps":
+        return gaussian_bumps_block(h, lo, dims, 16, seed)
+    full = make_rhs(kind, n, h, seed)
+    out = np.zeros((dims[2], dims[1], dims[0]), dtype=np.float64)
+    src = [slice(max(lo[d], 0), min(lo[d] + dims[d], n[d])) for d in range(3)]
+    dst = [slice(src[d].start - lo[d], src[d].stop - lo[d]) for d in range(3)]
+    out[dst[2], dst[1], dst[0]] = full[src[2], src[1], src[0]]
+    return out
+
+
 def random_field(n, seed=SEED, scale=1.0) -> np.ndarray:
     """Plain N(0, scale^2) field (used for operator-level parity inputs)."""
     rng = np.random.Generator(np.random.PCG64(seed))
