@@ -371,9 +371,34 @@ def test_corrections_increment_gsr_cells():
     # between the pre- and post-smoothing of an SR visit every GSR cell changes by exactly
     # P(w - t) (the smoother never touches GSR).  K = 3 covers the k = 1 hand-off (w - t
     # from the conventional level T) and k >= 2 (w - t from the segment's own coarse level).
+    _check_gsr_increments(Oracle)
+
+
+class _CorrectCOnly(Oracle):
+    """Mutant (the other reading SPEC leaves open): the corrections of the SR V-cycle act on
+    C only, so GSR cells stay as the FMG interpolation set them."""
+
+    def vsr(self, l):
+        self._in_vsr = getattr(self, "_in_vsr", 0) + 1
+        try:
+            super().vsr(l)
+        finally:
+            self._in_vsr -= 1
+
+    def CG(self, l, p):  # inside vsr CG is used by the corrections only
+        return self.C(l, p) if getattr(self, "_in_vsr", 0) else super().CG(l, p)
+
+
+def test_gsr_increment_pin_catches_the_correct_on_c_only_mutation():
+    # the pin above is not vacuous: the mutant that corrects C only fails it
+    with pytest.raises(AssertionError):
+        _check_gsr_increments(_CorrectCOnly)
+
+
+def _check_gsr_increments(cls):
     n = (32, 32, 32)
     f = W.make_rhs("manufactured+noise", n)
-    o = Oracle(Config(n=n, M=4, seg=16, buffer=2, K=3))
+    o = cls(Config(n=n, M=4, seg=16, buffer=2, K=3))
     saved, checked, moved = {}, [], [0.0]
 
     def on_cheb(phase, l, p, u, b, X):
@@ -391,7 +416,7 @@ def test_corrections_increment_gsr_cells():
         O.fill_bc_ghosts(e, o.dom[lc])
         stb = o.storage(l, p)
         inc = np.zeros(stb.shape)
-        CG = o.CG(l, p)
+        CG = Oracle.CG(o, l, p)     # the region as defined, not o's
         inc[tuple(slice(a - s, c - s) for a, c, s in zip(CG.lo, CG.hi, stb.lo))] = O.prolong(e, CG)
         got = u.a[m] - saved[(l, p)][m]
         np.testing.assert_allclose(got, inc[m], rtol=0, atol=1e-13 * np.abs(u.a[m]).max())
