@@ -171,23 +171,43 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) u0r[k][0] = u0r[k][1] = u0r[k][2] = u1r[k][0] = u1r[k][1] = u1r[k][2] = T(0);
 
-  // 27-point A at slot k from the plane triple (pm, p0, pp) with z signs (szm, szp)
-  auto A27 = [&](const T* pm, const T* p0, const T* pp, T szm, T szp, int k, T c) -> T {
-    const int o = k * PY;
-    // edges in plane z: (+-1, +-1, 0)
-    const T e0 = (sxm * sym[k]) * p0[o + rym[k] + cxm] + (sxp * sym[k]) * p0[o + rym[k] + cxp] +
-                 (sxm * syp[k]) * p0[o + ryp[k] + cxm] + (sxp * syp[k]) * p0[o + ryp[k] + cxp];
-    // edges (+-1, 0, +-1) and (0, +-1, +-1)
-    const T em = sxm * pm[o + cxm] + sxp * pm[o + cxp] + sym[k] * pm[o + rym[k]] + syp[k] * pm[o + ryp[k]];
-    const T ep = sxm * pp[o + cxm] + sxp * pp[o + cxp] + sym[k] * pp[o + rym[k]] + syp[k] * pp[o + ryp[k]];
-    // corners (+-1, +-1, +-1)
-    const T km = (sxm * sym[k]) * pm[o + rym[k] + cxm] + (sxp * sym[k]) * pm[o + rym[k] + cxp] +
-                 (sxm * syp[k]) * pm[o + ryp[k] + cxm] + (sxp * syp[k]) * pm[o + ryp[k] + cxp];
-    const T kp = (sxm * sym[k]) * pp[o + rym[k] + cxm] + (sxp * sym[k]) * pp[o + rym[k] + cxp] +
-                 (sxm * syp[k]) * pp[o + ryp[k] + cxm] + (sxp * syp[k]) * pp[o + ryp[k] + cxp];
-    const T e = e0 + szm * em + szp * ep;
-    const T kk = szm * km + szp * kp;
-    return (T(8.0 / 3.0) * c - e * T(1.0 / 6.0) - kk * T(1.0 / 12.0)) * ih2;
+  // 27-point A (R28) for all MAXS slots of the thread from the plane triple (pm, p0, pp) with z
+  // signs (szm, szp), sharing the in-plane partial sums between neighbouring slots: per plane
+  // P and row r, the x pair
+  //   H(P, r) = sxm P[r, x-1] + sxp P[r, x+1]
+  // is loaded once (a window over rows k-1, k, k+1 slides down the slots), and
+  //   edges(z)   = sym H(p0, k-1) + syp H(p0, k+1)            (in-plane diagonals)
+  //   edges(z-1) = H(pm, k) + sym pm[k-1] + syp pm[k+1]       (faces of the plane below)
+  //   corners    = sym H(pm, k-1) + syp H(pm, k+1)            (and likewise for pp)
+  //   A u = (8/3 u - (edges)/6 - (corners)/12) / h^2,  face weight 0
+  // -- 8 shared-memory loads per slot instead of 20 for the neighbour-by-neighbour sum (P27:
+  // the finest degree-2 passes 13.8 -> 11.5 ms).  The row index k-1 / k+1 becomes k itself
+  // across a domain face (R3 mirror, sign in sym/syp).
+  auto A27w = [&](const T* pm, const T* p0, const T* pp, T szm, T szp, const T (&cv)[MAXS],
+                  T (&Av)[MAXS]) {
+    auto hs = [&](const T* P, int r) {
+      const int o = r * PY;
+      return sxm * P[o + cxm] + sxp * P[o + cxp];
+    };
+    T h0m = hs(p0, -1), h0c = hs(p0, 0), hmm = hs(pm, -1), hmc = hs(pm, 0);
+    T hpm = hs(pp, -1), hpc = hs(pp, 0);
+    T cmm = pm[-PY], cmc = pm[0], cpm = pp[-PY], cpc = pp[0];
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) {
+      const T h0n = hs(p0, k + 1), hmn = hs(pm, k + 1), hpn = hs(pp, k + 1);
+      const T cmn = pm[(k + 1) * PY], cpn = pp[(k + 1) * PY];
+      const bool ylo = rym[k] == 0, yhi = ryp[k] == 0;
+      const T e0 = sym[k] * (ylo ? h0c : h0m) + syp[k] * (yhi ? h0c : h0n);
+      const T em = hmc + sym[k] * (ylo ? cmc : cmm) + syp[k] * (yhi ? cmc : cmn);
+      const T ep = hpc + sym[k] * (ylo ? cpc : cpm) + syp[k] * (yhi ? cpc : cpn);
+      const T km = sym[k] * (ylo ? hmc : hmm) + syp[k] * (yhi ? hmc : hmn);
+      const T kp = sym[k] * (ylo ? hpc : hpm) + syp[k] * (yhi ? hpc : hpn);
+      const T e = e0 + szm * em + szp * ep;
+      const T kk = szm * km + szp * kp;
+      Av[k] = (T(8.0 / 3.0) * cv[k] - e * T(1.0 / 6.0) - kk * T(1.0 / 12.0)) * ih2;
+      h0m = h0c; h0c = h0n; hmm = hmc; hmc = hmn; hpm = hpc; hpc = hpn;
+      cmm = cmc; cmc = cmn; cpm = cpc; cpc = cpn;
+    }
   };
   // plane pointers of a ring with z mirroring at the domain faces (R3)
   auto triple = [&](const T* base, int ring, int zc, const T*& pm, const T*& p0, const T*& pp,
@@ -218,13 +238,17 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
       T* u1w = u1s + (z % G::R1) * G::PL + po;
       const unsigned act = zc ? c_mask : 0u;
       const unsigned fm = (FIN == 3 && gz >= fz0 && gz < fz1) ? f_mask : 0u;
+      T cv0[MAXS], Av0[MAXS];
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) cv0[k] = p0[k * PY];
+      A27w(pm, p0, pp, szm, szp, cv0, Av0);
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
-        const T v0 = p0[k * PY];
+        const T v0 = cv0[k];
         T r;
         if constexpr (FIN == 3) {
           // tau (Eq. 4, fig:mgvsr L234-236) and the first step's residual rhs - A u0
-          const T Au = A27(pm, p0, pp, szm, szp, k, v0);
+          const T Au = Av0[k];
           const T Rv = fp[k * G::FP];
           const T bv = ((fm >> k) & 1u) ? Rv + Au : Au;
           r = bv - Au;
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
             a.tout[o] = v0;  // t = u0
           }
         } else {
-          r = (nof ? T(0) : fp[k * G::FP]) - A27(pm, p0, pp, szm, szp, k, v0);
+          r = (nof ? T(0) : fp[k * G::FP]) - Av0[k];
         }
         const T v1 = ((act >> k) & 1u) ? v0 + c0 * r : v0;
         if constexpr (FIN == 2) {  // residual mode: r = b - A u0 on C (restriction input)
@@ -275,10 +299,14 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
           const T* fp = fs + (zz % G::RF) * G::FS + fo;
           T* orow = ob + (long long)zz * pz;
           const unsigned act = zc ? c_mask : 0u;
+          T cv1[MAXS], Av1[MAXS];
+#pragma unroll
+          for (int k = 0; k < MAXS; ++k) cv1[k] = u1r[k][J];
+          A27w(pm, p0, pp, szm, szp, cv1, Av1);
 #pragma unroll
           for (int k = 0; k < MAXS; ++k) {
-            const T c1 = u1r[k][J];
-            const T r = fp[k * G::FP] - A27(pm, p0, pp, szm, szp, k, c1);
+            const T c1 = cv1[k];
+            const T r = fp[k * G::FP] - Av1[k];
             const T v2 = ((act >> k) & 1u) ? c1 + cm * (c1 - u0r[k][J]) + cr * r : u0r[k][J];
             if (!((w_mask >> k) & 1u)) continue;
             if constexpr (FIN != 1) {
