@@ -26,10 +26,13 @@ ap.add_argument("--dtype", default="f64")
 ap.add_argument("--what", default="solve", choices=["solve", "cheb", "restrict", "prolong", "correct"])
 ap.add_argument("--graph", type=int, default=1)
 ap.add_argument("--level", type=int, default=-1, help="level of the single operation (default M)")
+ap.add_argument("--stencil", default="7pt")
 a = ap.parse_args()
 n, M, seg, buf, K, rhs = WORKLOADS[a.config]
-s = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=a.dtype, use_graph=bool(a.graph))
-f = torch.from_numpy(W.make_rhs(rhs, n).astype(np.float64 if a.dtype == "f64" else np.float32)).cuda()
+h = 1.0 / n[0] if a.config != "P27" else 2.0 / n[0]
+s = Solver(n, M, seg=seg, buffer=buf, K=K, dtype=a.dtype, use_graph=bool(a.graph), h=h,
+           stencil=a.stencil)
+f = torch.from_numpy(W.make_rhs(rhs, n, h=h).astype(np.float64 if a.dtype == "f64" else np.float32)).cuda()
 u = torch.empty_like(f)
 s.solve(f, u)
 s.solve(f, u)
