@@ -181,13 +181,18 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
   //   corners    = sym H(pm, k-1) + syp H(pm, k+1)            (and likewise for pp)
   //   A u = (8/3 u - (edges)/6 - (corners)/12) / h^2,  face weight 0
   // -- 8 shared-memory loads per slot instead of 20 for the neighbour-by-neighbour sum (P27:
-  // the finest degree-2 passes 13.8 -> 11.5 ms).  The row index k-1 / k+1 becomes k itself
+  // the finest degree-2 passes 13.8 -> 11.5 ms; the interior path below: -> 10.4 ms).  The row index k-1 / k+1 becomes k itself
   // across a domain face (R3 mirror, sign in sym/syp).
-  auto A27w = [&](const T* pm, const T* p0, const T* pp, T szm, T szp, const T (&cv)[MAXS],
-                  T (&Av)[MAXS]) {
+  // INT (a CTA whose cells have no x or y neighbour across a domain face): every sign is +1
+  // and no row is mirrored, so the products and selects drop out -- the same operations on
+  // the same values otherwise (x * 1 exact, fma(1, a, b) = a + b): bitwise the general path
+  auto A27w = [&](auto INTt, const T* pm, const T* p0, const T* pp, T szm, T szp,
+                  const T (&cv)[MAXS], T (&Av)[MAXS]) {
+    constexpr bool INT = decltype(INTt)::value;
     auto hs = [&](const T* P, int r) {
       const int o = r * PY;
-      return sxm * P[o + cxm] + sxp * P[o + cxp];
+      if constexpr (INT) return P[o + cxm] + P[o + cxp];
+      else return sxm * P[o + cxm] + sxp * P[o + cxp];
     };
     T h0m = hs(p0, -1), h0c = hs(p0, 0), hmm = hs(pm, -1), hmc = hs(pm, 0);
     T hpm = hs(pp, -1), hpc = hs(pp, 0);
@@ -196,12 +201,21 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
     for (int k = 0; k < MAXS; ++k) {
       const T h0n = hs(p0, k + 1), hmn = hs(pm, k + 1), hpn = hs(pp, k + 1);
       const T cmn = pm[(k + 1) * PY], cpn = pp[(k + 1) * PY];
-      const bool ylo = rym[k] == 0, yhi = ryp[k] == 0;
-      const T e0 = sym[k] * (ylo ? h0c : h0m) + syp[k] * (yhi ? h0c : h0n);
-      const T em = hmc + sym[k] * (ylo ? cmc : cmm) + syp[k] * (yhi ? cmc : cmn);
-      const T ep = hpc + sym[k] * (ylo ? cpc : cpm) + syp[k] * (yhi ? cpc : cpn);
-      const T km = sym[k] * (ylo ? hmc : hmm) + syp[k] * (yhi ? hmc : hmn);
-      const T kp = sym[k] * (ylo ? hpc : hpm) + syp[k] * (yhi ? hpc : hpn);
+      T e0, em, ep, km, kp;
+      if constexpr (INT) {
+        e0 = h0m + h0n;
+        em = hmc + cmm + cmn;
+        ep = hpc + cpm + cpn;
+        km = hmm + hmn;
+        kp = hpm + hpn;
+      } else {
+        const bool ylo = rym[k] == 0, yhi = ryp[k] == 0;
+        e0 = sym[k] * (ylo ? h0c : h0m) + syp[k] * (yhi ? h0c : h0n);
+        em = hmc + sym[k] * (ylo ? cmc : cmm) + syp[k] * (yhi ? cmc : cmn);
+        ep = hpc + sym[k] * (ylo ? cpc : cpm) + syp[k] * (yhi ? cpc : cpn);
+        km = sym[k] * (ylo ? hmc : hmm) + syp[k] * (yhi ? hmc : hmn);
+        kp = sym[k] * (ylo ? hpc : hpm) + syp[k] * (yhi ? hpc : hpn);
+      }
       const T e = e0 + szm * em + szp * ep;
       const T kk = szm * km + szp * kp;
       Av[k] = (T(8.0 / 3.0) * cv[k] - e * T(1.0 / 6.0) - kk * T(1.0 / 12.0)) * ih2;
@@ -209,6 +223,11 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
       cmm = cmc; cmc = cmn; cpm = cpc; cpc = cpn;
     }
   };
+  // CTA-uniform: no thread column (x, all of the row pitch) and no thread row (y) is a domain
+  // boundary cell, i.e. the box [ox, ox + PY) x [oy + s0, oy + s0 + TR) lies within the
+  // cells 1 .. N - 2 (z is per plane: szm / szp)
+  const bool interior = ox >= 1 && ox + PY <= L.N[0] - 1 && oy + s0 >= 1 &&
+                        oy + s0 + G::TR <= L.N[1] - 1;
   // plane pointers of a ring with z mirroring at the domain faces (R3)
   auto triple = [&](const T* base, int ring, int zc, const T*& pm, const T*& p0, const T*& pp,
                     T& szm, T& szp) {
@@ -241,7 +260,8 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
       T cv0[MAXS], Av0[MAXS];
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) cv0[k] = p0[k * PY];
-      A27w(pm, p0, pp, szm, szp, cv0, Av0);
+      if (interior) A27w(std::true_type{}, pm, p0, pp, szm, szp, cv0, Av0);
+      else A27w(std::false_type{}, pm, p0, pp, szm, szp, cv0, Av0);
 #pragma unroll
       for (int k = 0; k < MAXS; ++k) {
         const T v0 = cv0[k];
@@ -302,7 +322,8 @@ __global__ void __launch_bounds__(G27<T, PY, BH, MAXS, RG>::NT, G27<T, PY, BH, M
           T cv1[MAXS], Av1[MAXS];
 #pragma unroll
           for (int k = 0; k < MAXS; ++k) cv1[k] = u1r[k][J];
-          A27w(pm, p0, pp, szm, szp, cv1, Av1);
+          if (interior) A27w(std::true_type{}, pm, p0, pp, szm, szp, cv1, Av1);
+          else A27w(std::false_type{}, pm, p0, pp, szm, szp, cv1, Av1);
 #pragma unroll
           for (int k = 0; k < MAXS; ++k) {
             const T c1 = cv1[k];
