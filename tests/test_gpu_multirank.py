@@ -33,6 +33,9 @@ def run_ranks(n, M, seg, J, K, pgrid, f, dtype="f64", dd_min=0, solves=1, **kw):
     ranks = [Solver(n, M, seg=seg, buffer=J, K=K, dtype=dtype, world=world, rank=r, pgrid=pgrid,
                     host_store=store, dd_min=dd_min, **kw) for r in range(world)]
     fl = [torch.from_numpy(s.local_f(f)).cuda() for s in ranks]
+    # the ranks solve on streams of their own: the inputs' copies (default stream) must have
+    # landed first (a pageable host-to-device copy can return before it has)
+    torch.cuda.synchronize()
     outs, errs = [None] * world, []
 
     def work(r):

@@ -608,6 +608,7 @@ def test_c4_ranks_full_size_equal_single_gpu(world, dd_min):
             dims = [s.block_n[d] + 2 * s.f_halo for d in range(3)]
             fl = torch.from_numpy(W.manufactured_f_block(h, R, lo, dims)).cuda()
             st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())  # the input copy before the solve
             with torch.cuda.stream(st):
                 outs[r] = s.solve(fl).cpu()
             st.synchronize()

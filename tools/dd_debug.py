@@ -40,6 +40,7 @@ ranks = [Solver(n, a.M, seg=a.seg, buffer=a.J, K=a.K, dtype=a.dtype, world=world
                 pgrid=pg, host_store=store, dd_min=a.dd_min, coarse_idle=bool(a.idle)) for r in range(world)]
 print("A", ranks[0].level_A, "T", ranks[0].T, "dd", ranks[0].dd_levels(), flush=True)
 fl = [torch.from_numpy(s.local_f(f)).cuda() for s in ranks]
+torch.cuda.synchronize()  # the rank threads solve on streams of their own
 outs = [None] * world
 
 
